@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the arrow-decomposition SpMM hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config R] [--k 128] [--dtype f32]
+    python bench.py --impl reference ...        # the oracle (O1, CPU) on the same workload
+
+Metric (BASELINE.json): "SpMM GFLOP/s and HBM-roofline % at 1/2/4/8 B200 (k=32,128)".
+A step = one arrow_spmm(plan, X, Y, k) = every §8(a) row (head stage, body rows + head
+slices, head epilogue, per level) over the whole synthetic input; FLOP = 2 nnz k.
+Workload at N=1: config R = RMAT(22,8,1) (65.2M nnz), b = 16384, k = 128, fp32 -- the
+configuration BASELINE.json's target is quoted on.  X and Y are 2 GiB each (> L2), so
+consecutive steps need no L2 flush.  Timing: CUDA events on the launching stream, W warm-up
+steps, barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+CONFIGS = {
+    "T": dict(graph="RMAT(12,4,1)", b=256, k=16, dtype="f64"),
+    "G": dict(graph="GRID(1024,1)", b=4096, k=32, dtype="f32"),
+    "R": dict(graph="RMAT(22,8,1)", b=16384, k=128, dtype="f32"),
+    "S20": dict(graph="RMAT(20,8,1)", b=4096, k=128, dtype="f32"),
+    "S21": dict(graph="RMAT(21,8,1)", b=8192, k=128, dtype="f32"),
+    "S23": dict(graph="RMAT(23,8,1)", b=32768, k=128, dtype="f32"),
+    "S24": dict(graph="RMAT(24,8,1)", b=65536, k=128, dtype="f32"),
+    "W": dict(graph="WEB(24,1)", b=65536, k=32, dtype="f32"),
+}
+METRIC = "SpMM GFLOP/s and HBM-roofline % at 1/2/4/8 B200 (k=32,128)"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def load_traffic(config, k, dtype):
+    """ncu-measured DRAM bytes per step of the dominant kernel, from a committed summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(f"{config}:k{k}:{dtype}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled every 20 ms while running."""
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for name, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": sorted(self.reasons)}
+
+
+def make_inputs(cfg, k, dtype):
+    g = datagen.make_graph(cfg["graph"])
+    X = datagen.make_x(g.n, k, dtype=np.float64 if dtype == "f64" else np.float32)
+    return g, X
+
+
+def cpu_oracle_baseline(g, X, k, budget_s=12.0, max_reps=10):
+    """O1 (oracle/spmm_ref.c, fp64, OpenMP over rows) on the host cores: full SpMMs repeated
+    until ~budget_s of CPU work (bounded sample of the same workload)."""
+    import oracle
+    threads = oracle.num_threads()
+    oracle.spmm(g.n, g.row_ptr, g.col, g.val, X[: min(g.n, 1024)] if False else X)  # warm-up (page-in)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_reps and (time.perf_counter() - t_all) < budget_s:
+        t0 = time.perf_counter()
+        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    gflops = 2.0 * g.nnz * k / t / 1e9
+    return {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{len(times)} full SpMMs Y=AX of the same A and X in fp64 (median {t:.3f} s each, "
+                      f"1 warm-up), oracle/spmm_ref.c with OpenMP over rows"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle as it stands, on this arm's config and metric (rank 0 only)."""
+    if rank != 0:
+        return
+    k, dtype = args.k or cfg["k"], args.dtype or cfg["dtype"]
+    g, X = make_inputs(cfg, k, dtype)
+    import oracle
+    threads = oracle.num_threads()
+    oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)  # page-in
+    times = []
+    for _ in range(args.warmup):
+        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    flop = 2.0 * g.nnz * k
+    val = flop / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}", "n": g.n, "nnz": g.nnz,
+                   "k": k, "b": cfg["b"]},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+                         "sample": f"each step = one full fp64 SpMM of the workload on the host (oracle/spmm_ref.c)"},
+        "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="R", choices=sorted(CONFIGS))
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--dtype", default="", choices=["", "f32", "f64"])
+    ap.add_argument("--impl", default="arrow", choices=["arrow", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--window-rows", type=int, default=0)
+    ap.add_argument("--head-chunk", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2402_19364_b200 as ab
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    k, dtype = args.k or cfg["k"], args.dtype or cfg["dtype"]
+    es = 8 if dtype == "f64" else 4
+    g, X = make_inputs(cfg, k, dtype)
+
+    comm = None
+    if world > 1:
+        uid = [ab.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = ab.Comm(world, rank, uid[0])
+    plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm,
+                   window_rows=args.window_rows, head_chunk=args.head_chunk)
+    info = plan.info()
+    lo, hi = plan.local_begin, plan.local_end
+    if comm is not None:
+        perm0 = plan.export_level(0)[0]
+        Xl = X[perm0[lo:hi]]
+    else:
+        Xl = X
+    plan.reserve(k)
+    stream = torch.cuda.Stream(dev)
+    Xd = torch.from_numpy(np.ascontiguousarray(Xl)).to(dev)
+    Yd = torch.empty_like(Xd)
+    torch.cuda.synchronize()
+
+    def step():
+        plan.spmm_ptr(Xd.data_ptr(), Yd.data_ptr(), k, stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    plan.set_profiling(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    kt = plan.kernel_times()
+    plan.set_profiling(False)
+    t_tensor = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t_tensor.item()) / args.steps
+
+    flop = 2.0 * g.nnz * k
+    gflops = flop / (ms_per_step * 1e-3) / 1e9
+    b_alg = plan.bytes_alg(k)
+
+    # dominant kernel (K-A segment stream): algorithmic bytes of its launches per step
+    s = es
+    ka_bytes = 0
+    ka_launches = 0
+    for i in range(info["levels"] + (1 if info["residual_nnz"] else 0)):
+        li = plan.level_info(i)
+        y_rows = (li["rows"] - li["head"]) if i == 0 else 2 * (li["n_i"] - li["head"])
+        ka_bytes += li["nnz"] * (s + 4) + (li["rows"] + 1) * 8 + li["rows"] * 4 + li["n_i"] * k * s + y_rows * k * s
+        ka_launches += 1
+    ka_ms_per_step = kt["segments"]["ms"] / max(1, kt["calls"])
+    peak, peak_src = load_peaks()
+    achieved = ka_bytes / (ka_ms_per_step * 1e-3) / 1e9
+    step_share = ka_ms_per_step / ms_per_step
+
+    # e2e: the same call with HOST buffers (H2D of X, D2H of Y inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        Xh = torch.from_numpy(np.ascontiguousarray(Xl)).pin_memory()
+        Yh = torch.empty_like(Xh).pin_memory()
+        Xh_np, Yh_np = Xh.numpy(), Yh.numpy()
+        plan.spmm_host(Xh_np, Yh_np, stream.cuda_stream)  # warm (allocates staging)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.spmm_host(Xh_np, Yh_np, stream.cuda_stream)
+        te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(flop / float(te.item()) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(Xl.nbytes) * world, "d2h_bytes_per_step": int(Xl.nbytes) * world,
+               "ms_per_step": round(float(te.item()) * 1e3, 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(g, X, k)
+
+    if rank == 0:
+        traffic = load_traffic(args.config, k, dtype)
+        line = {
+            "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}",
+                       "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
+                       "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
+                       "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},
+            "hbm_roofline": {"bytes_alg_per_step": b_alg, "achieved_GBs": round(b_alg / (ms_per_step * 1e-3) / 1e9, 1),
+                             "frac_of_measured": round(b_alg / (ms_per_step * 1e-3) / 1e9 / peak, 4),
+                             "frac_of_8TBs": round(b_alg / (ms_per_step * 1e-3) / 8e12, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k_segments (K-A)",
+                         "bytes_per_step": ka_bytes, "launches_per_step": ka_launches,
+                         "ms_per_step": round(ka_ms_per_step, 4), "share_of_step": round(step_share, 4),
+                         "peak_source": peak_src},
+            "kernel_ms_per_step": {kname: round(kt[kname]["ms"] / max(1, kt["calls"]), 4)
+                                   for kname in ("head_stage", "segments", "head_epilogue", "comm")},
+            "gpu_launches": int(sum(kt[kname]["launches"] for kname in ("head_stage", "segments", "head_epilogue"))),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "create_seconds": round(info["create_seconds"], 2),
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

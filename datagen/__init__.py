@@ -58,6 +58,8 @@ def lib():
             L.dg_values.argtypes = [p, p, i64, u64, p]
             L.dg_fill_x.argtypes = [i64, i64, i64, u64, p]
             L.dg_fill_x_f32.argtypes = [i64, i64, i64, u64, p]
+            L.dg_canonicalize.argtypes = [i64, i64, p, p, p, p]
+            L.dg_canonicalize.restype = i64
             for f in (L.dg_splitmix64, L.dg_scramble_keys, L.dg_rmat_edges, L.dg_values,
                       L.dg_fill_x, L.dg_fill_x_f32):
                 f.restype = None
@@ -132,6 +134,16 @@ def path_edges(n: int, s: int | None):
 def canonicalize(n: int, u, v):
     """Drop self-loops, merge duplicate undirected edges, store both (a,b) and (b,a),
     sort rows and columns.  Returns (row_ptr int64[n+1], col int32[nnz])."""
+    u = np.ascontiguousarray(u, dtype=np.int64)
+    v = np.ascontiguousarray(v, dtype=np.int64)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    col = np.empty(2 * len(u), dtype=np.int32)
+    nnz = lib().dg_canonicalize(n, len(u), _ptr(u), _ptr(v), _ptr(row_ptr), _ptr(col))
+    return row_ptr, col[:nnz].copy()
+
+
+def canonicalize_np(n: int, u, v):
+    """numpy rendering of canonicalize (cross-check in tests)."""
     u = np.asarray(u, dtype=np.int64)
     v = np.asarray(v, dtype=np.int64)
     keep = u != v

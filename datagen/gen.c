@@ -85,3 +85,57 @@ void dg_fill_x_f32(int64_t r0, int64_t r1, int64_t k, uint64_t s_x, float *out) 
             out[(i - r0) * k + j] = (float)((double)(h >> 48) / 65536.0);
         }
 }
+
+/* ---------------------------------------------------------------- canonical CSR
+ * Drop self-loops, merge duplicate undirected edges, store both (a,b) and (b,a), rows and
+ * columns sorted.  keys = (min << 32 | max) sorted by an LSD radix sort (16-bit digits),
+ * deduplicated; a sequential scan in (lo, hi) order then fills every row in ascending column
+ * order (entries c < r arrive from keys (c, r) before the keys (r, c') with c' > r). */
+#include <stdlib.h>
+#include <string.h>
+
+static void radix_sort_u64(uint64_t *a, uint64_t *tmp, int64_t m, int bits) {
+    int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * 65536);
+    for (int shift = 0; shift < bits; shift += 16) {
+        memset(cnt, 0, sizeof(int64_t) * 65536);
+        for (int64_t i = 0; i < m; ++i) cnt[(a[i] >> shift) & 0xFFFF]++;
+        int64_t s = 0;
+        for (int d = 0; d < 65536; ++d) { int64_t c = cnt[d]; cnt[d] = s; s += c; }
+        for (int64_t i = 0; i < m; ++i) tmp[cnt[(a[i] >> shift) & 0xFFFF]++] = a[i];
+        uint64_t *t = a; a = tmp; tmp = t;
+        memcpy(tmp, a, sizeof(uint64_t) * m);  /* keep result in both buffers */
+    }
+    free(cnt);
+}
+
+/* returns nnz (stored entries); row_ptr[n+1] filled; col must have room for 2*m entries */
+int64_t dg_canonicalize(int64_t n, int64_t m, const int64_t *u, const int64_t *v, int64_t *row_ptr, int32_t *col) {
+    uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (m > 0 ? m : 1));
+    uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * (m > 0 ? m : 1));
+    int64_t k = 0;
+    for (int64_t e = 0; e < m; ++e) {
+        uint64_t a = (uint64_t)u[e], b = (uint64_t)v[e];
+        if (a == b) continue;
+        uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+        keys[k++] = (lo << 32) | hi;
+    }
+    int bits = 32;
+    while (bits < 64 && (((uint64_t)n - 1) >> (bits - 32)) != 0) bits += 1;
+    bits = ((bits + 15) / 16) * 16;
+    radix_sort_u64(keys, tmp, k, bits);
+    int64_t w = 0;
+    for (int64_t i = 0; i < k; ++i)
+        if (i == 0 || keys[i] != keys[i - 1]) keys[w++] = keys[i];
+    for (int64_t r = 0; r <= n; ++r) row_ptr[r] = 0;
+    for (int64_t i = 0; i < w; ++i) { row_ptr[(keys[i] >> 32) + 1]++; row_ptr[(keys[i] & 0xFFFFFFFFu) + 1]++; }
+    for (int64_t r = 0; r < n; ++r) row_ptr[r + 1] += row_ptr[r];
+    int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    for (int64_t r = 0; r < n; ++r) cur[r] = row_ptr[r];
+    for (int64_t i = 0; i < w; ++i) {
+        int64_t lo = (int64_t)(keys[i] >> 32), hi = (int64_t)(keys[i] & 0xFFFFFFFFu);
+        col[cur[lo]++] = (int32_t)hi;
+        col[cur[hi]++] = (int32_t)lo;
+    }
+    free(cur); free(keys); free(tmp);
+    return row_ptr[n];
+}

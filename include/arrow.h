@@ -1,0 +1,234 @@
+/* include/arrow.h -- C ABI of the B200 arrow-decomposition SpMM library (libarrow_b200.so).
+ *
+ * The one operation: Y = A X for a sparse n x n matrix A with a symmetric pattern and a
+ * tall-skinny dense X (n x k), evaluated through an arrow matrix decomposition
+ *
+ *     A X = sum_i P_{pi_i} ( B_i ( P_{pi_i}^T X ) )                    PAPER.md Eq. (1)
+ *
+ * where every B_i has arrow-width b: nonzeros only in the first b rows/columns or in
+ * the b x b diagonal tiles (block-diagonal band of §4.1).  The
+ * decomposition (LA-Decompose with random-spanning-forest arrangements, §5.1/§5.3/
+ * §5.4) is host preprocessing done once in arrow_plan_create; arrow_spmm is
+ * the per-iteration hot path (the paper's setting T >> 1) and runs entirely in
+ * hand-written sm_100a CUDA kernels on the caller's stream.  There is no CPU fallback:
+ * without a usable CUDA device every call that needs one returns ARROW_E_CUDA.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns arrow_status; nothing throws or aborts across the boundary.
+ *     A human-readable detail of the last failure on this thread: arrow_last_error().
+ *   - Host inputs are borrowed for the duration of the call and deep-copied.
+ *   - A plan owns all its device memory; it is bound to the device current at creation.
+ *   - Numbering is 0-based; positions [0, b) of every level are its head (R2).
+ *
+ * Readings of the paper used by the boundary are listed in DESIGN.md §3 (R1-R23).
+ */
+#ifndef ARROW_B200_H
+#define ARROW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ARROW_ABI_VERSION 1
+
+typedef enum {
+    ARROW_OK = 0,
+    ARROW_E_INVALID_ARG = 1,    /* null pointer, b < 2, levels < 0, k < 0, bad dtype/option, aliasing */
+    ARROW_E_BAD_CSR = 2,        /* row_ptr not 0-based/nondecreasing, col out of [0,n), unsorted or duplicate columns */
+    ARROW_E_NOT_SYMMETRIC = 3,  /* pattern of A is not symmetric (§2: undirected G) */
+    ARROW_E_LEVELS = 4,         /* `levels` cap reached with entries left and residual mode is ERROR */
+    ARROW_E_CUDA = 5,           /* no device / launch / allocation / asynchronous CUDA error; plan unusable */
+    ARROW_E_NCCL = 6,           /* NCCL failure (distributed mode) */
+    ARROW_E_NOMEM = 7,          /* host allocation failed */
+    ARROW_E_STATE = 8,          /* wrong device current, plan poisoned, collective misuse */
+    ARROW_E_UNSUPPORTED = 9     /* size beyond the implementation's index widths, feature not built */
+} arrow_status;
+
+typedef enum { ARROW_F32 = 0, ARROW_F64 = 1 } arrow_dtype;
+
+/* Canonical CSR of A, host memory, borrowed.  row_ptr[0] = 0, nondecreasing,
+ * row_ptr[n] = nnz; col_idx in [0, n), strictly increasing within each row (no
+ * duplicates); values[nnz] of `dtype`.  Self-loops are allowed (they land in the head
+ * or their diagonal tile, R21).  The PATTERN must be symmetric; values need not be. */
+typedef struct {
+    int64_t n;
+    int64_t nnz;
+    const int64_t *row_ptr;     /* [n + 1] */
+    const int32_t *col_idx;     /* [nnz]   */
+    const void *values;         /* [nnz] of dtype */
+    arrow_dtype dtype;
+} arrow_csr;
+
+typedef struct arrow_plan_s *arrow_plan;
+typedef struct arrow_comm_s *arrow_comm;
+
+enum { ARROW_ORDER_ORIGINAL = 0,   /* X, Y rows in A's vertex order (default; R18) */
+       ARROW_ORDER_PERMUTED = 1 }; /* X, Y rows in pi_0 order: row p holds vertex perm_0[p] */
+enum { ARROW_RESIDUAL_ERROR = 0,   /* levels cap hit with entries left -> ARROW_E_LEVELS */
+       ARROW_RESIDUAL_CSR = 1 };   /* keep the leftover entries as one unstructured CSR level */
+
+typedef struct {
+    arrow_dtype compute;        /* element type of X, Y and the stored values; default = A's dtype.
+                                   fp64 -> fp32 conversion of values rounds to nearest. */
+    uint64_t seed;              /* s_decomp of the random spanning forests (R9); default 4 */
+    int32_t order;              /* ARROW_ORDER_*; default ORIGINAL.  Distributed mode forces PERMUTED. */
+    int32_t residual;           /* ARROW_RESIDUAL_*; default ERROR */
+    int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (65536) */
+    int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (256) */
+    int32_t reserved[7];
+} arrow_options;
+
+/* Fill *opt with the defaults above (compute = ARROW_F32 until a CSR is seen: callers that
+ * want "same as A" leave compute = -1 after this call, which is what the default sets). */
+arrow_status arrow_options_default(arrow_options *opt);
+
+typedef struct arrow_decomposition_s *arrow_decomposition;
+
+/* ---------------------------------------------------------------- north-star trio */
+
+/* Decompose A (LA-Decompose; pruning P:809; random MSF arrangement P:887-896;
+ * smallest-first tree order P:900/P:931; block-diagonal extraction P:467/P:473) with arrow
+ * width b >= 2 and at most `levels` arrow matrices (0 = no cap: loop until the remainder is
+ * empty, R7), then build and upload the device layout.  Validation order: arguments,
+ * canonical CSR, pattern symmetry, decomposition, device allocation.  On any error *out is
+ * set to NULL and nothing leaks.  The plan binds to the current CUDA device. */
+arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, arrow_plan *out);
+
+/* Y = A X.  X, Y: DEVICE pointers on the plan's device, row-major n x k (leading dimension k),
+ * of the plan's dtype, not overlapping (ARROW_E_INVALID_ARG).  Y is fully overwritten
+ * (zero rows included).  Stream-ordered on the plan's stream (default: the legacy default
+ * stream; see arrow_plan_set_stream); returns after enqueue.  Asynchronous faults surface at
+ * the caller's next synchronisation and poison the plan (ARROW_E_CUDA).  k = 0 is a no-op.
+ * Workspaces are sized for the largest k seen; call arrow_plan_reserve before graph capture. */
+arrow_status arrow_spmm(arrow_plan plan, const void *X, void *Y, int64_t k);
+
+/* Synchronises the plan's device work, frees everything.  NULL is a no-op. */
+arrow_status arrow_plan_destroy(arrow_plan plan);
+
+/* ---------------------------------------------------------------- extended */
+
+/* As arrow_plan_create with options; comm != NULL selects distributed mode (one process per
+ * GPU, every rank passes the same A, b, levels and options; see arrow_comm_create). */
+arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels,
+                                  const arrow_options *opt, arrow_comm comm, arrow_plan *out);
+
+/* `stream` is a cudaStream_t (NULL = legacy default stream). */
+arrow_status arrow_plan_set_stream(arrow_plan plan, void *stream);
+
+/* arrow_spmm on an explicit stream. */
+arrow_status arrow_spmm_ex(arrow_plan plan, const void *X, void *Y, int64_t k, void *stream);
+
+/* End-to-end call with HOST buffers: copies X (n x k, plan dtype; pinned memory recommended)
+ * to the device, runs arrow_spmm, copies Y back, and synchronises `stream` before returning.
+ * Device staging buffers are owned by the plan and reused. */
+arrow_status arrow_spmm_host(arrow_plan plan, const void *X_host, void *Y_host, int64_t k, void *stream);
+
+/* Pre-size the k-dependent workspaces (head block D0, head accumulator C0) for k <= k_max so
+ * that later arrow_spmm calls allocate nothing (CUDA-graph capture safe). */
+arrow_status arrow_plan_reserve(arrow_plan plan, int64_t k_max);
+
+typedef struct {
+    int64_t n, nnz, b;
+    int32_t levels;             /* number of arrow matrices (order of the decomposition) */
+    int32_t dtype;              /* arrow_dtype */
+    int32_t order;              /* ARROW_ORDER_* */
+    int32_t distributed;        /* 1 if built with a comm */
+    int64_t residual_nnz;       /* entries in the residual CSR level (0 unless RESIDUAL_CSR) */
+    int64_t sum_rows;           /* sum_i n_i */
+    int64_t isolated;           /* vertices with no entry in A (level-0 zero rows) */
+    double create_seconds;      /* wall time of decomposition + layout build + upload */
+    /* algorithmic bytes per SpMM (from the [iffalse] IO lemma P:1061-1066):
+     *   B_alg(k) = bytes_alg_fixed + bytes_alg_rows * k * sizeof(dtype)                      */
+    int64_t bytes_alg_fixed;    /* sum_i nnz_i (s+4) + (rows_i+1) 8 + rows_i 4 */
+    int64_t bytes_alg_rows;     /* sum_i cols_i + n + sum_{i>=1} 2 n_i  (rows moved per unit k*s) */
+    int64_t device_bytes;       /* device memory held by the plan (excluding k workspaces) */
+    int64_t reserved[8];
+} arrow_plan_info_t;
+
+arrow_status arrow_plan_info(arrow_plan plan, arrow_plan_info_t *info);
+
+typedef struct {
+    int64_t rows;               /* n for level 0 (A-isolated vertices appended as empty rows), n_i otherwise */
+    int64_t n_i;                /* vertices with an entry in A_i (R8) */
+    int64_t head;               /* h_i = min(b, n_i) */
+    int64_t nnz;                /* entries of B_i */
+    int64_t head_nnz;           /* entries in the head rows [0, h_i) */
+    int64_t tiles;              /* ceil(n_i / b) */
+    int64_t segments;           /* device work segments of this level */
+    int64_t reserved[4];
+} arrow_level_info_t;
+
+arrow_status arrow_plan_level_info(arrow_plan plan, int32_t level, arrow_level_info_t *info);
+
+/* Canonical B_i in positions (for bit-exact structure parity): perm[rows] = original vertex at
+ * each position (pi_i^{-1}), row_ptr[rows+1], col[nnz] positions sorted within each row,
+ * val[nnz] of the plan's dtype.  Any output pointer may be NULL to skip it.  Host memory. */
+arrow_status arrow_plan_export_level(arrow_plan plan, int32_t level, int32_t *perm, int64_t *row_ptr,
+                                     int32_t *col, void *val);
+
+/* Distributed mode: this rank's contiguous pi_0-order row range [begin, end) of X and Y. */
+arrow_status arrow_plan_local_rows(arrow_plan plan, int64_t *begin, int64_t *end);
+
+/* Per-kernel device time accumulated with CUDA events on the launching stream while profiling
+ * is on (arrow_plan_set_profiling).  Index by arrow_kernel_id. */
+enum { ARROW_K_HEAD_STAGE = 0,  /* S0: D0 = X[head], C0 = 0 */
+       ARROW_K_SEGMENTS = 1,    /* S1+S2: body rows and head slices (the dominant kernel) */
+       ARROW_K_HEAD_EPI = 2,    /* S3: Y[head] (=|+=) C0 */
+       ARROW_K_COMM = 3,        /* S6: NCCL calls + pack/unpack (distributed) */
+       ARROW_K_COUNT = 4 };
+typedef struct {
+    double ms[ARROW_K_COUNT];
+    int64_t launches[ARROW_K_COUNT];
+    int64_t calls;              /* arrow_spmm calls profiled */
+} arrow_kernel_times_t;
+
+arrow_status arrow_plan_set_profiling(arrow_plan plan, int32_t on);   /* on: resets the counters */
+arrow_status arrow_plan_kernel_times(arrow_plan plan, arrow_kernel_times_t *out); /* synchronises */
+
+/* ---------------------------------------------------------------- host decomposition object
+ * The preprocessing half of arrow_plan_create, exposed so that a decomposition can be computed
+ * once, checked, saved and shared (every rank of a distributed run can load the same file).
+ * Host only: no CUDA device is needed for these calls. */
+
+/* LA-Decompose of A (same algorithm and readings as arrow_plan_create).  keep_residual != 0
+ * keeps entries left at the `levels` cap instead of failing with ARROW_E_LEVELS. */
+arrow_status arrow_decompose(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                             arrow_decomposition *out);
+/* n, b, order (number of arrow matrices), residual entries; any pointer may be NULL. */
+arrow_status arrow_decomposition_info(arrow_decomposition d, int64_t *n, int64_t *b, int32_t *levels,
+                                      int64_t *residual_nnz);
+arrow_status arrow_decomposition_level_info(arrow_decomposition d, int32_t level, arrow_level_info_t *info);
+/* Canonical B_i in positions (see arrow_plan_export_level); values as fp64 (exact for fp32/fp64 A). */
+arrow_status arrow_decomposition_export_level(arrow_decomposition d, int32_t level, int32_t *perm, int64_t *row_ptr,
+                                              int32_t *col, double *val);
+/* Residual entries (original ids, CSR order): u[r], v[r], val[r]. */
+arrow_status arrow_decomposition_export_residual(arrow_decomposition d, int32_t *u, int32_t *v, double *val);
+/* Versioned little-endian binary file with a 64-bit FNV-1a checksum; load verifies it. */
+arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path);
+arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out);
+arrow_status arrow_decomposition_destroy(arrow_decomposition d);
+/* Build a device plan from a decomposition (options as arrow_plan_create_ex; opt->seed and the
+ * residual mode are taken from the decomposition). */
+arrow_status arrow_plan_create_from(arrow_decomposition d, const arrow_options *opt, arrow_comm comm, arrow_plan *out);
+
+/* ---------------------------------------------------------------- distributed (NCCL) */
+/* One process per GPU.  Rank 0 calls arrow_comm_unique_id and shares the 128 bytes (e.g.
+ * torch.distributed.broadcast_object_list); every rank then calls arrow_comm_create with its
+ * device current.  Collectives: per-level broadcast of the head block and reduction of the
+ * head partials (Alg. 1), plus the inter-level exchange of moved rows (Alg. 2,
+ * P:484-499). */
+arrow_status arrow_comm_unique_id(uint8_t id[128]);
+arrow_status arrow_comm_create(int32_t nranks, int32_t rank, const uint8_t id[128], arrow_comm *out);
+arrow_status arrow_comm_destroy(arrow_comm comm);
+
+/* ---------------------------------------------------------------- diagnostics */
+const char *arrow_status_string(arrow_status s);
+const char *arrow_last_error(void);          /* thread-local detail of the last failure ("" if none) */
+int32_t arrow_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARROW_B200_H */

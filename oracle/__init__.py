@@ -48,7 +48,7 @@ def build_lib(force: bool = False) -> str:
     if force or not os.path.exists(_LIBPATH) or os.path.getmtime(_LIBPATH) < os.path.getmtime(src):
         os.makedirs(os.path.dirname(_LIBPATH), exist_ok=True)
         tmp = _LIBPATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O3", "-march=native", "-fno-fast-math", "-fopenmp",
+        subprocess.check_call(["gcc", "-O3", "-fno-fast-math", "-fopenmp",
                                "-shared", "-fPIC", src, "-o", tmp])
         os.replace(tmp, _LIBPATH)
     return _LIBPATH

@@ -1,0 +1,852 @@
+// arrow_api.cpp -- the C ABI (include/arrow.h): validation, plan build (decomposition ->
+// window-ordered device segment layout), upload, and the arrow_spmm launch sequence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <omp.h>
+#include <string>
+#include <vector>
+
+#include "../../include/arrow.h"
+#include "arrow_internal.h"
+#include "comm.h"
+
+using namespace arrow;
+
+namespace {
+
+thread_local std::string g_err;
+
+arrow_status fail(arrow_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess) return fail(ARROW_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr int64_t kDefaultWindowRows = 65536;
+constexpr int32_t kDefaultHeadChunk = 256;
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct ProfRec {
+    int kid;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct arrow_plan_s {
+    int device = 0;
+    int num_sms = 148;
+    arrow_dtype dtype = ARROW_F32;
+    int order = ARROW_ORDER_ORIGINAL;
+    int64_t n = 0, nnz = 0, b = 0;
+    int64_t isolated = 0;
+    int64_t residual_nnz = 0;
+    int64_t max_head = 0;
+    double create_seconds = 0;
+    std::vector<DeviceLevel> levels;  // arrow levels, then (optionally) the residual level
+    int32_t arrow_levels = 0;
+    // host copy of the canonical levels for export
+    std::vector<HostLevel> host_levels;
+    std::vector<std::vector<uint8_t>> host_level_vals;  // per level, plan dtype
+    // device memory
+    void *arena = nullptr;
+    int64_t arena_bytes = 0;
+    void *ws = nullptr;          // D0 | C0
+    int64_t ws_k = 0;
+    void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
+    int64_t host_k = 0;
+    cudaStream_t stream = nullptr;
+    bool poisoned = false;
+    // profiling
+    bool profiling = false;
+    std::vector<ProfRec> prof;
+    arrow_kernel_times_t prof_acc{};
+    // distributed
+    arrow_comm comm = nullptr;
+    int64_t local_begin = 0, local_end = 0;
+    int64_t bytes_alg_fixed = 0, bytes_alg_rows = 0, sum_rows = 0;
+
+    ~arrow_plan_s() {
+        for (auto &r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+        if (arena) cudaFree(arena);
+        if (ws) cudaFree(ws);
+        if (host_x) cudaFree(host_x);
+        if (host_y) cudaFree(host_y);
+    }
+    size_t esize() const { return dtype == ARROW_F64 ? 8 : 4; }
+};
+
+// Host decomposition object: canonical levels (values as fp64) + residual triples.
+struct arrow_decomposition_s {
+    int64_t n = 0, b = 0;
+    uint64_t seed = 4;
+    int64_t isolated = 0;
+    std::vector<HostLevel> levels;
+    std::vector<int32_t> res_u, res_v;  // residual entries, original ids, CSR order
+    std::vector<double> res_a;
+    double seconds = 0;
+};
+
+// ------------------------------------------------------------------------------------ layout
+namespace {
+
+struct BuiltLevel {
+    std::vector<int32_t> seg_out;
+    std::vector<uint32_t> seg_beg;
+    std::vector<int32_t> ent_col;
+    std::vector<uint8_t> ent_val;  // plan dtype
+    std::vector<int32_t> head_rows;
+    int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
+    int mode = 0;
+};
+
+inline void put_val(std::vector<uint8_t> &dst, int64_t at, arrow_dtype pdt, double v) {
+    if (pdt == ARROW_F64) {
+        std::memcpy(dst.data() + at * 8, &v, 8);
+    } else {
+        const float f = (float)v;
+        std::memcpy(dst.data() + at * 4, &f, 4);
+    }
+}
+
+// Window-ordered segments of one arrow level (see arrow_internal.h for the encoding).
+void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_rows, int32_t head_chunk,
+                 const std::vector<int32_t> *pos0, arrow_dtype pdt, BuiltLevel &B) {
+    const int64_t n_i = L.n_i, h = L.head, rows = L.rows;
+    B.rows = rows;
+    B.n_i = n_i;
+    B.head = h;
+    B.nnz = L.row_ptr[rows];
+    B.head_nnz = L.row_ptr[h];
+    B.tiles = (n_i + b - 1) / b;
+    B.mode = level_idx == 0 ? 0 : 1;
+    auto rowid = [&](int32_t v) -> int32_t { return pos0 ? (*pos0)[v] : v; };
+    auto colmap = [&](int32_t q) -> int32_t { return q < h ? (int32_t)(kFlag | (uint32_t)q) : rowid(L.perm[q]); };
+    B.head_rows.resize(h);
+    for (int64_t j = 0; j < h; ++j) B.head_rows[j] = rowid(L.perm[j]);
+
+    const int64_t wt = std::max<int64_t>(1, window_rows / b);
+    const int64_t W = wt * b;
+    const int64_t NW = (n_i + W - 1) / W;
+    // count pass
+    std::vector<int64_t> wseg(NW + 2, 0), went(NW + 2, 0);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t w = 0; w < NW; ++w) {
+        const int64_t lo = w * W, hi = std::min(n_i, lo + W);
+        int64_t s = 0, e = 0;
+        for (int64_t p = std::max(h, lo); p < hi; ++p) { ++s; e += L.row_ptr[p + 1] - L.row_ptr[p]; }
+        for (int64_t j = 0; j < h; ++j) {
+            const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
+            const int64_t c = std::lower_bound(a, z, (int32_t)hi) - std::lower_bound(a, z, (int32_t)lo);
+            s += (c + head_chunk - 1) / head_chunk;
+            e += c;
+        }
+        wseg[w + 1] = s;
+        went[w + 1] = e;
+    }
+    // zero rows (A-isolated vertices, level 0 only) go last
+    wseg[NW + 1] = rows - n_i;
+    went[NW + 1] = 0;
+    for (int64_t w = 0; w <= NW; ++w) { wseg[w + 1] += wseg[w]; went[w + 1] += went[w]; }
+    const int64_t nseg = wseg[NW + 1], nent = went[NW + 1];
+    B.seg_out.resize(nseg);
+    B.seg_beg.resize(nseg + 1);
+    B.ent_col.resize(nent);
+    const size_t es = pdt == ARROW_F64 ? 8 : 4;
+    B.ent_val.resize(nent * es);
+    auto emit_entry = [&](int64_t at, int64_t e) {
+        B.ent_col[at] = colmap(L.col[e]);
+        put_val(B.ent_val, at, pdt, L.val[e]);
+    };
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t w = 0; w < NW; ++w) {
+        const int64_t lo = w * W, hi = std::min(n_i, lo + W);
+        int64_t s = wseg[w], e = went[w];
+        for (int64_t p = std::max(h, lo); p < hi; ++p) {
+            B.seg_out[s] = rowid(L.perm[p]);
+            B.seg_beg[s] = (uint32_t)e;
+            ++s;
+            for (int64_t x = L.row_ptr[p]; x < L.row_ptr[p + 1]; ++x) emit_entry(e++, x);
+        }
+        for (int64_t j = 0; j < h; ++j) {
+            const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
+            int64_t x0 = L.row_ptr[j] + (std::lower_bound(a, z, (int32_t)lo) - a);
+            const int64_t x1 = L.row_ptr[j] + (std::lower_bound(a, z, (int32_t)hi) - a);
+            while (x0 < x1) {
+                const int64_t x2 = std::min<int64_t>(x1, x0 + head_chunk);
+                B.seg_out[s] = (int32_t)(kFlag | (uint32_t)j);
+                B.seg_beg[s] = (uint32_t)e;
+                ++s;
+                for (int64_t x = x0; x < x2; ++x) emit_entry(e++, x);
+                x0 = x2;
+            }
+        }
+    }
+    {
+        int64_t s = wseg[NW];
+        for (int64_t p = n_i; p < rows; ++p) {
+            B.seg_out[s] = rowid(L.perm[p]);
+            B.seg_beg[s] = (uint32_t)nent;
+            ++s;
+        }
+    }
+    B.seg_beg[nseg] = (uint32_t)nent;
+}
+
+// Residual CSR level (ARROW_RESIDUAL_CSR): every row with leftover entries is one RMW segment.
+void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *pos0, arrow_dtype pdt, BuiltLevel &B) {
+    auto rowid = [&](int32_t v) -> int32_t { return pos0 ? (*pos0)[v] : v; };
+    const size_t m = D.res_u.size();
+    const size_t es = pdt == ARROW_F64 ? 8 : 4;
+    B.mode = 1;
+    B.nnz = (int64_t)m;
+    B.ent_col.resize(m);
+    B.ent_val.resize(m * es);
+    for (size_t t = 0; t < m; ++t) {
+        if (t == 0 || D.res_u[t] != D.res_u[t - 1]) {
+            B.seg_out.push_back(rowid(D.res_u[t]));
+            B.seg_beg.push_back((uint32_t)t);
+        }
+        B.ent_col[t] = rowid(D.res_v[t]);
+        put_val(B.ent_val, (int64_t)t, pdt, D.res_a[t]);
+    }
+    B.seg_beg.push_back((uint32_t)m);
+    B.rows = (int64_t)B.seg_out.size();
+    B.n_i = B.rows;
+}
+
+arrow_status validate_args(const arrow_csr *A, int64_t b, int32_t levels) {
+    if (!A) return fail(ARROW_E_INVALID_ARG, "A is NULL");
+    if (b < 2) return fail(ARROW_E_INVALID_ARG, "arrow width b must be >= 2 (PAPER.md P:807)");
+    if (levels < 0) return fail(ARROW_E_INVALID_ARG, "levels must be >= 0");
+    if (A->n < 0 || A->nnz < 0) return fail(ARROW_E_INVALID_ARG, "negative n or nnz");
+    if (A->dtype != ARROW_F32 && A->dtype != ARROW_F64) return fail(ARROW_E_INVALID_ARG, "bad dtype");
+    if (!A->row_ptr) return fail(ARROW_E_INVALID_ARG, "row_ptr is NULL");
+    if (A->nnz > 0 && (!A->col_idx || !A->values)) return fail(ARROW_E_INVALID_ARG, "col_idx/values NULL");
+    if (A->n >= ((int64_t)1 << 31) - 1) return fail(ARROW_E_UNSUPPORTED, "n must be < 2^31 - 1 (int32 indices)");
+    if (A->nnz >= ((int64_t)1 << 32) - 1) return fail(ARROW_E_UNSUPPORTED, "nnz must be < 2^32 - 1");
+    return ARROW_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------ ABI
+extern "C" {
+
+const char *arrow_status_string(arrow_status s) {
+    switch (s) {
+        case ARROW_OK: return "ARROW_OK";
+        case ARROW_E_INVALID_ARG: return "ARROW_E_INVALID_ARG";
+        case ARROW_E_BAD_CSR: return "ARROW_E_BAD_CSR";
+        case ARROW_E_NOT_SYMMETRIC: return "ARROW_E_NOT_SYMMETRIC";
+        case ARROW_E_LEVELS: return "ARROW_E_LEVELS";
+        case ARROW_E_CUDA: return "ARROW_E_CUDA";
+        case ARROW_E_NCCL: return "ARROW_E_NCCL";
+        case ARROW_E_NOMEM: return "ARROW_E_NOMEM";
+        case ARROW_E_STATE: return "ARROW_E_STATE";
+        case ARROW_E_UNSUPPORTED: return "ARROW_E_UNSUPPORTED";
+    }
+    return "ARROW_E_UNKNOWN";
+}
+
+const char *arrow_last_error(void) { return g_err.c_str(); }
+int32_t arrow_abi_version(void) { return ARROW_ABI_VERSION; }
+
+arrow_status arrow_options_default(arrow_options *opt) {
+    if (!opt) return fail(ARROW_E_INVALID_ARG, "opt is NULL");
+    std::memset(opt, 0, sizeof(*opt));
+    opt->compute = (arrow_dtype)-1;
+    opt->seed = 4;
+    opt->order = ARROW_ORDER_ORIGINAL;
+    opt->residual = ARROW_RESIDUAL_ERROR;
+    opt->window_rows = 0;
+    opt->head_chunk = 0;
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, arrow_plan *out) {
+    return arrow_plan_create_ex(A, b, levels, nullptr, nullptr, out);
+}
+
+static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, bool keep_residual,
+                                   std::unique_ptr<arrow_decomposition_s> &D) {
+    const auto t0 = std::chrono::steady_clock::now();
+    arrow_status st = validate_args(A, b, levels);
+    if (st != ARROW_OK) return st;
+    std::string err;
+    const int64_t n = A->n;
+    if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
+    if (check_symmetric(n, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_NOT_SYMMETRIC, err);
+    try {
+        D.reset(new arrow_decomposition_s());
+        D->n = n;
+        D->b = b;
+        D->seed = seed;
+        HostDecomposition H;
+        if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, H, err)) return fail(ARROW_E_INVALID_ARG, err);
+        if (!H.residual.empty() && !keep_residual)
+            return fail(ARROW_E_LEVELS, "levels cap " + std::to_string(levels) + " reached with " +
+                                            std::to_string(H.residual.size()) + " entries left");
+        auto value = [&](uint32_t e) -> double {
+            return A->dtype == ARROW_F64 ? ((const double *)A->values)[e] : (double)((const float *)A->values)[e];
+        };
+        for (auto &L : H.levels) {
+            L.val.resize(L.src.size());
+#pragma omp parallel for schedule(static)
+            for (int64_t t = 0; t < (int64_t)L.src.size(); ++t) L.val[t] = value(L.src[t]);
+            L.src.clear();
+            L.src.shrink_to_fit();
+        }
+        std::vector<uint32_t> r(H.residual);
+        std::sort(r.begin(), r.end());  // CSR order: rows then columns ascending
+        int64_t row = 0;
+        for (uint32_t e : r) {
+            while (A->row_ptr[row + 1] <= (int64_t)e) ++row;
+            D->res_u.push_back((int32_t)row);
+            D->res_v.push_back(A->col_idx[e]);
+            D->res_a.push_back(value(e));
+        }
+        for (int64_t v = 0; v < n; ++v) D->isolated += (A->row_ptr[v + 1] == A->row_ptr[v]) ? 1 : 0;
+        D->levels = std::move(H.levels);
+    } catch (const std::bad_alloc &) {
+        D.reset();
+        return fail(ARROW_E_NOMEM, "host allocation failed during decomposition");
+    }
+    D->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return ARROW_OK;
+}
+
+static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_options *opt_in, arrow_dtype default_dt,
+                              arrow_comm comm, arrow_plan *out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    arrow_options opt;
+    arrow_options_default(&opt);
+    if (opt_in) opt = *opt_in;
+    if ((int)opt.compute != -1 && opt.compute != ARROW_F32 && opt.compute != ARROW_F64)
+        return fail(ARROW_E_INVALID_ARG, "bad options.compute");
+    const arrow_dtype pdt = (opt.compute == ARROW_F32 || opt.compute == ARROW_F64) ? opt.compute : default_dt;
+    if (opt.order != ARROW_ORDER_ORIGINAL && opt.order != ARROW_ORDER_PERMUTED)
+        return fail(ARROW_E_INVALID_ARG, "bad options.order");
+    if (opt.window_rows < 0 || opt.head_chunk < 0) return fail(ARROW_E_INVALID_ARG, "negative window/chunk");
+    const int64_t window_rows = opt.window_rows > 0 ? opt.window_rows : kDefaultWindowRows;
+    const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : kDefaultHeadChunk;
+    const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
+    const int64_t n = D.n, b = D.b;
+
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::unique_ptr<arrow_plan_s> P;
+    std::vector<BuiltLevel> built;
+    try {
+        P.reset(new arrow_plan_s());
+        P->device = dev;
+        CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, dev));
+        P->dtype = pdt;
+        P->order = order;
+        P->n = n;
+        P->b = b;
+        P->isolated = D.isolated;
+        P->nnz = (int64_t)D.res_u.size();
+        for (auto &L : D.levels) P->nnz += L.row_ptr[L.rows];
+        std::vector<int32_t> pos0;
+        const std::vector<int32_t> *pos0p = nullptr;
+        if (order == ARROW_ORDER_PERMUTED && !D.levels.empty()) {
+            pos0.assign(n, 0);
+            for (int64_t p = 0; p < n; ++p) pos0[D.levels[0].perm[p]] = (int32_t)p;
+            pos0p = &pos0;
+        }
+        built.resize(D.levels.size() + (D.res_u.empty() ? 0 : 1));
+        for (size_t i = 0; i < D.levels.size(); ++i)
+            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, pos0p, pdt, built[i]);
+        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, built.back());
+        P->residual_nnz = (int64_t)D.res_u.size();
+        P->arrow_levels = (int32_t)D.levels.size();
+        P->host_levels.resize(D.levels.size());
+        P->host_level_vals.resize(D.levels.size());
+        for (size_t i = 0; i < D.levels.size(); ++i) {
+            const HostLevel &L = D.levels[i];
+            HostLevel &C = P->host_levels[i];
+            C.rows = L.rows; C.n_i = L.n_i; C.head = L.head;
+            C.perm = L.perm; C.row_ptr = L.row_ptr; C.col = L.col;
+            auto &hv = P->host_level_vals[i];
+            hv.resize(L.val.size() * P->esize());
+            for (size_t t = 0; t < L.val.size(); ++t) put_val(hv, (int64_t)t, pdt, L.val[t]);
+        }
+    } catch (const std::bad_alloc &) {
+        return fail(ARROW_E_NOMEM, "host allocation failed during layout build");
+    }
+
+    // algorithmic bytes model
+    {
+        const int64_t s = (int64_t)P->esize();
+        for (size_t i = 0; i < built.size(); ++i) {
+            const BuiltLevel &B = built[i];
+            P->bytes_alg_fixed += B.nnz * (s + 4) + (B.rows + 1) * 8 + B.rows * 4;
+            P->bytes_alg_rows += B.n_i + (i == 0 ? 0 : 2 * B.n_i);
+            P->sum_rows += (i < (size_t)P->arrow_levels) ? B.n_i : 0;
+            P->max_head = std::max(P->max_head, B.head);
+        }
+        P->bytes_alg_rows += n;  // level-0 store of every Y row
+    }
+
+    // upload: one arena for all levels
+    {
+        const size_t es = P->esize();
+        int64_t total = 0;
+        auto reserve = [&](int64_t bytes) { int64_t at = total; total += align_up(std::max<int64_t>(bytes, 1), 256); return at; };
+        std::vector<std::array<int64_t, 5>> offs(built.size());
+        for (size_t i = 0; i < built.size(); ++i) {
+            const BuiltLevel &B = built[i];
+            offs[i][0] = reserve((int64_t)B.seg_out.size() * 4);
+            offs[i][1] = reserve((int64_t)B.seg_beg.size() * 4);
+            offs[i][2] = reserve((int64_t)B.ent_col.size() * 4);
+            offs[i][3] = reserve((int64_t)B.ent_col.size() * (int64_t)es);
+            offs[i][4] = reserve((int64_t)B.head_rows.size() * 4);
+        }
+        if (total > 0) {
+            cudaError_t e = cudaMalloc(&P->arena, (size_t)total);
+            if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(plan arena): ") + cudaGetErrorString(e));
+        }
+        P->arena_bytes = total;
+        char *base = reinterpret_cast<char *>(P->arena);
+        for (size_t i = 0; i < built.size(); ++i) {
+            const BuiltLevel &B = built[i];
+            DeviceLevel L;
+            L.rows = B.rows; L.n_i = B.n_i; L.head = B.head; L.nnz = B.nnz; L.head_nnz = B.head_nnz;
+            L.tiles = B.tiles; L.nseg = (int64_t)B.seg_out.size(); L.mode = B.mode;
+            L.seg_out = reinterpret_cast<int32_t *>(base + offs[i][0]);
+            L.seg_beg = reinterpret_cast<uint32_t *>(base + offs[i][1]);
+            L.ent_col = reinterpret_cast<int32_t *>(base + offs[i][2]);
+            L.ent_val = base + offs[i][3];
+            L.head_rows = reinterpret_cast<int32_t *>(base + offs[i][4]);
+            CUDA_TRY(cudaMemcpy(L.seg_out, B.seg_out.data(), B.seg_out.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.seg_beg, B.seg_beg.data(), B.seg_beg.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.ent_col, B.ent_col.data(), B.ent_col.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.ent_val, B.ent_val.data(), B.ent_val.size(), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.head_rows, B.head_rows.data(), B.head_rows.size() * 4, cudaMemcpyHostToDevice));
+            P->levels.push_back(L);
+        }
+    }
+    P->local_begin = 0;
+    P->local_end = n;
+    if (comm) {
+        arrow_status cs = comm_attach(P.get(), comm);
+        if (cs != ARROW_OK) return cs;
+    }
+    P->create_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = P.release();
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels, const arrow_options *opt_in,
+                                  arrow_comm comm, arrow_plan *out) {
+    g_err.clear();
+    if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    arrow_options opt;
+    arrow_options_default(&opt);
+    if (opt_in) opt = *opt_in;
+    if (opt.residual != ARROW_RESIDUAL_ERROR && opt.residual != ARROW_RESIDUAL_CSR)
+        return fail(ARROW_E_INVALID_ARG, "bad options.residual");
+    std::unique_ptr<arrow_decomposition_s> D;
+    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, D);
+    if (st != ARROW_OK) return st;
+    st = plan_from(*D, &opt, A->dtype, comm, out);
+    if (st == ARROW_OK) (*out)->create_seconds += D->seconds;
+    return st;
+}
+
+arrow_status arrow_plan_create_from(arrow_decomposition d, const arrow_options *opt, arrow_comm comm, arrow_plan *out) {
+    g_err.clear();
+    if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!d) return fail(ARROW_E_INVALID_ARG, "decomposition is NULL");
+    return plan_from(*d, opt, ARROW_F64, comm, out);
+}
+
+arrow_status arrow_decompose(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                             arrow_decomposition *out) {
+    g_err.clear();
+    if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    std::unique_ptr<arrow_decomposition_s> D;
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, D);
+    if (st != ARROW_OK) return st;
+    *out = D.release();
+    return ARROW_OK;
+}
+
+arrow_status arrow_decomposition_destroy(arrow_decomposition d) {
+    delete d;
+    return ARROW_OK;
+}
+
+arrow_status arrow_decomposition_info(arrow_decomposition d, int64_t *n, int64_t *b, int32_t *levels,
+                                      int64_t *residual_nnz) {
+    if (!d) return fail(ARROW_E_INVALID_ARG, "decomposition is NULL");
+    if (n) *n = d->n;
+    if (b) *b = d->b;
+    if (levels) *levels = (int32_t)d->levels.size();
+    if (residual_nnz) *residual_nnz = (int64_t)d->res_u.size();
+    return ARROW_OK;
+}
+
+arrow_status arrow_decomposition_level_info(arrow_decomposition d, int32_t level, arrow_level_info_t *info) {
+    if (!d || !info) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    if (level < 0 || level >= (int32_t)d->levels.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
+    const HostLevel &L = d->levels[level];
+    std::memset(info, 0, sizeof(*info));
+    info->rows = L.rows;
+    info->n_i = L.n_i;
+    info->head = L.head;
+    info->nnz = L.row_ptr[L.rows];
+    info->head_nnz = L.row_ptr[L.head];
+    info->tiles = (L.n_i + d->b - 1) / d->b;
+    return ARROW_OK;
+}
+
+arrow_status arrow_decomposition_export_level(arrow_decomposition d, int32_t level, int32_t *perm, int64_t *row_ptr,
+                                              int32_t *col, double *val) {
+    if (!d) return fail(ARROW_E_INVALID_ARG, "decomposition is NULL");
+    if (level < 0 || level >= (int32_t)d->levels.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
+    const HostLevel &L = d->levels[level];
+    if (perm) std::memcpy(perm, L.perm.data(), L.perm.size() * 4);
+    if (row_ptr) std::memcpy(row_ptr, L.row_ptr.data(), L.row_ptr.size() * 8);
+    if (col) std::memcpy(col, L.col.data(), L.col.size() * 4);
+    if (val) std::memcpy(val, L.val.data(), L.val.size() * 8);
+    return ARROW_OK;
+}
+
+arrow_status arrow_decomposition_export_residual(arrow_decomposition d, int32_t *u, int32_t *v, double *val) {
+    if (!d) return fail(ARROW_E_INVALID_ARG, "decomposition is NULL");
+    if (u) std::memcpy(u, d->res_u.data(), d->res_u.size() * 4);
+    if (v) std::memcpy(v, d->res_v.data(), d->res_v.size() * 4);
+    if (val) std::memcpy(val, d->res_a.data(), d->res_a.size() * 8);
+    return ARROW_OK;
+}
+
+namespace {
+struct Fnv {
+    uint64_t h = 1469598103934665603ULL;
+    void add(const void *p, size_t n) {
+        const uint8_t *b = (const uint8_t *)p;
+        for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
+    }
+};
+const char kMagic[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '1'};
+}  // namespace
+
+arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path) {
+    if (!d || !path) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    FILE *f = std::fopen(path, "wb");
+    if (!f) return fail(ARROW_E_INVALID_ARG, std::string("cannot open ") + path);
+    Fnv fnv;
+    bool ok = true;
+    auto w = [&](const void *p, size_t n) {
+        if (n == 0) return;
+        fnv.add(p, n);
+        ok = ok && std::fwrite(p, 1, n, f) == n;
+    };
+    w(kMagic, 8);
+    const int64_t hdr[6] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated};
+    w(hdr, sizeof(hdr));
+    for (const HostLevel &L : d->levels) {
+        const int64_t lh[4] = {L.rows, L.n_i, L.head, L.row_ptr[L.rows]};
+        w(lh, sizeof(lh));
+        w(L.perm.data(), L.perm.size() * 4);
+        w(L.row_ptr.data(), L.row_ptr.size() * 8);
+        w(L.col.data(), L.col.size() * 4);
+        w(L.val.data(), L.val.size() * 8);
+    }
+    w(d->res_u.data(), d->res_u.size() * 4);
+    w(d->res_v.data(), d->res_v.size() * 4);
+    w(d->res_a.data(), d->res_a.size() * 8);
+    const uint64_t sum = fnv.h;
+    ok = ok && std::fwrite(&sum, 1, 8, f) == 8;
+    ok = (std::fclose(f) == 0) && ok;
+    return ok ? ARROW_OK : fail(ARROW_E_INVALID_ARG, std::string("write failed: ") + path);
+}
+
+arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out) {
+    if (!path || !out) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    *out = nullptr;
+    FILE *f = std::fopen(path, "rb");
+    if (!f) return fail(ARROW_E_INVALID_ARG, std::string("cannot open ") + path);
+    Fnv fnv;
+    bool ok = true;
+    auto r = [&](void *p, size_t n) {
+        if (n == 0 || !ok) return;
+        ok = std::fread(p, 1, n, f) == n;
+        if (ok) fnv.add(p, n);
+    };
+    std::unique_ptr<arrow_decomposition_s> D;
+    try {
+        D.reset(new arrow_decomposition_s());
+        char magic[8];
+        r(magic, 8);
+        if (!ok || std::memcmp(magic, kMagic, 8) != 0) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "not an arrow decomposition file"); }
+        int64_t hdr[6];
+        r(hdr, sizeof(hdr));
+        if (!ok || hdr[0] < 0 || hdr[1] < 2 || hdr[3] < 0 || hdr[4] < 0) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
+        D->n = hdr[0]; D->b = hdr[1]; D->seed = (uint64_t)hdr[2]; D->isolated = hdr[5];
+        D->levels.resize(hdr[3]);
+        for (HostLevel &L : D->levels) {
+            int64_t lh[4];
+            r(lh, sizeof(lh));
+            if (!ok || lh[0] < 0 || lh[0] > D->n || lh[3] < 0) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt level header"); }
+            L.rows = lh[0]; L.n_i = lh[1]; L.head = lh[2];
+            L.perm.resize(L.rows); L.row_ptr.resize(L.rows + 1); L.col.resize(lh[3]); L.val.resize(lh[3]);
+            r(L.perm.data(), L.perm.size() * 4);
+            r(L.row_ptr.data(), L.row_ptr.size() * 8);
+            r(L.col.data(), L.col.size() * 4);
+            r(L.val.data(), L.val.size() * 8);
+        }
+        D->res_u.resize(hdr[4]); D->res_v.resize(hdr[4]); D->res_a.resize(hdr[4]);
+        r(D->res_u.data(), D->res_u.size() * 4);
+        r(D->res_v.data(), D->res_v.size() * 4);
+        r(D->res_a.data(), D->res_a.size() * 8);
+    } catch (const std::bad_alloc &) {
+        std::fclose(f);
+        return fail(ARROW_E_NOMEM, "host allocation failed while loading");
+    }
+    const uint64_t expect = fnv.h;
+    uint64_t sum = 0;
+    const bool got = std::fread(&sum, 1, 8, f) == 8;
+    std::fclose(f);
+    if (!ok || !got || sum != expect) return fail(ARROW_E_INVALID_ARG, "truncated file or checksum mismatch");
+    *out = D.release();
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_destroy(arrow_plan plan) {
+    if (!plan) return ARROW_OK;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    const int dev = plan->device;
+    if (cur != dev) cudaSetDevice(dev);
+    if (plan->stream) cudaStreamSynchronize(plan->stream);
+    else cudaDeviceSynchronize();
+    if (plan->comm) comm_detach(plan);
+    delete plan;
+    if (cur != dev) cudaSetDevice(cur);
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_set_stream(arrow_plan plan, void *stream) {
+    if (!plan) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    plan->stream = reinterpret_cast<cudaStream_t>(stream);
+    return ARROW_OK;
+}
+
+static arrow_status ensure_ws(arrow_plan P, int64_t k) {
+    if (k <= P->ws_k) return ARROW_OK;
+    const int64_t bytes = 2 * align_up(std::max<int64_t>(P->max_head, 1) * k * (int64_t)P->esize(), 256);
+    if (P->ws) {
+        cudaError_t e = cudaStreamSynchronize(P->stream);
+        if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
+        cudaFree(P->ws);
+        P->ws = nullptr;
+        P->ws_k = 0;
+    }
+    cudaError_t e = cudaMalloc(&P->ws, (size_t)bytes);
+    if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(workspace): ") + cudaGetErrorString(e));
+    P->ws_k = k;
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_reserve(arrow_plan plan, int64_t k_max) {
+    if (!plan) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (k_max < 0) return fail(ARROW_E_INVALID_ARG, "k_max < 0");
+    int cur = 0;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != plan->device) return fail(ARROW_E_STATE, "plan used from another device");
+    return ensure_ws(plan, k_max);
+}
+
+namespace {
+inline void prof_begin(arrow_plan P, cudaStream_t st, cudaEvent_t &a) {
+    if (!P->profiling) return;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, st);
+}
+inline void prof_end(arrow_plan P, cudaStream_t st, int kid, cudaEvent_t a) {
+    if (!P->profiling) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, st);
+    P->prof.push_back(ProfRec{kid, a, b});
+}
+}  // namespace
+
+arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void *stream) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
+    if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
+    if (k == 0 || P->n == 0) return ARROW_OK;
+    if (!X || !Y) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
+    int cur = 0;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
+    const int64_t rows = P->local_end - P->local_begin;
+    const int64_t bytes = rows * k * (int64_t)P->esize();
+    const char *xa = (const char *)X, *ya = (const char *)Y;
+    if (xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
+    arrow_status s = ensure_ws(P, k);
+    if (s != ARROW_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (P->comm) return comm_spmm(P, X, Y, k, st);
+    const int dt = P->dtype == ARROW_F64 ? 1 : 0;
+    char *D0 = reinterpret_cast<char *>(P->ws);
+    char *C0 = D0 + align_up(std::max<int64_t>(P->max_head, 1) * k * (int64_t)P->esize(), 256);
+    if (P->levels.empty()) {
+        int e = launch_zero(Y, bytes, st);
+        if (e) return fail(ARROW_E_CUDA, cudaGetErrorString((cudaError_t)e));
+    }
+    if (P->profiling) P->prof_acc.calls += 1;
+    for (size_t i = 0; i < P->levels.size(); ++i) {
+        const DeviceLevel &L = P->levels[i];
+        cudaEvent_t a = nullptr;
+        int e = 0;
+        if (L.head > 0) {
+            prof_begin(P, st, a);
+            e = launch_head_stage(dt, X, L.head_rows, L.head, k, D0, C0, st);
+            prof_end(P, st, ARROW_K_HEAD_STAGE, a);
+            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-H: ") + cudaGetErrorString((cudaError_t)e)); }
+        }
+        prof_begin(P, st, a);
+        e = launch_segments(dt, L, X, D0, Y, C0, k, P->num_sms, st);
+        prof_end(P, st, ARROW_K_SEGMENTS, a);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
+        if (L.head > 0) {
+            prof_begin(P, st, a);
+            e = launch_head_epilogue(dt, C0, L.head_rows, L.head, k, L.mode, Y, st);
+            prof_end(P, st, ARROW_K_HEAD_EPI, a);
+            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-C: ") + cudaGetErrorString((cudaError_t)e)); }
+        }
+    }
+    return ARROW_OK;
+}
+
+arrow_status arrow_spmm(arrow_plan plan, const void *X, void *Y, int64_t k) {
+    if (!plan) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    return arrow_spmm_ex(plan, X, Y, k, plan->stream);
+}
+
+arrow_status arrow_spmm_host(arrow_plan P, const void *Xh, void *Yh, int64_t k, void *stream) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
+    if (k == 0 || P->n == 0) return ARROW_OK;
+    if (!Xh || !Yh) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t rows = P->local_end - P->local_begin;
+    const int64_t bytes = rows * k * (int64_t)P->esize();
+    if (k > P->host_k) {
+        if (P->host_x) { cudaFree(P->host_x); P->host_x = nullptr; }
+        if (P->host_y) { cudaFree(P->host_y); P->host_y = nullptr; }
+        P->host_k = 0;
+        CUDA_TRY(cudaMalloc(&P->host_x, (size_t)std::max<int64_t>(bytes, 1)));
+        CUDA_TRY(cudaMalloc(&P->host_y, (size_t)std::max<int64_t>(bytes, 1)));
+        P->host_k = k;
+    }
+    CUDA_TRY(cudaMemcpyAsync(P->host_x, Xh, (size_t)bytes, cudaMemcpyHostToDevice, st));
+    arrow_status s = arrow_spmm_ex(P, P->host_x, P->host_y, k, stream);
+    if (s != ARROW_OK) return s;
+    CUDA_TRY(cudaMemcpyAsync(Yh, P->host_y, (size_t)bytes, cudaMemcpyDeviceToHost, st));
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_info(arrow_plan P, arrow_plan_info_t *info) {
+    if (!P || !info) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n = P->n;
+    info->nnz = P->nnz;
+    info->b = P->b;
+    info->levels = P->arrow_levels;
+    info->dtype = P->dtype;
+    info->order = P->order;
+    info->distributed = P->comm ? 1 : 0;
+    info->residual_nnz = P->residual_nnz;
+    info->sum_rows = P->sum_rows;
+    info->isolated = P->isolated;
+    info->create_seconds = P->create_seconds;
+    info->bytes_alg_fixed = P->bytes_alg_fixed;
+    info->bytes_alg_rows = P->bytes_alg_rows;
+    info->device_bytes = P->arena_bytes;
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_level_info(arrow_plan P, int32_t level, arrow_level_info_t *info) {
+    if (!P || !info) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    if (level < 0 || level >= (int32_t)P->levels.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
+    std::memset(info, 0, sizeof(*info));
+    const DeviceLevel &L = P->levels[level];
+    info->rows = L.rows;
+    info->n_i = L.n_i;
+    info->head = L.head;
+    info->nnz = L.nnz;
+    info->head_nnz = L.head_nnz;
+    info->tiles = L.tiles;
+    info->segments = L.nseg;
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_export_level(arrow_plan P, int32_t level, int32_t *perm, int64_t *row_ptr, int32_t *col,
+                                     void *val) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (level < 0 || level >= P->arrow_levels) return fail(ARROW_E_INVALID_ARG, "level out of range");
+    const HostLevel &L = P->host_levels[level];
+    if (perm) std::memcpy(perm, L.perm.data(), L.perm.size() * 4);
+    if (row_ptr) std::memcpy(row_ptr, L.row_ptr.data(), L.row_ptr.size() * 8);
+    if (col) std::memcpy(col, L.col.data(), L.col.size() * 4);
+    if (val) std::memcpy(val, P->host_level_vals[level].data(), P->host_level_vals[level].size());
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_local_rows(arrow_plan P, int64_t *begin, int64_t *end) {
+    if (!P || !begin || !end) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    *begin = P->local_begin;
+    *end = P->local_end;
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_set_profiling(arrow_plan P, int32_t on) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    for (auto &r : P->prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    P->prof.clear();
+    P->prof_acc = arrow_kernel_times_t{};
+    P->profiling = on != 0;
+    return ARROW_OK;
+}
+
+arrow_status arrow_plan_kernel_times(arrow_plan P, arrow_kernel_times_t *out) {
+    if (!P || !out) return fail(ARROW_E_INVALID_ARG, "NULL argument");
+    for (auto &r : P->prof) {
+        CUDA_TRY(cudaEventSynchronize(r.b));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+        P->prof_acc.ms[r.kid] += ms;
+        P->prof_acc.launches[r.kid] += 1;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    P->prof.clear();
+    *out = P->prof_acc;
+    return ARROW_OK;
+}
+
+}  // extern "C"

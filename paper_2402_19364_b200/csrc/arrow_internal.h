@@ -1,0 +1,70 @@
+// arrow_internal.h -- internal types shared by the host decomposer, plan builder and kernels.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace arrow {
+
+// One arrow matrix B_i of the decomposition, in positions (Eq. (1)).
+// perm[p] = original vertex at position p (pi_i^{-1}); entries carry the index of the
+// originating entry of A (`src`) so that values are gathered in the plan's dtype.
+struct HostLevel {
+    int64_t rows = 0;     // n for level 0 (A-isolated vertices appended), n_i otherwise
+    int64_t n_i = 0;      // vertices with an entry in A_i
+    int64_t head = 0;     // h_i = min(b, n_i)
+    std::vector<int32_t> perm;      // [rows]
+    std::vector<int64_t> row_ptr;   // [rows + 1]
+    std::vector<int32_t> col;       // [nnz] positions, strictly increasing per row
+    std::vector<uint32_t> src;      // [nnz] entry index into A's CSR arrays (decomposer output)
+    std::vector<double> val;        // [nnz] values (exact copy of A's fp32/fp64 values)
+};
+
+struct HostDecomposition {
+    int64_t n = 0, b = 0;
+    std::vector<HostLevel> levels;
+    std::vector<uint32_t> residual;  // entry indices of A left when the level cap is reached
+};
+
+// LA-Decompose (decompose.cpp).  Returns 0 on success, else sets `err`.
+int la_decompose(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
+                 uint64_t seed, HostDecomposition &out, std::string &err);
+
+// Validation helpers (decompose.cpp): 0 ok, 1 bad CSR, 2 not symmetric.
+int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, std::string &err);
+int check_symmetric(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &err);
+
+// ------------------------------------------------------------------ device layout of one level
+// Work is a stream of "segments": a segment is a list of (column, value) entries whose sum
+// sum_e val_e * src_row(col_e) goes to one output row.
+//   out >= 0 : Y row `out` (body row p >= h_i of B_i, folded: out = perm_i[p] or its pi_0 position)
+//   out <  0 : head accumulator row (out & 0x7fffffff) = j, partial sum of head row j restricted
+//              to one tile window (Alg. 1 line 2, C^(0) = sum_t B^(0,t) D^(t))
+//   col >= 0 : X row col (folded permutation: P_pi^T X never materialised, S4)
+//   col <  0 : head block row (col & 0x7fffffff) of D0 = X[head_i] (Alg. 1 line 1)
+// Segments are ordered by tile window so that concurrently running warps touch the same
+// X rows (L2 reuse, the IO lemma's "tiles stay resident").
+constexpr uint32_t kFlag = 0x80000000u;
+
+struct DeviceLevel {
+    int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
+    int64_t nseg = 0;
+    int mode = 0;                 // 0: level 0 stores Y rows; 1: levels >= 1 read-modify-write (S5)
+    // device pointers (into the plan arena)
+    int32_t *seg_out = nullptr;   // [nseg]
+    uint32_t *seg_beg = nullptr;  // [nseg + 1]
+    int32_t *ent_col = nullptr;   // [nnz]
+    void *ent_val = nullptr;      // [nnz] of dtype
+    int32_t *head_rows = nullptr; // [head] X/Y row of head vertex j
+};
+
+// kernels.cu launchers (all on `stream`; return cudaError_t as int)
+int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k,
+                      void *D0, void *C0, void *stream);
+int launch_segments(int dtype, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
+                    int64_t k, int num_sms, void *stream);
+int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k,
+                         int add, void *Y, void *stream);
+int launch_zero(void *Y, int64_t bytes, void *stream);
+
+}  // namespace arrow

@@ -1,0 +1,347 @@
+// kernels.cu -- the hot path of arrow_spmm on sm_100a (B200).
+//
+// Per level i of the decomposition A X = sum_i P_{pi_i} (B_i (P_{pi_i}^T X))  (Eq. (1)):
+//   K-H  head stage      D0 = X[head_i] (Alg. 1 line 1 "Broadcast(D^(0))"), C0 = 0
+//   K-A  segment stream  body rows  y_p = B^(p,0) D0 + B^(p,p) X_p  -> Y[perm_i[p]] (store at level 0,
+//                        read-modify-write at levels >= 1: Alg. 2's reverse aggregation)
+//                        head rows  C0[j] += B^(0,t) X_t, one tile window t at a time (Alg. 1 line 2,
+//                        P:464), combined with fp atomics in L2 (C0 is L2-resident)
+//   K-C  head epilogue   Y[head_i] (= or +=) C0 (Alg. 1 line 3 "Reduce(C^(0))")
+// The permutations P_pi^T X / P_pi Y are folded into the column and output indices at plan
+// time (S4): no permuted copy of X or Y ever exists.
+//
+// The path is HBM-bound (<= 2 FLOP/B), so there are no tensor cores: the design
+// goal is that every X row of a tile is fetched from DRAM once (window-ordered work keeps the
+// tile's rows L2-hot while all its users run) and that each warp keeps many 16-byte loads in
+// flight.  A "sub-warp" of LPE lanes owns one row slab of LPE*VEC elements: LPE=32 lanes x float4
+// covers a 512-byte row (k=128 fp32) with one coalesced request per entry.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "arrow_internal.h"
+
+namespace arrow {
+namespace {
+
+template <typename T, int VEC> struct VecT;
+template <> struct VecT<float, 4> { using type = float4; };
+template <> struct VecT<float, 2> { using type = float2; };
+template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<double, 2> { using type = double2; };
+template <> struct VecT<double, 1> { using type = double; };
+
+template <typename T, int VEC> struct Frag {
+    T v[VEC];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) v[i] = T(0);
+    }
+};
+
+template <typename T, int VEC>
+__device__ __forceinline__ Frag<T, VEC> ld_x(const T *p) {  // read-only path, 16 B per lane at VEC*sizeof(T)=16
+    using V = typename VecT<T, VEC>::type;
+    V r = __ldg(reinterpret_cast<const V *>(p));
+    Frag<T, VEC> f;
+    static_assert(sizeof(V) == sizeof(f), "frag size");
+    memcpy(&f, &r, sizeof(V));
+    return f;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ Frag<T, VEC> ld_plain(const T *p) {
+    using V = typename VecT<T, VEC>::type;
+    V r = *reinterpret_cast<const V *>(p);
+    Frag<T, VEC> f;
+    memcpy(&f, &r, sizeof(V));
+    return f;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void st_stream(T *p, const Frag<T, VEC> &f) {  // evict-first: Y is write-once
+    using V = typename VecT<T, VEC>::type;
+    V r;
+    memcpy(&r, &f, sizeof(V));
+    __stcs(reinterpret_cast<V *>(p), r);
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void st_plain(T *p, const Frag<T, VEC> &f) {
+    using V = typename VecT<T, VEC>::type;
+    V r;
+    memcpy(&r, &f, sizeof(V));
+    *reinterpret_cast<V *>(p) = r;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
+    if constexpr (sizeof(T) == 4 && VEC == 4) {
+        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(f.v[0], f.v[1], f.v[2], f.v[3]));
+    } else if constexpr (sizeof(T) == 4 && VEC == 2) {
+        atomicAdd(reinterpret_cast<float2 *>(p), make_float2(f.v[0], f.v[1]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) atomicAdd(p + i, f.v[i]);
+    }
+}
+
+// ------------------------------------------------------------------------------------ K-A
+// Segment stream: sub-warp `sw` takes batches of LPE consecutive segments, grid-strided so that
+// all sub-warps advance through the (window-ordered) segment list together.  Lane l of the
+// sub-warp holds descriptor l of the batch; the batch's entries are contiguous and are streamed
+// in chunks of LPE (one coalesced load of col/val per lane), broadcast with shuffles, and
+// consumed UNROLL at a time with all UNROLL row loads issued before any FMA -- independent of
+// where segment boundaries fall, so short rows do not serialise on latency.
+template <typename T, int VEC, int LPE, int MODE>
+__global__ void __launch_bounds__(256) k_segments(const int32_t *__restrict__ seg_out,
+                                                  const uint32_t *__restrict__ seg_beg, int64_t nseg,
+                                                  const int32_t *__restrict__ ent_col,
+                                                  const T *__restrict__ ent_val, const T *__restrict__ X,
+                                                  const T *__restrict__ D0, T *__restrict__ Y,
+                                                  T *__restrict__ C0, int64_t k) {
+    constexpr int UNROLL = (LPE >= 8) ? 8 : 4;
+    constexpr int SLAB = LPE * VEC;
+    const int lane = threadIdx.x & 31;
+    const int sl = lane % LPE;
+    const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (lane - sl));
+    const int64_t nsub = (int64_t)gridDim.x * blockDim.x / LPE;
+    const int64_t nbatch = (nseg + LPE - 1) / LPE;
+
+    for (int64_t bt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPE; bt < nbatch; bt += nsub) {
+        const int64_t s0 = bt * LPE;
+        const int nb = (nseg - s0 < LPE) ? (int)(nseg - s0) : LPE;
+        const int32_t my_out = (sl < nb) ? __ldg(seg_out + s0 + sl) : 0;
+        const uint32_t my_beg = __ldg(seg_beg + s0 + (sl < nb ? sl : nb));
+        const uint32_t e_end = __ldg(seg_beg + s0 + nb);
+        const uint32_t e_begin = __shfl_sync(mask, my_beg, 0, LPE);
+
+        for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
+            const int64_t col0 = c0 + (int64_t)sl * VEC;
+            const bool active = col0 < k;
+            Frag<T, VEC> acc;
+            acc.zero();
+            int cur = 0;
+            uint32_t cend = (nb > 1) ? __shfl_sync(mask, my_beg, 1, LPE) : e_end;
+
+            auto flush = [&](int s) {
+                const int32_t o = __shfl_sync(mask, my_out, s, LPE);
+                if (active) {
+                    if (o < 0) {
+                        atomic_add_frag<T, VEC>(C0 + (int64_t)(o & 0x7fffffff) * k + col0, acc);
+                    } else if (MODE == 0) {
+                        st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
+                    } else {
+                        T *p = Y + (int64_t)o * k + col0;
+                        Frag<T, VEC> y = ld_plain<T, VEC>(p);
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                        st_plain<T, VEC>(p, y);
+                    }
+                }
+            };
+
+            for (uint32_t cb = e_begin; cb < e_end; cb += LPE) {
+                const int cnt = (e_end - cb < (uint32_t)LPE) ? (int)(e_end - cb) : LPE;
+                int32_t mycol = 0;
+                T myval = T(0);
+                if (sl < cnt) {
+                    mycol = __ldcs(ent_col + cb + sl);
+                    myval = __ldcs(ent_val + cb + sl);
+                }
+#pragma unroll 1
+                for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
+                    Frag<T, VEC> xv[UNROLL];
+                    T av[UNROLL];
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+                        const int idx = u0 + t;
+                        const int32_t cc = __shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
+                        av[t] = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
+                        if (idx < cnt && active) {
+                            const T *base = (cc < 0) ? D0 + (int64_t)(cc & 0x7fffffff) * k : X + (int64_t)cc * k;
+                            xv[t] = ld_x<T, VEC>(base + col0);
+                        } else {
+                            xv[t].zero();
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+                        if (u0 + t < cnt) {
+                            const uint32_t e = cb + u0 + t;
+                            while (e >= cend) {        // segment boundary (sub-warp uniform)
+                                flush(cur);
+                                acc.zero();
+                                ++cur;
+                                cend = (cur + 1 < nb) ? __shfl_sync(mask, my_beg, cur + 1, LPE) : e_end;
+                            }
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        }
+                    }
+                }
+            }
+            while (cur < nb) {  // last segment and trailing empty segments (zero rows)
+                flush(cur);
+                acc.zero();
+                ++cur;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------ K-H / K-C
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_head_stage(const T *__restrict__ X, const int32_t *__restrict__ head,
+                                                    int64_t h, int64_t k, T *__restrict__ D0, T *__restrict__ C0) {
+    const int64_t kv = k / VEC, total = h * kv;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / kv, c = (t - j * kv) * VEC;
+        const Frag<T, VEC> x = ld_x<T, VEC>(X + (int64_t)__ldg(head + j) * k + c);
+        st_plain<T, VEC>(D0 + j * k + c, x);
+        Frag<T, VEC> z;
+        z.zero();
+        st_plain<T, VEC>(C0 + j * k + c, z);
+    }
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_head_epilogue(const T *__restrict__ C0, const int32_t *__restrict__ head,
+                                                       int64_t h, int64_t k, int add, T *__restrict__ Y) {
+    const int64_t kv = k / VEC, total = h * kv;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / kv, c = (t - j * kv) * VEC;
+        Frag<T, VEC> a = ld_plain<T, VEC>(C0 + j * k + c);
+        T *p = Y + (int64_t)__ldg(head + j) * k + c;
+        if (add) {
+            Frag<T, VEC> y = ld_plain<T, VEC>(p);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) a.v[i] += y.v[i];
+        }
+        st_plain<T, VEC>(p, a);
+    }
+}
+
+// ------------------------------------------------------------------------------------ dispatch
+inline int pick_vec(int dtype, int64_t k, std::initializer_list<const void *> ptrs) {
+    const int es = dtype == 1 ? 8 : 4;
+    int vec = 16 / es;
+    while (vec > 1) {
+        bool ok = (k % vec) == 0;
+        for (const void *p : ptrs) ok = ok && ((reinterpret_cast<uintptr_t>(p) % (vec * es)) == 0);
+        if (ok) break;
+        vec >>= 1;
+    }
+    return vec;
+}
+
+inline int pick_lpe(int64_t k, int vec) {
+    const int64_t need = (k + vec - 1) / vec;
+    int lpe = 1;
+    while (lpe < 32 && lpe < need) lpe <<= 1;
+    return lpe;
+}
+
+template <typename T, int VEC, int LPE, int MODE>
+int run_segments(const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
+                 cudaStream_t st) {
+    auto kern = k_segments<T, VEC, LPE, MODE>;
+    static int bps = 0;
+    if (bps == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+        if (bps <= 0) bps = 1;
+    }
+    const int64_t nbatch = (L.nseg + LPE - 1) / LPE;
+    const int64_t sub_per_block = 256 / LPE;
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * bps, (nbatch + sub_per_block - 1) / sub_per_block);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_beg, L.nseg, L.ent_col,
+                                            reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                            reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
+                                            reinterpret_cast<T *>(C0), k);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int VEC, int MODE>
+int run_segments_lpe(int lpe, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+                     int num_sms, cudaStream_t st) {
+    switch (lpe) {
+        case 32: return run_segments<T, VEC, 32, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+        case 16: return run_segments<T, VEC, 16, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+        case 8: return run_segments<T, VEC, 8, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+        case 4: return run_segments<T, VEC, 4, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+        case 2: return run_segments<T, VEC, 2, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+        default: return run_segments<T, VEC, 1, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+    }
+}
+
+template <typename T, int VEC>
+int run_segments_mode(int lpe, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+                      int num_sms, cudaStream_t st) {
+    return L.mode == 0 ? run_segments_lpe<T, VEC, 0>(lpe, L, X, D0, Y, C0, k, num_sms, st)
+                       : run_segments_lpe<T, VEC, 1>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+}
+
+inline unsigned grid_for(int64_t total) {
+    int64_t g = (total + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+}  // namespace
+
+int launch_segments(int dtype, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+                    int num_sms, void *stream) {
+    if (L.nseg == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {X, Y, D0, C0});
+    const int lpe = pick_lpe(k, vec);
+    if (dtype == 0) {
+        if (vec == 4) return run_segments_mode<float, 4>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+        if (vec == 2) return run_segments_mode<float, 2>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+        return run_segments_mode<float, 1>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+    }
+    if (vec == 2) return run_segments_mode<double, 2>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+    return run_segments_mode<double, 1>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+}
+
+int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k, void *D0, void *C0,
+                      void *stream) {
+    if (h == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {X, D0, C0});
+    const unsigned g = grid_for(h * (k / vec));
+    if (dtype == 0) {
+        if (vec == 4) k_head_stage<float, 4><<<g, 256, 0, st>>>((const float *)X, head_rows, h, k, (float *)D0, (float *)C0);
+        else if (vec == 2) k_head_stage<float, 2><<<g, 256, 0, st>>>((const float *)X, head_rows, h, k, (float *)D0, (float *)C0);
+        else k_head_stage<float, 1><<<g, 256, 0, st>>>((const float *)X, head_rows, h, k, (float *)D0, (float *)C0);
+    } else {
+        if (vec == 2) k_head_stage<double, 2><<<g, 256, 0, st>>>((const double *)X, head_rows, h, k, (double *)D0, (double *)C0);
+        else k_head_stage<double, 1><<<g, 256, 0, st>>>((const double *)X, head_rows, h, k, (double *)D0, (double *)C0);
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k, int add, void *Y,
+                         void *stream) {
+    if (h == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {C0, Y});
+    const unsigned g = grid_for(h * (k / vec));
+    if (dtype == 0) {
+        if (vec == 4) k_head_epilogue<float, 4><<<g, 256, 0, st>>>((const float *)C0, head_rows, h, k, add, (float *)Y);
+        else if (vec == 2) k_head_epilogue<float, 2><<<g, 256, 0, st>>>((const float *)C0, head_rows, h, k, add, (float *)Y);
+        else k_head_epilogue<float, 1><<<g, 256, 0, st>>>((const float *)C0, head_rows, h, k, add, (float *)Y);
+    } else {
+        if (vec == 2) k_head_epilogue<double, 2><<<g, 256, 0, st>>>((const double *)C0, head_rows, h, k, add, (double *)Y);
+        else k_head_epilogue<double, 1><<<g, 256, 0, st>>>((const double *)C0, head_rows, h, k, add, (double *)Y);
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_zero(void *Y, int64_t bytes, void *stream) {
+    if (bytes == 0) return 0;
+    return (int)cudaMemsetAsync(Y, 0, (size_t)bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // namespace arrow
