@@ -64,6 +64,7 @@ struct arrow_plan_s {
     // device memory
     void *arena = nullptr;
     int64_t arena_bytes = 0;
+    unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
     void *ws = nullptr;          // D0 | C0
     int64_t ws_k = 0;
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
@@ -105,10 +106,11 @@ namespace {
 
 struct BuiltLevel {
     std::vector<int32_t> seg_out;
-    std::vector<uint32_t> seg_beg;
+    std::vector<uint32_t> seg_end;
     std::vector<int32_t> ent_col;
     std::vector<uint8_t> ent_val;  // plan dtype
     std::vector<int32_t> head_rows;
+    std::vector<int32_t> zero_rows;
     int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
     int mode = 0;
 };
@@ -122,9 +124,12 @@ inline void put_val(std::vector<uint8_t> &dst, int64_t at, arrow_dtype pdt, doub
     }
 }
 
-// Window-ordered segments of one arrow level (see arrow_internal.h for the encoding).
+// Window-ordered non-empty segments of one arrow level (encoding: arrow_internal.h).
+//   dist = 0: head columns read X directly, head-row partials add into Y[perm_i[j]];
+//             level 0 zeroes head rows and entry-less rows first (zero_rows).
+//   dist = 1: head columns read the staged head block D0, head partials add into C0[j].
 void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_rows, int32_t head_chunk,
-                 const std::vector<int32_t> *pos0, arrow_dtype pdt, BuiltLevel &B) {
+                 const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, BuiltLevel &B) {
     const int64_t n_i = L.n_i, h = L.head, rows = L.rows;
     B.rows = rows;
     B.n_i = n_i;
@@ -134,39 +139,49 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
     B.tiles = (n_i + b - 1) / b;
     B.mode = level_idx == 0 ? 0 : 1;
     auto rowid = [&](int32_t v) -> int32_t { return pos0 ? (*pos0)[v] : v; };
-    auto colmap = [&](int32_t q) -> int32_t { return q < h ? (int32_t)(kFlag | (uint32_t)q) : rowid(L.perm[q]); };
+    auto colmap = [&](int32_t q) -> int32_t {
+        return (dist && q < h) ? (int32_t)(kFlag | (uint32_t)q) : rowid(L.perm[q]);
+    };
+    auto headout = [&](int64_t j) -> int32_t {
+        return (int32_t)(kFlag | (uint32_t)(dist ? j : rowid(L.perm[j])));
+    };
     B.head_rows.resize(h);
     for (int64_t j = 0; j < h; ++j) B.head_rows[j] = rowid(L.perm[j]);
+    if (level_idx == 0) {
+        if (!dist)
+            for (int64_t j = 0; j < h; ++j) B.zero_rows.push_back(rowid(L.perm[j]));
+        for (int64_t p = h; p < rows; ++p)
+            if (L.row_ptr[p + 1] == L.row_ptr[p]) B.zero_rows.push_back(rowid(L.perm[p]));
+    }
 
     const int64_t wt = std::max<int64_t>(1, window_rows / b);
     const int64_t W = wt * b;
     const int64_t NW = (n_i + W - 1) / W;
-    // count pass
-    std::vector<int64_t> wseg(NW + 2, 0), went(NW + 2, 0);
+    std::vector<int64_t> wseg(NW + 1, 0), went(NW + 1, 0);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t w = 0; w < NW; ++w) {
         const int64_t lo = w * W, hi = std::min(n_i, lo + W);
-        int64_t s = 0, e = 0;
-        for (int64_t p = std::max(h, lo); p < hi; ++p) { ++s; e += L.row_ptr[p + 1] - L.row_ptr[p]; }
+        int64_t sc = 0, ec = 0;
+        for (int64_t p = std::max(h, lo); p < hi; ++p) {
+            const int64_t c = L.row_ptr[p + 1] - L.row_ptr[p];
+            sc += c > 0 ? 1 : 0;
+            ec += c;
+        }
         for (int64_t j = 0; j < h; ++j) {
             const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
             const int64_t c = std::lower_bound(a, z, (int32_t)hi) - std::lower_bound(a, z, (int32_t)lo);
-            s += (c + head_chunk - 1) / head_chunk;
-            e += c;
+            sc += (c + head_chunk - 1) / head_chunk;
+            ec += c;
         }
-        wseg[w + 1] = s;
-        went[w + 1] = e;
+        wseg[w + 1] = sc;
+        went[w + 1] = ec;
     }
-    // zero rows (A-isolated vertices, level 0 only) go last
-    wseg[NW + 1] = rows - n_i;
-    went[NW + 1] = 0;
-    for (int64_t w = 0; w <= NW; ++w) { wseg[w + 1] += wseg[w]; went[w + 1] += went[w]; }
-    const int64_t nseg = wseg[NW + 1], nent = went[NW + 1];
+    for (int64_t w = 0; w < NW; ++w) { wseg[w + 1] += wseg[w]; went[w + 1] += went[w]; }
+    const int64_t nseg = wseg[NW], nent = went[NW];
     B.seg_out.resize(nseg);
-    B.seg_beg.resize(nseg + 1);
+    B.seg_end.resize(nseg);
     B.ent_col.resize(nent);
-    const size_t es = pdt == ARROW_F64 ? 8 : 4;
-    B.ent_val.resize(nent * es);
+    B.ent_val.resize(nent * (pdt == ARROW_F64 ? 8 : 4));
     auto emit_entry = [&](int64_t at, int64_t e) {
         B.ent_col[at] = colmap(L.col[e]);
         put_val(B.ent_val, at, pdt, L.val[e]);
@@ -176,10 +191,11 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
         const int64_t lo = w * W, hi = std::min(n_i, lo + W);
         int64_t s = wseg[w], e = went[w];
         for (int64_t p = std::max(h, lo); p < hi; ++p) {
-            B.seg_out[s] = rowid(L.perm[p]);
-            B.seg_beg[s] = (uint32_t)e;
-            ++s;
+            if (L.row_ptr[p + 1] == L.row_ptr[p]) continue;
             for (int64_t x = L.row_ptr[p]; x < L.row_ptr[p + 1]; ++x) emit_entry(e++, x);
+            B.seg_out[s] = rowid(L.perm[p]);
+            B.seg_end[s] = (uint32_t)e;
+            ++s;
         }
         for (int64_t j = 0; j < h; ++j) {
             const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
@@ -187,43 +203,32 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
             const int64_t x1 = L.row_ptr[j] + (std::lower_bound(a, z, (int32_t)hi) - a);
             while (x0 < x1) {
                 const int64_t x2 = std::min<int64_t>(x1, x0 + head_chunk);
-                B.seg_out[s] = (int32_t)(kFlag | (uint32_t)j);
-                B.seg_beg[s] = (uint32_t)e;
-                ++s;
                 for (int64_t x = x0; x < x2; ++x) emit_entry(e++, x);
+                B.seg_out[s] = headout(j);
+                B.seg_end[s] = (uint32_t)e;
+                ++s;
                 x0 = x2;
             }
         }
     }
-    {
-        int64_t s = wseg[NW];
-        for (int64_t p = n_i; p < rows; ++p) {
-            B.seg_out[s] = rowid(L.perm[p]);
-            B.seg_beg[s] = (uint32_t)nent;
-            ++s;
-        }
-    }
-    B.seg_beg[nseg] = (uint32_t)nent;
 }
 
 // Residual CSR level (ARROW_RESIDUAL_CSR): every row with leftover entries is one RMW segment.
 void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *pos0, arrow_dtype pdt, BuiltLevel &B) {
     auto rowid = [&](int32_t v) -> int32_t { return pos0 ? (*pos0)[v] : v; };
     const size_t m = D.res_u.size();
-    const size_t es = pdt == ARROW_F64 ? 8 : 4;
     B.mode = 1;
     B.nnz = (int64_t)m;
     B.ent_col.resize(m);
-    B.ent_val.resize(m * es);
+    B.ent_val.resize(m * (pdt == ARROW_F64 ? 8 : 4));
     for (size_t t = 0; t < m; ++t) {
-        if (t == 0 || D.res_u[t] != D.res_u[t - 1]) {
-            B.seg_out.push_back(rowid(D.res_u[t]));
-            B.seg_beg.push_back((uint32_t)t);
-        }
         B.ent_col[t] = rowid(D.res_v[t]);
         put_val(B.ent_val, (int64_t)t, pdt, D.res_a[t]);
+        if (t + 1 == m || D.res_u[t + 1] != D.res_u[t]) {
+            B.seg_out.push_back(rowid(D.res_u[t]));
+            B.seg_end.push_back((uint32_t)(t + 1));
+        }
     }
-    B.seg_beg.push_back((uint32_t)m);
     B.rows = (int64_t)B.seg_out.size();
     B.n_i = B.rows;
 }
@@ -370,7 +375,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         }
         built.resize(D.levels.size() + (D.res_u.empty() ? 0 : 1));
         for (size_t i = 0; i < D.levels.size(); ++i)
-            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, pos0p, pdt, built[i]);
+            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, pos0p, pdt, comm ? 1 : 0, built[i]);
         if (!D.res_u.empty()) build_residual(D, pos0p, pdt, built.back());
         P->residual_nnz = (int64_t)D.res_u.size();
         P->arrow_levels = (int32_t)D.levels.size();
@@ -407,15 +412,17 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         const size_t es = P->esize();
         int64_t total = 0;
         auto reserve = [&](int64_t bytes) { int64_t at = total; total += align_up(std::max<int64_t>(bytes, 1), 256); return at; };
-        std::vector<std::array<int64_t, 5>> offs(built.size());
+        std::vector<std::array<int64_t, 6>> offs(built.size());
         for (size_t i = 0; i < built.size(); ++i) {
             const BuiltLevel &B = built[i];
             offs[i][0] = reserve((int64_t)B.seg_out.size() * 4);
-            offs[i][1] = reserve((int64_t)B.seg_beg.size() * 4);
+            offs[i][1] = reserve((int64_t)B.seg_end.size() * 4);
             offs[i][2] = reserve((int64_t)B.ent_col.size() * 4);
             offs[i][3] = reserve((int64_t)B.ent_col.size() * (int64_t)es);
             offs[i][4] = reserve((int64_t)B.head_rows.size() * 4);
+            offs[i][5] = reserve((int64_t)B.zero_rows.size() * 4);
         }
+        const int64_t off_counters = reserve((int64_t)(built.size() + 1) * 4);
         if (total > 0) {
             cudaError_t e = cudaMalloc(&P->arena, (size_t)total);
             if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(plan arena): ") + cudaGetErrorString(e));
@@ -427,18 +434,22 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
             DeviceLevel L;
             L.rows = B.rows; L.n_i = B.n_i; L.head = B.head; L.nnz = B.nnz; L.head_nnz = B.head_nnz;
             L.tiles = B.tiles; L.nseg = (int64_t)B.seg_out.size(); L.mode = B.mode;
+            L.nzero = (int64_t)B.zero_rows.size();
             L.seg_out = reinterpret_cast<int32_t *>(base + offs[i][0]);
-            L.seg_beg = reinterpret_cast<uint32_t *>(base + offs[i][1]);
+            L.seg_end = reinterpret_cast<uint32_t *>(base + offs[i][1]);
             L.ent_col = reinterpret_cast<int32_t *>(base + offs[i][2]);
             L.ent_val = base + offs[i][3];
             L.head_rows = reinterpret_cast<int32_t *>(base + offs[i][4]);
+            L.zero_rows = reinterpret_cast<int32_t *>(base + offs[i][5]);
+            CUDA_TRY(cudaMemcpy(L.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(L.seg_out, B.seg_out.data(), B.seg_out.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.seg_beg, B.seg_beg.data(), B.seg_beg.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.seg_end, B.seg_end.data(), B.seg_end.size() * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(L.ent_col, B.ent_col.data(), B.ent_col.size() * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(L.ent_val, B.ent_val.data(), B.ent_val.size(), cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(L.head_rows, B.head_rows.data(), B.head_rows.size() * 4, cudaMemcpyHostToDevice));
             P->levels.push_back(L);
         }
+        P->counters = reinterpret_cast<unsigned *>(base + off_counters);
     }
     P->local_begin = 0;
     P->local_end = n;
@@ -704,38 +715,34 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     const int64_t bytes = rows * k * (int64_t)P->esize();
     const char *xa = (const char *)X, *ya = (const char *)Y;
     if (xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
-    arrow_status s = ensure_ws(P, k);
-    if (s != ARROW_OK) return s;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (P->comm) return comm_spmm(P, X, Y, k, st);
+    if (P->comm) {
+        arrow_status s = ensure_ws(P, k);
+        if (s != ARROW_OK) return s;
+        return comm_spmm(P, X, Y, k, st);
+    }
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
-    char *D0 = reinterpret_cast<char *>(P->ws);
-    char *C0 = D0 + align_up(std::max<int64_t>(P->max_head, 1) * k * (int64_t)P->esize(), 256);
     if (P->levels.empty()) {
         int e = launch_zero(Y, bytes, st);
         if (e) return fail(ARROW_E_CUDA, cudaGetErrorString((cudaError_t)e));
+        return ARROW_OK;
     }
     if (P->profiling) P->prof_acc.calls += 1;
+    CUDA_TRY(cudaMemsetAsync(P->counters, 0, P->levels.size() * sizeof(unsigned), st));
     for (size_t i = 0; i < P->levels.size(); ++i) {
         const DeviceLevel &L = P->levels[i];
         cudaEvent_t a = nullptr;
         int e = 0;
-        if (L.head > 0) {
+        if (L.nzero > 0) {  // S0/S3 single GPU: head rows and entry-less rows of level 0 start at zero
             prof_begin(P, st, a);
-            e = launch_head_stage(dt, X, L.head_rows, L.head, k, D0, C0, st);
+            e = launch_zero_rows(dt, L.zero_rows, L.nzero, k, Y, st);
             prof_end(P, st, ARROW_K_HEAD_STAGE, a);
-            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-H: ") + cudaGetErrorString((cudaError_t)e)); }
+            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
-        e = launch_segments(dt, L, X, D0, Y, C0, k, P->num_sms, st);
+        e = launch_segments(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
-        if (L.head > 0) {
-            prof_begin(P, st, a);
-            e = launch_head_epilogue(dt, C0, L.head_rows, L.head, k, L.mode, Y, st);
-            prof_end(P, st, ARROW_K_HEAD_EPI, a);
-            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-C: ") + cudaGetErrorString((cudaError_t)e)); }
-        }
     }
     return ARROW_OK;
 }

@@ -35,36 +35,39 @@ int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *
 int check_symmetric(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &err);
 
 // ------------------------------------------------------------------ device layout of one level
-// Work is a stream of "segments": a segment is a list of (column, value) entries whose sum
-// sum_e val_e * src_row(col_e) goes to one output row.
-//   out >= 0 : Y row `out` (body row p >= h_i of B_i, folded: out = perm_i[p] or its pi_0 position)
-//   out <  0 : head accumulator row (out & 0x7fffffff) = j, partial sum of head row j restricted
-//              to one tile window (Alg. 1 line 2, C^(0) = sum_t B^(0,t) D^(t))
-//   col >= 0 : X row col (folded permutation: P_pi^T X never materialised, S4)
-//   col <  0 : head block row (col & 0x7fffffff) of D0 = X[head_i] (Alg. 1 line 1)
-// Segments are ordered by tile window so that concurrently running warps touch the same
-// X rows (L2 reuse, the IO lemma's "tiles stay resident").
+// Work is a stream of non-empty "segments": a segment is a list of (column, value) entries whose
+// sum  sum_e val_e * src_row(col_e)  goes to one output row.
+//   out >= 0 : Y row `out` (body row p >= h_i of B_i; folded: out = perm_i[p] or its pi_0 position)
+//   out <  0 : head-row partial restricted to one tile window (Alg. 1 line 2, C^(0) = sum_t B^(0,t) D^(t),
+//              P:464), added atomically: single GPU -> Y row (out & 0x7fffffff) = perm_i[j];
+//              distributed -> C0 row j (reduced over ranks, then written by the head epilogue)
+//   col >= 0 : X row col (folded permutation: P_pi^T X is never materialised, S4)
+//   col <  0 : (distributed only) head block row (col & 0x7fffffff) of D0 = X[head_i]
+// Segments are ordered by tile window so that concurrently running warps touch the same X rows
+// (L2 reuse, the IO lemma's "tiles stay resident").
 constexpr uint32_t kFlag = 0x80000000u;
 
 struct DeviceLevel {
     int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
-    int64_t nseg = 0;
+    int64_t nseg = 0, nzero = 0;
     int mode = 0;                 // 0: level 0 stores Y rows; 1: levels >= 1 read-modify-write (S5)
     // device pointers (into the plan arena)
     int32_t *seg_out = nullptr;   // [nseg]
-    uint32_t *seg_beg = nullptr;  // [nseg + 1]
+    uint32_t *seg_end = nullptr;  // [nseg]  end offset of each segment (begin = previous end)
     int32_t *ent_col = nullptr;   // [nnz]
     void *ent_val = nullptr;      // [nnz] of dtype
     int32_t *head_rows = nullptr; // [head] X/Y row of head vertex j
+    int32_t *zero_rows = nullptr; // [nzero] level 0: Y rows written as 0 before the level runs
 };
 
 // kernels.cu launchers (all on `stream`; return cudaError_t as int)
 int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k,
                       void *D0, void *C0, void *stream);
-int launch_segments(int dtype, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                    int64_t k, int num_sms, void *stream);
+int launch_segments(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
+                    int64_t k, int num_sms, unsigned *counter, void *stream);
 int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k,
                          int add, void *Y, void *stream);
+int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream);
 int launch_zero(void *Y, int64_t bytes, void *stream);
 
 }  // namespace arrow

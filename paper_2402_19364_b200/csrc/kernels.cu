@@ -86,34 +86,49 @@ __device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
 }
 
 // ------------------------------------------------------------------------------------ K-A
-// Segment stream: sub-warp `sw` takes batches of LPE consecutive segments, grid-strided so that
-// all sub-warps advance through the (window-ordered) segment list together.  Lane l of the
-// sub-warp holds descriptor l of the batch; the batch's entries are contiguous and are streamed
-// in chunks of LPE (one coalesced load of col/val per lane), broadcast with shuffles, and
-// consumed UNROLL at a time with all UNROLL row loads issued before any FMA -- independent of
-// where segment boundaries fall, so short rows do not serialise on latency.
-template <typename T, int VEC, int LPE, int MODE>
-__global__ void __launch_bounds__(256) k_segments(const int32_t *__restrict__ seg_out,
-                                                  const uint32_t *__restrict__ seg_beg, int64_t nseg,
-                                                  const int32_t *__restrict__ ent_col,
-                                                  const T *__restrict__ ent_val, const T *__restrict__ X,
-                                                  const T *__restrict__ D0, T *__restrict__ Y,
-                                                  T *__restrict__ C0, int64_t k) {
-    constexpr int UNROLL = (LPE >= 8) ? 8 : 4;
+// Segment stream.  A sub-warp of LPE lanes owns a row slab of LPE*VEC elements.  Work is a list
+// of non-empty segments in tile-window order, cut into batches of LPE consecutive segments.
+// Warps grab batches dynamically from a per-launch counter (one atomic per warp per grab), so
+// all resident warps work on a narrow, advancing front of the window-ordered list and the X rows
+// of the current window stay L2-resident while every user of them runs (the IO lemma's "tiles
+// stay resident").  Lane s of a sub-warp holds the output row and end offset of
+// segment s of its batch; the batch's entries are contiguous and are streamed in chunks of LPE
+// (one coalesced load of col and val per lane).  A per-chunk bit mask of segment ends
+// (__reduce_or_sync) tells the accumulate loop where to flush; UNROLL row loads are issued
+// before their FMAs so short rows do not serialise on latency.
+//   out >= 0             : store (MODE 0, level 0) or read-modify-write (MODE 1) Y[out]
+//   out <  0, DIST == 0  : atomic add into Y[out & 0x7fffffff]  (head-row slice of one window)
+//   out <  0, DIST == 1  : atomic add into C0[out & 0x7fffffff] (head partial, reduced over ranks)
+//   col <  0 (DIST only) : the row comes from the head block D0 (broadcast), else from X
+template <typename T, int VEC, int LPE, int MODE, int DIST>
+__global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__ seg_out,
+                                                     const uint32_t *__restrict__ seg_end, int64_t nseg,
+                                                     const int32_t *__restrict__ ent_col,
+                                                     const T *__restrict__ ent_val, const T *__restrict__ X,
+                                                     const T *__restrict__ D0, T *__restrict__ Y,
+                                                     T *__restrict__ C0, int64_t k, unsigned *__restrict__ counter) {
+    constexpr int UNROLL = (LPE == 32) ? 8 : 4;
     constexpr int SLAB = LPE * VEC;
+    constexpr int SUBS = 32 / LPE;
     const int lane = threadIdx.x & 31;
     const int sl = lane % LPE;
-    const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (lane - sl));
-    const int64_t nsub = (int64_t)gridDim.x * blockDim.x / LPE;
+    const int sub = lane / LPE;
+    const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (sub * LPE));
     const int64_t nbatch = (nseg + LPE - 1) / LPE;
 
-    for (int64_t bt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPE; bt < nbatch; bt += nsub) {
+    for (;;) {
+        unsigned wb = 0;
+        if (lane == 0) wb = atomicAdd(counter, 1u);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        const int64_t bt = (int64_t)wb * SUBS + sub;
+        if ((int64_t)wb * SUBS >= nbatch) break;       // warp-uniform exit
+        if (bt >= nbatch) continue;                    // sub-warp idle this round
         const int64_t s0 = bt * LPE;
         const int nb = (nseg - s0 < LPE) ? (int)(nseg - s0) : LPE;
         const int32_t my_out = (sl < nb) ? __ldg(seg_out + s0 + sl) : 0;
-        const uint32_t my_beg = __ldg(seg_beg + s0 + (sl < nb ? sl : nb));
-        const uint32_t e_end = __ldg(seg_beg + s0 + nb);
-        const uint32_t e_begin = __shfl_sync(mask, my_beg, 0, LPE);
+        const uint32_t my_end = (sl < nb) ? __ldg(seg_end + s0 + sl) : 0xffffffffu;
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(mask, my_end, nb - 1, LPE);
 
         for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
             const int64_t col0 = c0 + (int64_t)sl * VEC;
@@ -121,25 +136,6 @@ __global__ void __launch_bounds__(256) k_segments(const int32_t *__restrict__ se
             Frag<T, VEC> acc;
             acc.zero();
             int cur = 0;
-            uint32_t cend = (nb > 1) ? __shfl_sync(mask, my_beg, 1, LPE) : e_end;
-
-            auto flush = [&](int s) {
-                const int32_t o = __shfl_sync(mask, my_out, s, LPE);
-                if (active) {
-                    if (o < 0) {
-                        atomic_add_frag<T, VEC>(C0 + (int64_t)(o & 0x7fffffff) * k + col0, acc);
-                    } else if (MODE == 0) {
-                        st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
-                    } else {
-                        T *p = Y + (int64_t)o * k + col0;
-                        Frag<T, VEC> y = ld_plain<T, VEC>(p);
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
-                        st_plain<T, VEC>(p, y);
-                    }
-                }
-            };
-
             for (uint32_t cb = e_begin; cb < e_end; cb += LPE) {
                 const int cnt = (e_end - cb < (uint32_t)LPE) ? (int)(e_end - cb) : LPE;
                 int32_t mycol = 0;
@@ -148,6 +144,8 @@ __global__ void __launch_bounds__(256) k_segments(const int32_t *__restrict__ se
                     mycol = __ldcs(ent_col + cb + sl);
                     myval = __ldcs(ent_val + cb + sl);
                 }
+                const uint32_t rel = my_end - 1u - cb;  // position of my segment's last entry in this chunk
+                const unsigned endmask = __reduce_or_sync(mask, (rel < (uint32_t)LPE) ? (1u << rel) : 0u);
 #pragma unroll 1
                 for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
                     Frag<T, VEC> xv[UNROLL];
@@ -156,9 +154,12 @@ __global__ void __launch_bounds__(256) k_segments(const int32_t *__restrict__ se
                     for (int t = 0; t < UNROLL; ++t) {
                         const int idx = u0 + t;
                         const int32_t cc = __shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
-                        av[t] = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
+                        const T a = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
+                        av[t] = (idx < cnt) ? a : T(0);
                         if (idx < cnt && active) {
-                            const T *base = (cc < 0) ? D0 + (int64_t)(cc & 0x7fffffff) * k : X + (int64_t)cc * k;
+                            const T *base;
+                            if (DIST) base = (cc < 0) ? D0 + (int64_t)(cc & 0x7fffffff) * k : X + (int64_t)cc * k;
+                            else base = X + (int64_t)cc * k;
                             xv[t] = ld_x<T, VEC>(base + col0);
                         } else {
                             xv[t].zero();
@@ -166,26 +167,45 @@ __global__ void __launch_bounds__(256) k_segments(const int32_t *__restrict__ se
                     }
 #pragma unroll
                     for (int t = 0; t < UNROLL; ++t) {
-                        if (u0 + t < cnt) {
-                            const uint32_t e = cb + u0 + t;
-                            while (e >= cend) {        // segment boundary (sub-warp uniform)
-                                flush(cur);
-                                acc.zero();
-                                ++cur;
-                                cend = (cur + 1 < nb) ? __shfl_sync(mask, my_beg, cur + 1, LPE) : e_end;
-                            }
 #pragma unroll
-                            for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        if ((endmask >> ((u0 + t) & 31)) & 1u & (u0 + t < cnt)) {   // sub-warp uniform
+                            const int32_t o = __shfl_sync(mask, my_out, cur, LPE);
+                            if (active) {
+                                if (o < 0) {
+                                    T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
+                                    atomic_add_frag<T, VEC>(dst + col0, acc);
+                                } else if (MODE == 0) {
+                                    st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
+                                } else {
+                                    T *p = Y + (int64_t)o * k + col0;
+                                    Frag<T, VEC> y = ld_plain<T, VEC>(p);
+#pragma unroll
+                                    for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                    st_plain<T, VEC>(p, y);
+                                }
+                            }
+                            acc.zero();
+                            ++cur;
                         }
                     }
                 }
             }
-            while (cur < nb) {  // last segment and trailing empty segments (zero rows)
-                flush(cur);
-                acc.zero();
-                ++cur;
-            }
         }
+    }
+}
+
+// K-Z: zero the listed Y rows (level 0: head rows, which then accumulate head slices atomically,
+// and rows with no entry in B_0, incl. A-isolated vertices).
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_zero_rows(const int32_t *__restrict__ rows, int64_t nrows, int64_t k,
+                                                   T *__restrict__ Y) {
+    const int64_t kv = k / VEC, total = nrows * kv;
+    Frag<T, VEC> z;
+    z.zero();
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / kv, c = (t - j * kv) * VEC;
+        st_stream<T, VEC>(Y + (int64_t)__ldg(rows + j) * k + c, z);
     }
 }
 
@@ -241,44 +261,48 @@ inline int pick_lpe(int64_t k, int vec) {
     return lpe;
 }
 
-template <typename T, int VEC, int LPE, int MODE>
+template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segments(const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-                 cudaStream_t st) {
-    auto kern = k_segments<T, VEC, LPE, MODE>;
+                 unsigned *counter, cudaStream_t st) {
+    auto kern = k_segments<T, VEC, LPE, MODE, DIST>;
     static int bps = 0;
     if (bps == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
         if (bps <= 0) bps = 1;
     }
     const int64_t nbatch = (L.nseg + LPE - 1) / LPE;
-    const int64_t sub_per_block = 256 / LPE;
-    int64_t blocks = std::min<int64_t>((int64_t)num_sms * bps, (nbatch + sub_per_block - 1) / sub_per_block);
+    const int64_t batches_per_block = 8 * (32 / LPE);
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * bps, (nbatch + batches_per_block - 1) / batches_per_block);
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_beg, L.nseg, L.ent_col,
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
                                             reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
                                             reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
-                                            reinterpret_cast<T *>(C0), k);
+                                            reinterpret_cast<T *>(C0), k, counter);
     return (int)cudaGetLastError();
 }
 
-template <typename T, int VEC, int MODE>
+template <typename T, int VEC, int MODE, int DIST>
 int run_segments_lpe(int lpe, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                     int num_sms, cudaStream_t st) {
+                     int num_sms, unsigned *counter, cudaStream_t st) {
     switch (lpe) {
-        case 32: return run_segments<T, VEC, 32, MODE>(L, X, D0, Y, C0, k, num_sms, st);
-        case 16: return run_segments<T, VEC, 16, MODE>(L, X, D0, Y, C0, k, num_sms, st);
-        case 8: return run_segments<T, VEC, 8, MODE>(L, X, D0, Y, C0, k, num_sms, st);
-        case 4: return run_segments<T, VEC, 4, MODE>(L, X, D0, Y, C0, k, num_sms, st);
-        case 2: return run_segments<T, VEC, 2, MODE>(L, X, D0, Y, C0, k, num_sms, st);
-        default: return run_segments<T, VEC, 1, MODE>(L, X, D0, Y, C0, k, num_sms, st);
+        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
+        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
+        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
+        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
+        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
+        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
     }
 }
 
 template <typename T, int VEC>
-int run_segments_mode(int lpe, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                      int num_sms, cudaStream_t st) {
-    return L.mode == 0 ? run_segments_lpe<T, VEC, 0>(lpe, L, X, D0, Y, C0, k, num_sms, st)
-                       : run_segments_lpe<T, VEC, 1>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+int run_segments_mode(int lpe, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
+                      int64_t k, int num_sms, unsigned *counter, cudaStream_t st) {
+    if (dist) {
+        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st)
+                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st);
+    }
+    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st)
+                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st);
 }
 
 inline unsigned grid_for(int64_t total) {
@@ -290,19 +314,35 @@ inline unsigned grid_for(int64_t total) {
 
 }  // namespace
 
-int launch_segments(int dtype, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                    int num_sms, void *stream) {
+int launch_segments(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
+                    int64_t k, int num_sms, unsigned *counter, void *stream) {
     if (L.nseg == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int vec = pick_vec(dtype, k, {X, Y, D0, C0});
+    const int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
     const int lpe = pick_lpe(k, vec);
     if (dtype == 0) {
-        if (vec == 4) return run_segments_mode<float, 4>(lpe, L, X, D0, Y, C0, k, num_sms, st);
-        if (vec == 2) return run_segments_mode<float, 2>(lpe, L, X, D0, Y, C0, k, num_sms, st);
-        return run_segments_mode<float, 1>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
+        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
+        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
     }
-    if (vec == 2) return run_segments_mode<double, 2>(lpe, L, X, D0, Y, C0, k, num_sms, st);
-    return run_segments_mode<double, 1>(lpe, L, X, D0, Y, C0, k, num_sms, st);
+    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
+    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
+}
+
+int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream) {
+    if (nrows == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {Y});
+    const unsigned g = grid_for(nrows * (k / vec));
+    if (dtype == 0) {
+        if (vec == 4) k_zero_rows<float, 4><<<g, 256, 0, st>>>(rows, nrows, k, (float *)Y);
+        else if (vec == 2) k_zero_rows<float, 2><<<g, 256, 0, st>>>(rows, nrows, k, (float *)Y);
+        else k_zero_rows<float, 1><<<g, 256, 0, st>>>(rows, nrows, k, (float *)Y);
+    } else {
+        if (vec == 2) k_zero_rows<double, 2><<<g, 256, 0, st>>>(rows, nrows, k, (double *)Y);
+        else k_zero_rows<double, 1><<<g, 256, 0, st>>>(rows, nrows, k, (double *)Y);
+    }
+    return (int)cudaGetLastError();
 }
 
 int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k, void *D0, void *C0,
