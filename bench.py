@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
+    ap.add_argument("--batch-segments", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -215,7 +216,7 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         comm = ab.Comm(world, rank, uid[0])
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm,
-                   window_rows=args.window_rows, head_chunk=args.head_chunk)
+                   window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments)
     info = plan.info()
     lo, hi = plan.local_begin, plan.local_end
     if comm is not None:

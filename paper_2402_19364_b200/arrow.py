@@ -52,7 +52,7 @@ class CSR(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("compute", ctypes.c_int), ("seed", ctypes.c_uint64), ("order", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("window_rows", ctypes.c_int64), ("head_chunk", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 7)]
+                ("batch_segments", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -156,7 +156,7 @@ def _dtype_code(dtype) -> int:
 
 
 def options(dtype=None, seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
-            head_chunk: int = 0) -> Options:
+            head_chunk: int = 0, batch_segments: int = 0) -> Options:
     o = Options()
     _check(lib().arrow_options_default(ctypes.byref(o)), "arrow_options_default")
     o.compute = _dtype_code(dtype)
@@ -165,6 +165,7 @@ def options(dtype=None, seed: int = 4, order: str = "original", residual: str = 
     o.residual = RESIDUAL[residual]
     o.window_rows = window_rows
     o.head_chunk = head_chunk
+    o.batch_segments = batch_segments
     return o
 
 
@@ -263,9 +264,10 @@ class Plan:
 
     def __init__(self, n=None, row_ptr=None, col=None, val=None, b: int = 2, levels: int = 0, dtype=None,
                  seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
-                 head_chunk: int = 0, comm=None, decomposition: Optional[Decomposition] = None):
+                 head_chunk: int = 0, batch_segments: int = 0, comm=None,
+                 decomposition: Optional[Decomposition] = None):
         self._h = ctypes.c_void_p()
-        opt = options(dtype, seed, order, residual, window_rows, head_chunk)
+        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments)
         comm_h = comm.handle if comm is not None else None
         if decomposition is not None:
             _check(lib().arrow_plan_create_from(decomposition._h, ctypes.byref(opt), comm_h, ctypes.byref(self._h)),

@@ -64,6 +64,7 @@ struct arrow_plan_s {
     // device memory
     void *arena = nullptr;
     int64_t arena_bytes = 0;
+    int batch_segments = 0;        // segments per K-A batch (0: one per lane of a sub-warp)
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
     void *ws = nullptr;          // D0 | C0
     int64_t ws_k = 0;
@@ -345,7 +346,8 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     const arrow_dtype pdt = (opt.compute == ARROW_F32 || opt.compute == ARROW_F64) ? opt.compute : default_dt;
     if (opt.order != ARROW_ORDER_ORIGINAL && opt.order != ARROW_ORDER_PERMUTED)
         return fail(ARROW_E_INVALID_ARG, "bad options.order");
-    if (opt.window_rows < 0 || opt.head_chunk < 0) return fail(ARROW_E_INVALID_ARG, "negative window/chunk");
+    if (opt.window_rows < 0 || opt.head_chunk < 0 || opt.batch_segments < 0)
+        return fail(ARROW_E_INVALID_ARG, "negative window/chunk/batch");
     const int64_t window_rows = opt.window_rows > 0 ? opt.window_rows : kDefaultWindowRows;
     const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : kDefaultHeadChunk;
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
@@ -361,6 +363,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, dev));
         P->dtype = pdt;
         P->order = order;
+        P->batch_segments = opt.batch_segments;
         P->n = n;
         P->b = b;
         P->isolated = D.isolated;
@@ -740,7 +743,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
-        e = launch_segments(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
+        e = launch_segments(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->batch_segments, st);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
     }

@@ -64,7 +64,7 @@ struct DeviceLevel {
 int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k,
                       void *D0, void *C0, void *stream);
 int launch_segments(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                    int64_t k, int num_sms, unsigned *counter, void *stream);
+                    int64_t k, int num_sms, unsigned *counter, int bseg, void *stream);
 int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k,
                          int add, void *Y, void *stream);
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream);

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
                                                      const int32_t *__restrict__ ent_col,
                                                      const T *__restrict__ ent_val, const T *__restrict__ X,
                                                      const T *__restrict__ D0, T *__restrict__ Y,
-                                                     T *__restrict__ C0, int64_t k, unsigned *__restrict__ counter) {
+                                                     T *__restrict__ C0, int64_t k, unsigned *__restrict__ counter,
+                                                     int bseg) {
     constexpr int UNROLL = (LPE == 32) ? 8 : 4;
     constexpr int SLAB = LPE * VEC;
     constexpr int SUBS = 32 / LPE;
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
     const int sl = lane % LPE;
     const int sub = lane / LPE;
     const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (sub * LPE));
-    const int64_t nbatch = (nseg + LPE - 1) / LPE;
+    const int64_t nbatch = (nseg + bseg - 1) / bseg;
+    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
 
     for (;;) {
         unsigned wb = 0;
@@ -123,8 +125,8 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
         const int64_t bt = (int64_t)wb * SUBS + sub;
         if ((int64_t)wb * SUBS >= nbatch) break;       // warp-uniform exit
         if (bt >= nbatch) continue;                    // sub-warp idle this round
-        const int64_t s0 = bt * LPE;
-        const int nb = (nseg - s0 < LPE) ? (int)(nseg - s0) : LPE;
+        const int64_t s0 = bt * bseg;
+        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
         const int32_t my_out = (sl < nb) ? __ldg(seg_out + s0 + sl) : 0;
         const uint32_t my_end = (sl < nb) ? __ldg(seg_end + s0 + sl) : 0xffffffffu;
         const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
@@ -133,6 +135,8 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
         for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
             const int64_t col0 = c0 + (int64_t)sl * VEC;
             const bool active = col0 < k;
+            const char *xlane = reinterpret_cast<const char *>(X + (active ? col0 : 0));
+            const char *dlane = reinterpret_cast<const char *>(D0 + (active ? col0 : 0));
             Frag<T, VEC> acc;
             acc.zero();
             int cur = 0;
@@ -153,23 +157,21 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
 #pragma unroll
                     for (int t = 0; t < UNROLL; ++t) {
                         const int idx = u0 + t;
-                        const int32_t cc = __shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
+                        const uint32_t cc = (uint32_t)__shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
                         const T a = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
-                        av[t] = (idx < cnt) ? a : T(0);
-                        if (idx < cnt && active) {
-                            const T *base;
-                            if (DIST) base = (cc < 0) ? D0 + (int64_t)(cc & 0x7fffffff) * k : X + (int64_t)cc * k;
-                            else base = X + (int64_t)cc * k;
-                            xv[t] = ld_x<T, VEC>(base + col0);
-                        } else {
-                            xv[t].zero();
-                        }
+                        const bool ok = idx < cnt;
+                        av[t] = ok ? a : T(0);
+                        const char *p;
+                        if (DIST && (int32_t)cc < 0) p = dlane + (uint64_t)(cc & 0x7fffffffu) * rowbytes;
+                        else p = xlane + (uint64_t)cc * rowbytes;
+                        if (ok && active) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
+                        else xv[t].zero();
                     }
 #pragma unroll
                     for (int t = 0; t < UNROLL; ++t) {
 #pragma unroll
                         for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
-                        if ((endmask >> ((u0 + t) & 31)) & 1u & (u0 + t < cnt)) {   // sub-warp uniform
+                        if ((u0 + t < cnt) && ((endmask >> ((u0 + t) & 31)) & 1u)) {   // sub-warp uniform
                             const int32_t o = __shfl_sync(mask, my_out, cur, LPE);
                             if (active) {
                                 if (o < 0) {
@@ -178,11 +180,11 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
                                 } else if (MODE == 0) {
                                     st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
                                 } else {
-                                    T *p = Y + (int64_t)o * k + col0;
-                                    Frag<T, VEC> y = ld_plain<T, VEC>(p);
+                                    T *py = Y + (int64_t)o * k + col0;
+                                    Frag<T, VEC> y = ld_plain<T, VEC>(py);
 #pragma unroll
                                     for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
-                                    st_plain<T, VEC>(p, y);
+                                    st_plain<T, VEC>(py, y);
                                 }
                             }
                             acc.zero();
@@ -263,46 +265,47 @@ inline int pick_lpe(int64_t k, int vec) {
 
 template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segments(const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-                 unsigned *counter, cudaStream_t st) {
+                 unsigned *counter, int bseg, cudaStream_t st) {
+    if (bseg <= 0 || bseg > LPE) bseg = LPE;
     auto kern = k_segments<T, VEC, LPE, MODE, DIST>;
     static int bps = 0;
     if (bps == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
         if (bps <= 0) bps = 1;
     }
-    const int64_t nbatch = (L.nseg + LPE - 1) / LPE;
+    const int64_t nbatch = (L.nseg + bseg - 1) / bseg;
     const int64_t batches_per_block = 8 * (32 / LPE);
     int64_t blocks = std::min<int64_t>((int64_t)num_sms * bps, (nbatch + batches_per_block - 1) / batches_per_block);
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
                                             reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
                                             reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
-                                            reinterpret_cast<T *>(C0), k, counter);
+                                            reinterpret_cast<T *>(C0), k, counter, bseg);
     return (int)cudaGetLastError();
 }
 
 template <typename T, int VEC, int MODE, int DIST>
 int run_segments_lpe(int lpe, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                     int num_sms, unsigned *counter, cudaStream_t st) {
+                     int num_sms, unsigned *counter, int bseg, cudaStream_t st) {
     switch (lpe) {
-        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
-        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
-        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
-        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
-        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
-        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, st);
+        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
     }
 }
 
 template <typename T, int VEC>
 int run_segments_mode(int lpe, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                      int64_t k, int num_sms, unsigned *counter, cudaStream_t st) {
+                      int64_t k, int num_sms, unsigned *counter, int bseg, cudaStream_t st) {
     if (dist) {
-        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st)
-                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st);
+        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st)
+                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
     }
-    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st)
-                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, st);
+    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st)
+                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
 }
 
 inline unsigned grid_for(int64_t total) {
@@ -315,18 +318,18 @@ inline unsigned grid_for(int64_t total) {
 }  // namespace
 
 int launch_segments(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                    int64_t k, int num_sms, unsigned *counter, void *stream) {
+                    int64_t k, int num_sms, unsigned *counter, int bseg, void *stream) {
     if (L.nseg == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
     const int lpe = pick_lpe(k, vec);
     if (dtype == 0) {
-        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
-        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
-        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
+        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
     }
-    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
-    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, st);
+    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
 }
 
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream) {
