@@ -55,7 +55,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "arrow.h"), __file__]
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "arrow.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -66,8 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     inc_nccl, lib_nccl = nccl_paths()
     incs = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(CUDA, "include"), "-I", inc_nccl]
-    objs = []
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -78,7 +77,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if src.endswith(".cu"):
             with open(os.path.join(BUILD, "ptxas_" + os.path.basename(src) + ".txt"), "w") as f:
                 f.write(out)
-        objs.append(obj)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, sources()))
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp",
            "-L", lib_nccl, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib_nccl}"]

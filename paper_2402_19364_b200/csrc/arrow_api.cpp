@@ -36,6 +36,7 @@ arrow_status fail(arrow_status s, const std::string &msg) {
 
 constexpr int64_t kDefaultWindowRows = 65536;
 constexpr int32_t kDefaultHeadChunk = 256;
+constexpr int32_t kDefaultBatchRecords = 256;
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -64,7 +65,6 @@ struct arrow_plan_s {
     // device memory
     void *arena = nullptr;
     int64_t arena_bytes = 0;
-    int batch_segments = 0;        // segments per K-A batch (0: one per lane of a sub-warp)
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
     void *ws = nullptr;          // D0 | C0
     int64_t ws_k = 0;
@@ -106,13 +106,12 @@ struct arrow_decomposition_s {
 namespace {
 
 struct BuiltLevel {
-    std::vector<int32_t> seg_out;
-    std::vector<uint32_t> seg_end;
-    std::vector<int32_t> ent_col;
-    std::vector<uint8_t> ent_val;  // plan dtype
+    std::vector<uint32_t> keys;
+    std::vector<uint8_t> vals;     // plan dtype
+    std::vector<uint32_t> bstart;  // batch boundaries (record offsets)
     std::vector<int32_t> head_rows;
     std::vector<int32_t> zero_rows;
-    int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
+    int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0, nseg = 0;
     int mode = 0;
 };
 
@@ -125,12 +124,26 @@ inline void put_val(std::vector<uint8_t> &dst, int64_t at, arrow_dtype pdt, doub
     }
 }
 
-// Window-ordered non-empty segments of one arrow level (encoding: arrow_internal.h).
+// Cut the record stream into batches of >= target records, at pseudo records.
+void cut_batches(BuiltLevel &B, int32_t target) {
+    B.bstart.clear();
+    B.bstart.push_back(0);
+    const int64_t m = (int64_t)B.keys.size();
+    int64_t start = 0;
+    for (int64_t r = 0; r < m; ++r) {
+        if ((B.keys[r] & kPseudoRec) && (r + 1 - start >= target || r + 1 == m)) {
+            B.bstart.push_back((uint32_t)(r + 1));
+            start = r + 1;
+        }
+    }
+}
+
+// Window-ordered record stream of one arrow level (encoding: arrow_internal.h).
 //   dist = 0: head columns read X directly, head-row partials add into Y[perm_i[j]];
 //             level 0 zeroes head rows and entry-less rows first (zero_rows).
 //   dist = 1: head columns read the staged head block D0, head partials add into C0[j].
 void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_rows, int32_t head_chunk,
-                 const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, BuiltLevel &B) {
+                 int32_t batch_records, const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, BuiltLevel &B) {
     const int64_t n_i = L.n_i, h = L.head, rows = L.rows;
     B.rows = rows;
     B.n_i = n_i;
@@ -139,26 +152,26 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
     B.head_nnz = L.row_ptr[h];
     B.tiles = (n_i + b - 1) / b;
     B.mode = level_idx == 0 ? 0 : 1;
-    auto rowid = [&](int32_t v) -> int32_t { return pos0 ? (*pos0)[v] : v; };
-    auto colmap = [&](int32_t q) -> int32_t {
-        return (dist && q < h) ? (int32_t)(kFlag | (uint32_t)q) : rowid(L.perm[q]);
+    auto rowid = [&](int32_t v) -> uint32_t { return (uint32_t)(pos0 ? (*pos0)[v] : v); };
+    auto colkey = [&](int32_t q) -> uint32_t {
+        return (dist && q < h) ? (kAuxRec | (uint32_t)q) : rowid(L.perm[q]);
     };
-    auto headout = [&](int64_t j) -> int32_t {
-        return (int32_t)(kFlag | (uint32_t)(dist ? j : rowid(L.perm[j])));
+    auto headkey = [&](int64_t j) -> uint32_t {
+        return kPseudoRec | kAuxRec | (dist ? (uint32_t)j : rowid(L.perm[j]));
     };
     B.head_rows.resize(h);
-    for (int64_t j = 0; j < h; ++j) B.head_rows[j] = rowid(L.perm[j]);
+    for (int64_t j = 0; j < h; ++j) B.head_rows[j] = (int32_t)rowid(L.perm[j]);
     if (level_idx == 0) {
         if (!dist)
-            for (int64_t j = 0; j < h; ++j) B.zero_rows.push_back(rowid(L.perm[j]));
+            for (int64_t j = 0; j < h; ++j) B.zero_rows.push_back((int32_t)rowid(L.perm[j]));
         for (int64_t p = h; p < rows; ++p)
-            if (L.row_ptr[p + 1] == L.row_ptr[p]) B.zero_rows.push_back(rowid(L.perm[p]));
+            if (L.row_ptr[p + 1] == L.row_ptr[p]) B.zero_rows.push_back((int32_t)rowid(L.perm[p]));
     }
 
     const int64_t wt = std::max<int64_t>(1, window_rows / b);
     const int64_t W = wt * b;
     const int64_t NW = (n_i + W - 1) / W;
-    std::vector<int64_t> wseg(NW + 1, 0), went(NW + 1, 0);
+    std::vector<int64_t> wrec(NW + 1, 0), wseg(NW + 1, 0);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t w = 0; w < NW; ++w) {
         const int64_t lo = w * W, hi = std::min(n_i, lo + W);
@@ -175,28 +188,26 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
             ec += c;
         }
         wseg[w + 1] = sc;
-        went[w + 1] = ec;
+        wrec[w + 1] = ec + sc;
     }
-    for (int64_t w = 0; w < NW; ++w) { wseg[w + 1] += wseg[w]; went[w + 1] += went[w]; }
-    const int64_t nseg = wseg[NW], nent = went[NW];
-    B.seg_out.resize(nseg);
-    B.seg_end.resize(nseg);
-    B.ent_col.resize(nent);
-    B.ent_val.resize(nent * (pdt == ARROW_F64 ? 8 : 4));
-    auto emit_entry = [&](int64_t at, int64_t e) {
-        B.ent_col[at] = colmap(L.col[e]);
-        put_val(B.ent_val, at, pdt, L.val[e]);
-    };
+    for (int64_t w = 0; w < NW; ++w) { wrec[w + 1] += wrec[w]; wseg[w + 1] += wseg[w]; }
+    const int64_t nrec = wrec[NW];
+    B.nseg = wseg[NW];
+    B.keys.resize(nrec);
+    B.vals.assign(nrec * (pdt == ARROW_F64 ? 8 : 4), 0);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t w = 0; w < NW; ++w) {
         const int64_t lo = w * W, hi = std::min(n_i, lo + W);
-        int64_t s = wseg[w], e = went[w];
+        int64_t r = wrec[w];
+        auto entry = [&](int64_t e) {
+            B.keys[r] = colkey(L.col[e]);
+            put_val(B.vals, r, pdt, L.val[e]);
+            ++r;
+        };
         for (int64_t p = std::max(h, lo); p < hi; ++p) {
             if (L.row_ptr[p + 1] == L.row_ptr[p]) continue;
-            for (int64_t x = L.row_ptr[p]; x < L.row_ptr[p + 1]; ++x) emit_entry(e++, x);
-            B.seg_out[s] = rowid(L.perm[p]);
-            B.seg_end[s] = (uint32_t)e;
-            ++s;
+            for (int64_t x = L.row_ptr[p]; x < L.row_ptr[p + 1]; ++x) entry(x);
+            B.keys[r++] = kPseudoRec | rowid(L.perm[p]);
         }
         for (int64_t j = 0; j < h; ++j) {
             const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
@@ -204,34 +215,37 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
             const int64_t x1 = L.row_ptr[j] + (std::lower_bound(a, z, (int32_t)hi) - a);
             while (x0 < x1) {
                 const int64_t x2 = std::min<int64_t>(x1, x0 + head_chunk);
-                for (int64_t x = x0; x < x2; ++x) emit_entry(e++, x);
-                B.seg_out[s] = headout(j);
-                B.seg_end[s] = (uint32_t)e;
-                ++s;
+                for (int64_t x = x0; x < x2; ++x) entry(x);
+                B.keys[r++] = headkey(j);
                 x0 = x2;
             }
         }
     }
+    cut_batches(B, batch_records);
 }
 
 // Residual CSR level (ARROW_RESIDUAL_CSR): every row with leftover entries is one RMW segment.
-void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *pos0, arrow_dtype pdt, BuiltLevel &B) {
-    auto rowid = [&](int32_t v) -> int32_t { return pos0 ? (*pos0)[v] : v; };
+void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *pos0, arrow_dtype pdt,
+                    int32_t batch_records, BuiltLevel &B) {
+    auto rowid = [&](int32_t v) -> uint32_t { return (uint32_t)(pos0 ? (*pos0)[v] : v); };
     const size_t m = D.res_u.size();
     B.mode = 1;
     B.nnz = (int64_t)m;
-    B.ent_col.resize(m);
-    B.ent_val.resize(m * (pdt == ARROW_F64 ? 8 : 4));
+    const size_t es = pdt == ARROW_F64 ? 8 : 4;
+    B.vals.reserve((m + m / 2 + 1) * es);
     for (size_t t = 0; t < m; ++t) {
-        B.ent_col[t] = rowid(D.res_v[t]);
-        put_val(B.ent_val, (int64_t)t, pdt, D.res_a[t]);
+        B.keys.push_back(rowid(D.res_v[t]));
+        B.vals.resize(B.keys.size() * es);
+        put_val(B.vals, (int64_t)B.keys.size() - 1, pdt, D.res_a[t]);
         if (t + 1 == m || D.res_u[t + 1] != D.res_u[t]) {
-            B.seg_out.push_back(rowid(D.res_u[t]));
-            B.seg_end.push_back((uint32_t)(t + 1));
+            B.keys.push_back(kPseudoRec | rowid(D.res_u[t]));
+            B.vals.resize(B.keys.size() * es, 0);
+            ++B.nseg;
         }
     }
-    B.rows = (int64_t)B.seg_out.size();
-    B.n_i = B.rows;
+    B.rows = B.nseg;
+    B.n_i = B.nseg;
+    cut_batches(B, batch_records);
 }
 
 arrow_status validate_args(const arrow_csr *A, int64_t b, int32_t levels) {
@@ -350,8 +364,10 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         return fail(ARROW_E_INVALID_ARG, "negative window/chunk/batch");
     const int64_t window_rows = opt.window_rows > 0 ? opt.window_rows : kDefaultWindowRows;
     const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : kDefaultHeadChunk;
+    const int32_t batch_records = opt.batch_segments > 0 ? opt.batch_segments : kDefaultBatchRecords;
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
     const int64_t n = D.n, b = D.b;
+    if (n >= kMaxRows) return fail(ARROW_E_UNSUPPORTED, "n must be < 2^30 (30-bit row keys)");
 
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
@@ -363,7 +379,6 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, dev));
         P->dtype = pdt;
         P->order = order;
-        P->batch_segments = opt.batch_segments;
         P->n = n;
         P->b = b;
         P->isolated = D.isolated;
@@ -378,8 +393,8 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         }
         built.resize(D.levels.size() + (D.res_u.empty() ? 0 : 1));
         for (size_t i = 0; i < D.levels.size(); ++i)
-            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, pos0p, pdt, comm ? 1 : 0, built[i]);
-        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, built.back());
+            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, batch_records, pos0p, pdt, comm ? 1 : 0, built[i]);
+        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, batch_records, built.back());
         P->residual_nnz = (int64_t)D.res_u.size();
         P->arrow_levels = (int32_t)D.levels.size();
         P->host_levels.resize(D.levels.size());
@@ -415,15 +430,14 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         const size_t es = P->esize();
         int64_t total = 0;
         auto reserve = [&](int64_t bytes) { int64_t at = total; total += align_up(std::max<int64_t>(bytes, 1), 256); return at; };
-        std::vector<std::array<int64_t, 6>> offs(built.size());
+        std::vector<std::array<int64_t, 5>> offs(built.size());
         for (size_t i = 0; i < built.size(); ++i) {
             const BuiltLevel &B = built[i];
-            offs[i][0] = reserve((int64_t)B.seg_out.size() * 4);
-            offs[i][1] = reserve((int64_t)B.seg_end.size() * 4);
-            offs[i][2] = reserve((int64_t)B.ent_col.size() * 4);
-            offs[i][3] = reserve((int64_t)B.ent_col.size() * (int64_t)es);
-            offs[i][4] = reserve((int64_t)B.head_rows.size() * 4);
-            offs[i][5] = reserve((int64_t)B.zero_rows.size() * 4);
+            offs[i][0] = reserve((int64_t)B.keys.size() * 4);
+            offs[i][1] = reserve((int64_t)B.vals.size());
+            offs[i][2] = reserve((int64_t)B.bstart.size() * 4);
+            offs[i][3] = reserve((int64_t)B.head_rows.size() * 4);
+            offs[i][4] = reserve((int64_t)B.zero_rows.size() * 4);
         }
         const int64_t off_counters = reserve((int64_t)(built.size() + 1) * 4);
         if (total > 0) {
@@ -436,20 +450,20 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
             const BuiltLevel &B = built[i];
             DeviceLevel L;
             L.rows = B.rows; L.n_i = B.n_i; L.head = B.head; L.nnz = B.nnz; L.head_nnz = B.head_nnz;
-            L.tiles = B.tiles; L.nseg = (int64_t)B.seg_out.size(); L.mode = B.mode;
+            L.tiles = B.tiles; L.nseg = B.nseg; L.mode = B.mode;
+            L.nrec = (int64_t)B.keys.size();
+            L.nbatch = (int64_t)B.bstart.size() - 1;
             L.nzero = (int64_t)B.zero_rows.size();
-            L.seg_out = reinterpret_cast<int32_t *>(base + offs[i][0]);
-            L.seg_end = reinterpret_cast<uint32_t *>(base + offs[i][1]);
-            L.ent_col = reinterpret_cast<int32_t *>(base + offs[i][2]);
-            L.ent_val = base + offs[i][3];
-            L.head_rows = reinterpret_cast<int32_t *>(base + offs[i][4]);
-            L.zero_rows = reinterpret_cast<int32_t *>(base + offs[i][5]);
-            CUDA_TRY(cudaMemcpy(L.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.seg_out, B.seg_out.data(), B.seg_out.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.seg_end, B.seg_end.data(), B.seg_end.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.ent_col, B.ent_col.data(), B.ent_col.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.ent_val, B.ent_val.data(), B.ent_val.size(), cudaMemcpyHostToDevice));
+            L.keys = reinterpret_cast<uint32_t *>(base + offs[i][0]);
+            L.vals = base + offs[i][1];
+            L.bstart = reinterpret_cast<uint32_t *>(base + offs[i][2]);
+            L.head_rows = reinterpret_cast<int32_t *>(base + offs[i][3]);
+            L.zero_rows = reinterpret_cast<int32_t *>(base + offs[i][4]);
+            CUDA_TRY(cudaMemcpy(L.keys, B.keys.data(), B.keys.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.vals, B.vals.data(), B.vals.size(), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.bstart, B.bstart.data(), B.bstart.size() * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(L.head_rows, B.head_rows.data(), B.head_rows.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(L.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
             P->levels.push_back(L);
         }
         P->counters = reinterpret_cast<unsigned *>(base + off_counters);
@@ -714,6 +728,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     int cur = 0;
     CUDA_TRY(cudaGetDevice(&cur));
     if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
+    if (k * (int64_t)P->esize() >= ((int64_t)1 << 32)) return fail(ARROW_E_UNSUPPORTED, "row of X exceeds 4 GiB");
     const int64_t rows = P->local_end - P->local_begin;
     const int64_t bytes = rows * k * (int64_t)P->esize();
     const char *xa = (const char *)X, *ya = (const char *)Y;
@@ -743,7 +758,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
-        e = launch_segments(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->batch_segments, st);
+        e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
     }
@@ -812,6 +827,8 @@ arrow_status arrow_plan_level_info(arrow_plan P, int32_t level, arrow_level_info
     info->head_nnz = L.head_nnz;
     info->tiles = L.tiles;
     info->segments = L.nseg;
+    info->reserved[0] = L.nrec;
+    info->reserved[1] = L.nbatch;
     return ARROW_OK;
 }
 

@@ -1,5 +1,7 @@
 // arrow_internal.h -- internal types shared by the host decomposer, plan builder and kernels.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -35,36 +37,53 @@ int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *
 int check_symmetric(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &err);
 
 // ------------------------------------------------------------------ device layout of one level
-// Work is a stream of non-empty "segments": a segment is a list of (column, value) entries whose
-// sum  sum_e val_e * src_row(col_e)  goes to one output row.
-//   out >= 0 : Y row `out` (body row p >= h_i of B_i; folded: out = perm_i[p] or its pi_0 position)
-//   out <  0 : head-row partial restricted to one tile window (Alg. 1 line 2, C^(0) = sum_t B^(0,t) D^(t),
-//              P:464), added atomically: single GPU -> Y row (out & 0x7fffffff) = perm_i[j];
-//              distributed -> C0 row j (reduced over ranks, then written by the head epilogue)
-//   col >= 0 : X row col (folded permutation: P_pi^T X is never materialised, S4)
-//   col <  0 : (distributed only) head block row (col & 0x7fffffff) of D0 = X[head_i]
-// Segments are ordered by tile window so that concurrently running warps touch the same X rows
-// (L2 reuse, the IO lemma's "tiles stay resident").
-constexpr uint32_t kFlag = 0x80000000u;
+// A level is a stream of records (key, val) in tile-window order (see stream_kernel.cuh):
+//   plain record  : key = X row (the folded permutation: P_pi^T X is never materialised, S4);
+//                   kAux set (distributed only) = row of the staged head block D0 = X[head_i]
+//   pseudo record : kPseudo | out row -- closes the current segment.  kAux set = head-row partial of
+//                   one tile window (Alg. 1 line 2, C^(0) = sum_t B^(0,t) D^(t)) added
+//                   atomically (single GPU: into Y[perm_i[j]]; distributed: into C0[j]); otherwise
+//                   body row p >= h_i stored (level 0) or read-modify-written (levels >= 1, S5).
+// Batches (bstart) are record ranges cut at pseudo records.
+constexpr uint32_t kPseudoRec = 0x80000000u;
+constexpr uint32_t kAuxRec = 0x40000000u;
+constexpr int64_t kMaxRows = (int64_t)1 << 30;
 
 struct DeviceLevel {
     int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
-    int64_t nseg = 0, nzero = 0;
-    int mode = 0;                 // 0: level 0 stores Y rows; 1: levels >= 1 read-modify-write (S5)
-    // device pointers (into the plan arena)
-    int32_t *seg_out = nullptr;   // [nseg]
-    uint32_t *seg_end = nullptr;  // [nseg]  end offset of each segment (begin = previous end)
-    int32_t *ent_col = nullptr;   // [nnz]
-    void *ent_val = nullptr;      // [nnz] of dtype
-    int32_t *head_rows = nullptr; // [head] X/Y row of head vertex j
-    int32_t *zero_rows = nullptr; // [nzero] level 0: Y rows written as 0 before the level runs
+    int64_t nseg = 0, nrec = 0, nbatch = 0, nzero = 0;
+    int mode = 0;                  // 0: level 0 stores Y rows; 1: levels >= 1 read-modify-write (S5)
+    uint32_t *keys = nullptr;      // [nrec]
+    void *vals = nullptr;          // [nrec] of dtype
+    uint32_t *bstart = nullptr;    // [nbatch + 1]
+    int32_t *head_rows = nullptr;  // [head] X/Y row of head vertex j
+    int32_t *zero_rows = nullptr;  // [nzero] level 0: Y rows written as 0 before the level runs
 };
 
+struct StreamArgs {
+    const uint32_t *keys;
+    const void *vals;
+    const uint32_t *bstart;
+    int64_t nbatch;
+    const void *X, *D0;
+    void *Y, *C0;
+    int64_t k;
+    unsigned *counter;
+    int num_sms, mode, dist;
+};
+struct StreamCfg {
+    int vb, lpe, nv, d;
+};
+
+StreamCfg pick_stream_cfg(int dtype, int64_t k, const void *X, const void *Y, const void *D0, const void *C0);
+int launch_stream_f32(const StreamArgs &a, const StreamCfg &c, cudaStream_t st);
+int launch_stream_f64(const StreamArgs &a, const StreamCfg &c, cudaStream_t st);
+
 // kernels.cu launchers (all on `stream`; return cudaError_t as int)
+int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
+                  int64_t k, int num_sms, unsigned *counter, void *stream);
 int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k,
                       void *D0, void *C0, void *stream);
-int launch_segments(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                    int64_t k, int num_sms, unsigned *counter, int bseg, void *stream);
 int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k,
                          int add, void *Y, void *stream);
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream);

@@ -1,0 +1,23 @@
+// kernels_f64.cu -- fp64 instantiations of the record-stream kernel (see stream_kernel.cuh).
+#include "stream_dispatch.cuh"
+
+namespace arrow {
+
+int launch_stream_f64(const StreamArgs &a, const StreamCfg &c, cudaStream_t st) {
+    using namespace ks;
+#define ARROW_CFG(L, N, B, DD) \
+    if (c.lpe == L && c.nv == N && c.vb == B && c.d == DD) return run_cfg<double, L, N, B, DD>(a, st);
+    ARROW_CFG(8, 4, 16, 4)
+    ARROW_CFG(4, 4, 16, 4)
+    ARROW_CFG(2, 4, 16, 4)
+    ARROW_CFG(1, 4, 16, 4)
+    ARROW_CFG(8, 1, 16, 8)
+    ARROW_CFG(1, 1, 16, 8)
+    ARROW_CFG(32, 1, 8, 8)
+    ARROW_CFG(8, 1, 8, 8)
+    ARROW_CFG(1, 1, 8, 8)
+#undef ARROW_CFG
+    return (int)cudaErrorInvalidConfiguration;
+}
+
+}  // namespace arrow
