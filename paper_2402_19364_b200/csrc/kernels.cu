@@ -201,8 +201,16 @@ int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, cons
                   int64_t k, int num_sms, unsigned *counter, void *stream) {
     if (L.nbatch == 0 || k == 0) return 0;
     StreamArgs a{L.keys, L.vals, L.bstart, L.nbatch, X, D0, Y, C0, k, counter, num_sms, L.mode, dist};
-    const StreamCfg c = pick_stream_cfg(dtype, k, X, Y, dist ? D0 : nullptr, dist ? C0 : nullptr);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // TMA bulk-gather kernel when rows are 16-byte multiples of at most 1 KiB on 16-byte aligned
+    // buffers; otherwise the register-pipelined record-stream kernel.
+    const int es = dtype == 1 ? 8 : 4;
+    const int64_t rb = k * es;
+    bool tma = rb % 16 == 0 && rb <= 1024;
+    for (const void *p : {X, (const void *)Y, D0, (const void *)C0})
+        if (p && (reinterpret_cast<uintptr_t>(p) % 16) != 0) tma = false;
+    if (const char *e = std::getenv("ARROW_KA_STREAM")) tma = tma && std::atoi(e) == 0;
+    StreamCfg c = tma ? StreamCfg{16, 0, 0, 0} : pick_stream_cfg(dtype, k, X, Y, dist ? D0 : nullptr, dist ? C0 : nullptr);
     return dtype == 1 ? launch_stream_f64(a, c, st) : launch_stream_f32(a, c, st);
 }
 

@@ -5,6 +5,11 @@ namespace arrow {
 
 int launch_stream_f32(const StreamArgs &a, const StreamCfg &c, cudaStream_t st) {
     using namespace ks;
+    if (c.lpe == 0) {
+        const int r = kt::run_tma<float>(a, st);
+        if (r >= 0) return r;
+        return (int)cudaErrorInvalidConfiguration;
+    }
 #define ARROW_CFG(L, N, B, DD) \
     if (c.lpe == L && c.nv == N && c.vb == B && c.d == DD) return run_cfg<float, L, N, B, DD>(a, st);
     ARROW_CFG(8, 4, 16, 4)
@@ -14,6 +19,9 @@ int launch_stream_f32(const StreamArgs &a, const StreamCfg &c, cudaStream_t st) 
     ARROW_CFG(2, 4, 16, 4)
     ARROW_CFG(1, 4, 16, 4)
     ARROW_CFG(8, 1, 16, 8)
+    ARROW_CFG(32, 1, 16, 8)
+    ARROW_CFG(32, 1, 16, 16)
+    ARROW_CFG(16, 2, 16, 8)
     ARROW_CFG(1, 1, 16, 8)
     ARROW_CFG(32, 1, 8, 8)
     ARROW_CFG(8, 1, 8, 8)

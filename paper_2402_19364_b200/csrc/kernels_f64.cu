@@ -5,6 +5,11 @@ namespace arrow {
 
 int launch_stream_f64(const StreamArgs &a, const StreamCfg &c, cudaStream_t st) {
     using namespace ks;
+    if (c.lpe == 0) {
+        const int r = kt::run_tma<double>(a, st);
+        if (r >= 0) return r;
+        return (int)cudaErrorInvalidConfiguration;
+    }
 #define ARROW_CFG(L, N, B, DD) \
     if (c.lpe == L && c.nv == N && c.vb == B && c.d == DD) return run_cfg<double, L, N, B, DD>(a, st);
     ARROW_CFG(8, 4, 16, 4)

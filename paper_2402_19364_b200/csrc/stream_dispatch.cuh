@@ -5,6 +5,8 @@
 
 #include "arrow_internal.h"
 #include "stream_kernel.cuh"
+#include "tma_kernel.cuh"
+#include <cstdlib>
 
 namespace arrow {
 namespace ks {
@@ -33,4 +35,64 @@ int run_cfg(const StreamArgs &a, cudaStream_t st) {
 }
 
 }  // namespace ks
+
+namespace kt {
+
+inline int env_int(const char *name, int dflt) {
+    const char *e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+template <typename T, int NV, int NCH, int MODE, int DIST>
+int run_tma_one(const StreamArgs &a, int warps, cudaStream_t st) {
+    auto kern = k_tma<T, NV, NCH, MODE, DIST>;
+    const uint32_t RB = (uint32_t)(a.k * (int64_t)sizeof(T));
+    const size_t warp_bytes = ((size_t)NCH * 32 * RB + NCH * 8 + 127) / 128 * 128;
+    const size_t smem = warp_bytes * (size_t)warps;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        configured = smem;
+    }
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, warps * 32, smem);
+    if (bps <= 0) bps = 1;
+    int64_t blocks = std::min<int64_t>((int64_t)a.num_sms * bps, (a.nbatch + warps - 1) / warps);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, warps * 32, smem, st>>>(a.keys, reinterpret_cast<const T *>(a.vals), a.bstart, a.nbatch,
+                                                      reinterpret_cast<const T *>(a.X),
+                                                      reinterpret_cast<const T *>(a.D0), reinterpret_cast<T *>(a.Y),
+                                                      reinterpret_cast<T *>(a.C0), a.k, a.counter);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int NV, int NCH>
+int run_tma_cfg(const StreamArgs &a, int warps, cudaStream_t st) {
+    if (a.dist) return a.mode == 0 ? run_tma_one<T, NV, NCH, 0, 1>(a, warps, st) : run_tma_one<T, NV, NCH, 1, 1>(a, warps, st);
+    return a.mode == 0 ? run_tma_one<T, NV, NCH, 0, 0>(a, warps, st) : run_tma_one<T, NV, NCH, 1, 0>(a, warps, st);
+}
+
+// TMA path for rows of 16..1024 bytes (multiple of 16).  Returns -1 if not applicable.
+template <typename T>
+int run_tma(const StreamArgs &a, cudaStream_t st) {
+    const int64_t RB = a.k * (int64_t)sizeof(T);
+    if (RB % 16 != 0 || RB > 1024 || env_int("ARROW_KA_STREAM", 0)) return -1;
+    const int nv = RB <= 512 ? 1 : 2;
+    int nch = env_int("ARROW_TMA_NCH", RB <= 512 ? 3 : 2);
+    if (nch < 2) nch = 2;
+    if (nch > 4) nch = 4;
+    const size_t warp_bytes = ((size_t)nch * 32 * RB + nch * 8 + 127) / 128 * 128;
+    int warps = env_int("ARROW_TMA_WARPS", (int)std::min<size_t>(8, (200 * 1024) / warp_bytes));
+    if (warps < 1) warps = 1;
+    if (warps > 8) warps = 8;
+    if (nv == 1) {
+        if (nch == 2) return run_tma_cfg<T, 1, 2>(a, warps, st);
+        if (nch == 3) return run_tma_cfg<T, 1, 3>(a, warps, st);
+        return run_tma_cfg<T, 1, 4>(a, warps, st);
+    }
+    return run_tma_cfg<T, 2, 2>(a, warps, st);
+}
+
+}  // namespace kt
 }  // namespace arrow

@@ -50,6 +50,32 @@ __device__ __forceinline__ Vec<T, VB> ldg_vec(const char *p) {
     return out;
 }
 
+// Predicated read-only load into `dst` (unchanged when !pred).  Written as one PTX instruction
+// with read-write operands so that every pipeline slot keeps its own registers: a C++
+// "if (pred) dst = load" makes the compiler merge through a temporary and wait on the load.
+template <typename T, int VB>
+__device__ __forceinline__ void ldg_vec_pred(bool pred, const char *p, Vec<T, VB> &dst) {
+    if constexpr (VB == 16) {
+        uint32_t *r = reinterpret_cast<uint32_t *>(&dst);
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                     "@q ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+                     : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])
+                     : "l"(p), "r"((int)pred));
+    } else if constexpr (VB == 8) {
+        uint32_t *r = reinterpret_cast<uint32_t *>(&dst);
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+                     "@q ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];\n\t}"
+                     : "+r"(r[0]), "+r"(r[1])
+                     : "l"(p), "r"((int)pred));
+    } else {
+        uint32_t *r = reinterpret_cast<uint32_t *>(&dst);
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                     "@q ld.global.nc.L1::no_allocate.u32 %0, [%1];\n\t}"
+                     : "+r"(r[0])
+                     : "l"(p), "r"((int)pred));
+    }
+}
+
 template <typename T, int VB>
 __device__ __forceinline__ Vec<T, VB> ld_vec(const char *p) {
     using R = typename Raw<VB>::type;
@@ -81,11 +107,14 @@ __device__ __forceinline__ void zero(Vec<T, VB> &a) {
     for (int i = 0; i < Vec<T, VB>::N; ++i) a.v[i] = T(0);
 }
 
-// acc += a * x
+// acc += a * x.  The packed FFMA2 (fma.rn.f32x2) halves the FMA instructions but makes ptxas
+// allocate the row registers as 64-bit pairs, which breaks the aligned quads LDG.128 writes and
+// serialises the load pipeline; plain FFMA keeps the loads landing in their slots.
+constexpr bool kUseFfma2 = false;
 template <typename T, int VB>
 __device__ __forceinline__ void fma_vec(Vec<T, VB> &acc, T a, const Vec<T, VB> &x) {
     constexpr int N = Vec<T, VB>::N;
-    if constexpr (sizeof(T) == 4 && (N % 2) == 0) {
+    if constexpr (kUseFfma2 && sizeof(T) == 4 && (N % 2) == 0) {
 #pragma unroll
         for (int i = 0; i < N; i += 2) {
             uint64_t c, xb;
@@ -136,10 +165,14 @@ k_stream(const uint32_t *__restrict__ keys, const T *__restrict__ vals, const ui
         if (lane == 0) wb = atomicAdd(counter, 1u);
         wb = __shfl_sync(0xffffffffu, wb, 0);
         if ((int64_t)wb * SUBS >= nbatch) break;            // warp-uniform exit
+        // The SUBS sub-warps of a warp run their streams in lockstep: the same relative record
+        // index every step, so chunk refills and shuffles are warp-uniform and per-stream
+        // differences are lane predicates, not divergent branches.
         const int64_t bt = (int64_t)wb * SUBS + sub;
-        if (bt >= nbatch) continue;                         // this sub-warp idles for one grab
-        const uint32_t r0 = __ldg(bstart + bt), r1 = __ldg(bstart + bt + 1);
+        uint32_t r0 = 0, r1 = 0;
+        if (bt < nbatch) { r0 = __ldg(bstart + bt); r1 = __ldg(bstart + bt + 1); }
         const int len = (int)(r1 - r0);
+        const int maxlen = (SUBS == 1) ? len : (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
 
         for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
             bool act[NV];
@@ -152,7 +185,7 @@ k_stream(const uint32_t *__restrict__ keys, const T *__restrict__ vals, const ui
 #pragma unroll
             for (int v = 0; v < NV; ++v) zero<T, VB>(acc[v]);
 
-            // record chunks: lane sl holds record cb + sl (cur) and cb + LPE + sl (nxt)
+            // record chunks: lane sl holds record cb + sl (cur) and cb + LPE + sl (nxt) of its stream
             int cb = 0;
             uint32_t ckey = kPseudo, nkey = kPseudo;
             T cval = T(0), nval = T(0);
@@ -162,15 +195,28 @@ k_stream(const uint32_t *__restrict__ keys, const T *__restrict__ vals, const ui
             uint32_t skey[D];
             T sval[D];
             V xs[D][NV];
-
-            for (int base = 0; base < len + D; base += D) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) {
-                    const int r = base + d;
-                    // ---- consume record r - D from slot d
-                    if (r >= D && r - D < len) {
+            for (int d = 0; d < D; ++d) skey[d] = 0;
+
+            // Two ping-pong groups of G = D/2 slots: consume a whole group (its loads were issued
+            // together, so one scoreboard wait covers them), then refill it D records ahead while
+            // the other group's loads stay in flight.
+            constexpr int G = D / 2;
+            for (int base = 0; base < maxlen + D; base += D) {
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                    for (int t = 0; t < G; ++t) {
+                        const int d = half * G + t;
+                        const int r = base + d;
+                        // ---- consume record r - D of this stream from slot d
+                        const bool live = (r >= D) && (r - D < len);
                         const uint32_t key = skey[d];
-                        if (key & kPseudo) {
+                        if (live && !(key & kPseudo)) {
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) fma_vec<T, VB>(acc[v], sval[d], xs[d][v]);
+                        }
+                        if (live && (key & kPseudo)) {
                             const uint32_t row = key & kRowMask;
                             if (key & kAux) {
                                 char *dst = reinterpret_cast<char *>(DIST ? C0 : Y) + (uint64_t)row * rowbytes + lane_off;
@@ -194,34 +240,33 @@ k_stream(const uint32_t *__restrict__ keys, const T *__restrict__ vals, const ui
                             }
 #pragma unroll
                             for (int v = 0; v < NV; ++v) zero<T, VB>(acc[v]);
-                        } else {
-#pragma unroll
-                            for (int v = 0; v < NV; ++v) fma_vec<T, VB>(acc[v], sval[d], xs[d][v]);
                         }
                     }
-                    // ---- issue record r into slot d
-                    if (r < len) {
-                        if (r - cb == LPE) {                  // advance the record chunk (sub-warp uniform)
-                            cb += LPE;
-                            ckey = nkey;
-                            cval = nval;
-                            nkey = kPseudo;
-                            nval = T(0);
-                            if (cb + LPE + sl < len) {
-                                nkey = __ldcs(keys + r0 + cb + LPE + sl);
-                                nval = __ldcs(vals + r0 + cb + LPE + sl);
-                            }
-                        }
-                        const uint32_t key = __shfl_sync(mask, ckey, r - cb, LPE);
-                        skey[d] = key;
-                        sval[d] = __shfl_sync(mask, cval, r - cb, LPE);
-                        if (!(key & kPseudo)) {
-                            const char *p = ((DIST && (key & kAux)) ? dl : xl) + (uint64_t)(key & kRowMask) * (uint64_t)rowbytes;
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) {
-                                if (act[v]) xs[d][v] = ldg_vec<T, VB>(p + v * LPE * VB);
-                                else zero<T, VB>(xs[d][v]);
+                    for (int t = 0; t < G; ++t) {
+                        const int d = half * G + t;
+                        const int r = base + d;
+                        // ---- issue record r into slot d
+                        if (r < maxlen) {                          // warp-uniform
+                            if (r - cb == LPE) {                   // advance the record chunk (warp-uniform)
+                                cb += LPE;
+                                ckey = nkey;
+                                cval = nval;
+                                nkey = kPseudo;
+                                nval = T(0);
+                                if (cb + LPE + sl < len) {
+                                    nkey = __ldcs(keys + r0 + cb + LPE + sl);
+                                    nval = __ldcs(vals + r0 + cb + LPE + sl);
+                                }
                             }
+                            const uint32_t kk = __shfl_sync(0xffffffffu, ckey, r - cb, LPE);
+                            const T vv = __shfl_sync(0xffffffffu, cval, r - cb, LPE);
+                            skey[d] = kk;
+                            sval[d] = vv;
+                            const bool ld = r < len && !(kk & kPseudo);
+                            const char *p = ((DIST && (kk & kAux)) ? dl : xl) + (uint64_t)(kk & kRowMask) * (uint64_t)rowbytes;
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) ldg_vec_pred<T, VB>(ld && act[v], p + v * LPE * VB, xs[d][v]);
                         }
                     }
                 }
