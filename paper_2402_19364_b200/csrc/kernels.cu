@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "arrow_internal.h"
 
@@ -209,8 +210,12 @@ int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, cons
     bool tma = rb % 16 == 0 && rb <= 1024;
     for (const void *p : {X, (const void *)Y, D0, (const void *)C0})
         if (p && (reinterpret_cast<uintptr_t>(p) % 16) != 0) tma = false;
-    if (const char *e = std::getenv("ARROW_KA_STREAM")) tma = tma && std::atoi(e) == 0;
-    StreamCfg c = tma ? StreamCfg{16, 0, 0, 0} : pick_stream_cfg(dtype, k, X, Y, dist ? D0 : nullptr, dist ? C0 : nullptr);
+    // kernel choice: ARROW_KA=rec (default for 16-byte rows <= 1 KiB), tma, stream
+    const char *ka = std::getenv("ARROW_KA");
+    const std::string kas = ka ? ka : "rec";
+    StreamCfg c = pick_stream_cfg(dtype, k, X, Y, dist ? D0 : nullptr, dist ? C0 : nullptr);
+    if (tma && kas == "rec") c = StreamCfg{16, -1, 0, 0};
+    else if (tma && kas == "tma") c = StreamCfg{16, 0, 0, 0};
     return dtype == 1 ? launch_stream_f64(a, c, st) : launch_stream_f32(a, c, st);
 }
 

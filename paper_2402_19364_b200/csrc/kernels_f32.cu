@@ -5,6 +5,11 @@ namespace arrow {
 
 int launch_stream_f32(const StreamArgs &a, const StreamCfg &c, cudaStream_t st) {
     using namespace ks;
+    if (c.lpe == -1) {
+        const int r = kr::run_rec<float>(a, st);
+        if (r >= 0) return r;
+        return (int)cudaErrorInvalidConfiguration;
+    }
     if (c.lpe == 0) {
         const int r = kt::run_tma<float>(a, st);
         if (r >= 0) return r;

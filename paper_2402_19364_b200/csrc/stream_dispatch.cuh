@@ -6,6 +6,7 @@
 #include "arrow_internal.h"
 #include "stream_kernel.cuh"
 #include "tma_kernel.cuh"
+#include "rec_kernel.cuh"
 #include <cstdlib>
 
 namespace arrow {
@@ -95,4 +96,38 @@ int run_tma(const StreamArgs &a, cudaStream_t st) {
 }
 
 }  // namespace kt
+
+namespace kr {
+
+template <typename T, int NV, int MODE, int DIST>
+int run_rec_one(const StreamArgs &a, cudaStream_t st) {
+    auto kern = k_rec<T, NV, MODE, DIST>;
+    static int bps = 0;
+    if (bps == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+        if (bps <= 0) bps = 1;
+    }
+    int64_t blocks = std::min<int64_t>((int64_t)a.num_sms * bps, (a.nbatch + 7) / 8);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(a.keys, reinterpret_cast<const T *>(a.vals), a.bstart, a.nbatch,
+                                            reinterpret_cast<const T *>(a.X), reinterpret_cast<const T *>(a.D0),
+                                            reinterpret_cast<T *>(a.Y), reinterpret_cast<T *>(a.C0), a.k, a.counter);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int NV>
+int run_rec_cfg(const StreamArgs &a, cudaStream_t st) {
+    if (a.dist) return a.mode == 0 ? run_rec_one<T, NV, 0, 1>(a, st) : run_rec_one<T, NV, 1, 1>(a, st);
+    return a.mode == 0 ? run_rec_one<T, NV, 0, 0>(a, st) : run_rec_one<T, NV, 1, 0>(a, st);
+}
+
+// Whole-warp record kernel for rows of 16-byte multiples up to 1 KiB.  Returns -1 otherwise.
+template <typename T>
+int run_rec(const StreamArgs &a, cudaStream_t st) {
+    const int64_t RB = a.k * (int64_t)sizeof(T);
+    if (RB % 16 != 0 || RB > 1024) return -1;
+    return RB <= 512 ? run_rec_cfg<T, 1>(a, st) : run_rec_cfg<T, 2>(a, st);
+}
+
+}  // namespace kr
 }  // namespace arrow

@@ -85,6 +85,16 @@ __device__ __forceinline__ Vec<T, VB> ld_vec(const char *p) {
     return out;
 }
 
+// streaming (evict-first) load of a Y row that is read once and rewritten (levels >= 1)
+template <typename T, int VB>
+__device__ __forceinline__ Vec<T, VB> ld_vec_stream(const char *p) {
+    using R = typename Raw<VB>::type;
+    R r = __ldcs(reinterpret_cast<const R *>(p));
+    Vec<T, VB> out;
+    memcpy(&out, &r, VB);
+    return out;
+}
+
 template <typename T, int VB>
 __device__ __forceinline__ void st_vec(char *p, const Vec<T, VB> &v) {
     using R = typename Raw<VB>::type;
