@@ -6,6 +6,7 @@
 #include <array>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -57,7 +58,8 @@ struct arrow_plan_s {
     int64_t residual_nnz = 0;
     int64_t max_head = 0;
     double create_seconds = 0;
-    std::vector<DeviceLevel> levels;  // arrow levels, then (optionally) the residual level
+    std::vector<DeviceLevel> levels;  // device launch list: level 0, then levels >= 1 (+ residual), possibly merged
+    std::vector<DeviceLevel> meta;    // per arrow level (+ residual) metadata for introspection
     int32_t arrow_levels = 0;
     // host copy of the canonical levels for export
     std::vector<HostLevel> host_levels;
@@ -143,7 +145,8 @@ void cut_batches(BuiltLevel &B, int32_t target) {
 //             level 0 zeroes head rows and entry-less rows first (zero_rows).
 //   dist = 1: head columns read the staged head block D0, head partials add into C0[j].
 void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_rows, int32_t head_chunk,
-                 int32_t batch_records, const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, BuiltLevel &B) {
+                 int32_t batch_records, const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, bool tail_atomic,
+                 BuiltLevel &B) {
     const int64_t n_i = L.n_i, h = L.head, rows = L.rows;
     B.rows = rows;
     B.n_i = n_i;
@@ -207,7 +210,9 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
         for (int64_t p = std::max(h, lo); p < hi; ++p) {
             if (L.row_ptr[p + 1] == L.row_ptr[p]) continue;
             for (int64_t x = L.row_ptr[p]; x < L.row_ptr[p + 1]; ++x) entry(x);
-            B.keys[r++] = kPseudoRec | rowid(L.perm[p]);
+            // levels >= 1 add into Y rows written by earlier levels: a fire-and-forget L2 reduction
+            // (tail_atomic) or a read-modify-write
+            B.keys[r++] = kPseudoRec | ((tail_atomic && level_idx > 0) ? kAuxRec : 0u) | rowid(L.perm[p]);
         }
         for (int64_t j = 0; j < h; ++j) {
             const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
@@ -226,7 +231,7 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
 
 // Residual CSR level (ARROW_RESIDUAL_CSR): every row with leftover entries is one RMW segment.
 void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *pos0, arrow_dtype pdt,
-                    int32_t batch_records, BuiltLevel &B) {
+                    int32_t batch_records, bool tail_atomic, BuiltLevel &B) {
     auto rowid = [&](int32_t v) -> uint32_t { return (uint32_t)(pos0 ? (*pos0)[v] : v); };
     const size_t m = D.res_u.size();
     B.mode = 1;
@@ -238,7 +243,7 @@ void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *
         B.vals.resize(B.keys.size() * es);
         put_val(B.vals, (int64_t)B.keys.size() - 1, pdt, D.res_a[t]);
         if (t + 1 == m || D.res_u[t + 1] != D.res_u[t]) {
-            B.keys.push_back(kPseudoRec | rowid(D.res_u[t]));
+            B.keys.push_back(kPseudoRec | (tail_atomic ? kAuxRec : 0u) | rowid(D.res_u[t]));
             B.vals.resize(B.keys.size() * es, 0);
             ++B.nseg;
         }
@@ -246,6 +251,28 @@ void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *
     B.rows = B.nseg;
     B.n_i = B.nseg;
     cut_batches(B, batch_records);
+}
+
+// Concatenate the record streams of levels 1.. (all flushes are L2 reductions, so their order does
+// not matter) into one launch; batch boundaries are rebased.
+BuiltLevel merge_tail(std::vector<BuiltLevel> &built) {
+    BuiltLevel M;
+    M.mode = 1;
+    M.bstart.push_back(0);
+    for (size_t i = 1; i < built.size(); ++i) {
+        BuiltLevel &B = built[i];
+        const uint32_t base = (uint32_t)M.keys.size();
+        M.keys.insert(M.keys.end(), B.keys.begin(), B.keys.end());
+        M.vals.insert(M.vals.end(), B.vals.begin(), B.vals.end());
+        for (size_t j = 1; j < B.bstart.size(); ++j) M.bstart.push_back(base + B.bstart[j]);
+        M.nseg += B.nseg;
+        M.nnz += B.nnz;
+        M.rows += B.rows;
+        M.n_i += B.n_i;
+        std::vector<uint32_t>().swap(B.keys);
+        std::vector<uint8_t>().swap(B.vals);
+    }
+    return M;
 }
 
 arrow_status validate_args(const arrow_csr *A, int64_t b, int32_t levels) {
@@ -367,6 +394,9 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     const int32_t batch_records = opt.batch_segments > 0 ? opt.batch_segments : kDefaultBatchRecords;
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
     const int64_t n = D.n, b = D.b;
+    // levels >= 1: L2 reductions instead of read-modify-write, all of them in one launch
+    bool tail_atomic = !comm;
+    if (const char *e = std::getenv("ARROW_TAIL_ATOMIC")) tail_atomic = tail_atomic && std::atoi(e) != 0;
     if (n >= kMaxRows) return fail(ARROW_E_UNSUPPORTED, "n must be < 2^30 (30-bit row keys)");
 
     int dev = 0;
@@ -393,8 +423,9 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         }
         built.resize(D.levels.size() + (D.res_u.empty() ? 0 : 1));
         for (size_t i = 0; i < D.levels.size(); ++i)
-            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, batch_records, pos0p, pdt, comm ? 1 : 0, built[i]);
-        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, batch_records, built.back());
+            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, batch_records, pos0p, pdt, comm ? 1 : 0, tail_atomic,
+                        built[i]);
+        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, batch_records, tail_atomic, built.back());
         P->residual_nnz = (int64_t)D.res_u.size();
         P->arrow_levels = (int32_t)D.levels.size();
         P->host_levels.resize(D.levels.size());
@@ -425,7 +456,23 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         P->bytes_alg_rows += n;  // level-0 store of every Y row
     }
 
-    // upload: one arena for all levels
+    // per-level metadata for introspection; device launch list (levels >= 1 merged when atomic)
+    for (const BuiltLevel &B : built) {
+        DeviceLevel L;
+        L.rows = B.rows; L.n_i = B.n_i; L.head = B.head; L.nnz = B.nnz; L.head_nnz = B.head_nnz;
+        L.tiles = B.tiles; L.nseg = B.nseg; L.mode = B.mode;
+        L.nrec = (int64_t)B.keys.size();
+        L.nbatch = (int64_t)B.bstart.size() - 1;
+        L.nzero = (int64_t)B.zero_rows.size();
+        P->meta.push_back(L);
+    }
+    if (tail_atomic && built.size() > 2) {
+        BuiltLevel M = merge_tail(built);
+        built.resize(1);
+        built.push_back(std::move(M));
+    }
+
+    // upload: one arena for all launch levels
     {
         const size_t es = P->esize();
         int64_t total = 0;
@@ -817,9 +864,9 @@ arrow_status arrow_plan_info(arrow_plan P, arrow_plan_info_t *info) {
 
 arrow_status arrow_plan_level_info(arrow_plan P, int32_t level, arrow_level_info_t *info) {
     if (!P || !info) return fail(ARROW_E_INVALID_ARG, "NULL argument");
-    if (level < 0 || level >= (int32_t)P->levels.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
+    if (level < 0 || level >= (int32_t)P->meta.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
     std::memset(info, 0, sizeof(*info));
-    const DeviceLevel &L = P->levels[level];
+    const DeviceLevel &L = P->meta[level];
     info->rows = L.rows;
     info->n_i = L.n_i;
     info->head = L.head;

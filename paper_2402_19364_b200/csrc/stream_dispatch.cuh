@@ -99,26 +99,39 @@ int run_tma(const StreamArgs &a, cudaStream_t st) {
 
 namespace kr {
 
-template <typename T, int NV, int MODE, int DIST>
+template <typename T, int NV, int MODE, int DIST, int PIPE, int G>
 int run_rec_one(const StreamArgs &a, cudaStream_t st) {
-    auto kern = k_rec<T, NV, MODE, DIST>;
+    auto kern = k_rec<T, NV, MODE, DIST, PIPE, G>;
+    constexpr int threads = 128;
     static int bps = 0;
     if (bps == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, threads, 0);
         if (bps <= 0) bps = 1;
     }
-    int64_t blocks = std::min<int64_t>((int64_t)a.num_sms * bps, (a.nbatch + 7) / 8);
+    int64_t blocks = std::min<int64_t>((int64_t)a.num_sms * bps, (a.nbatch + threads / 32 - 1) / (threads / 32));
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 256, 0, st>>>(a.keys, reinterpret_cast<const T *>(a.vals), a.bstart, a.nbatch,
-                                            reinterpret_cast<const T *>(a.X), reinterpret_cast<const T *>(a.D0),
-                                            reinterpret_cast<T *>(a.Y), reinterpret_cast<T *>(a.C0), a.k, a.counter);
+    kern<<<(unsigned)blocks, threads, 0, st>>>(a.keys, reinterpret_cast<const T *>(a.vals), a.bstart, a.nbatch,
+                                                reinterpret_cast<const T *>(a.X), reinterpret_cast<const T *>(a.D0),
+                                                reinterpret_cast<T *>(a.Y), reinterpret_cast<T *>(a.C0), a.k, a.counter);
     return (int)cudaGetLastError();
 }
 
+template <typename T, int NV, int PIPE, int G>
+int run_rec_pipe(const StreamArgs &a, cudaStream_t st) {
+    if (a.dist) return a.mode == 0 ? run_rec_one<T, NV, 0, 1, PIPE, G>(a, st) : run_rec_one<T, NV, 1, 1, PIPE, G>(a, st);
+    return a.mode == 0 ? run_rec_one<T, NV, 0, 0, PIPE, G>(a, st) : run_rec_one<T, NV, 1, 0, PIPE, G>(a, st);
+}
+
+// variants: ARROW_REC=<pipe><group>, e.g. 18 (default: one buffer of 8 rows), 14, 24, 28
 template <typename T, int NV>
 int run_rec_cfg(const StreamArgs &a, cudaStream_t st) {
-    if (a.dist) return a.mode == 0 ? run_rec_one<T, NV, 0, 1>(a, st) : run_rec_one<T, NV, 1, 1>(a, st);
-    return a.mode == 0 ? run_rec_one<T, NV, 0, 0>(a, st) : run_rec_one<T, NV, 1, 0>(a, st);
+    static const int v = kt::env_int("ARROW_REC", 18);
+    switch (v) {
+        case 14: return run_rec_pipe<T, NV, 1, 4>(a, st);
+        case 24: return run_rec_pipe<T, NV, 2, 4>(a, st);
+        case 28: return run_rec_pipe<T, NV, 2, 8>(a, st);
+        default: return run_rec_pipe<T, NV, 1, 8>(a, st);
+    }
 }
 
 // Whole-warp record kernel for rows of 16-byte multiples up to 1 KiB.  Returns -1 otherwise.

@@ -76,6 +76,17 @@ __device__ __forceinline__ void ldg_vec_pred(bool pred, const char *p, Vec<T, VB
     }
 }
 
+// Predicated coherent streaming load (evict-first) of a Y row that this warp will rewrite.
+template <typename T, int VB>
+__device__ __forceinline__ void ld_vec_pred_cs(bool pred, const char *p, Vec<T, VB> &dst) {
+    static_assert(VB == 16, "16-byte rows only");
+    uint32_t *r = reinterpret_cast<uint32_t *>(&dst);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+                 "@q ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])
+                 : "l"(p), "r"((int)pred));
+}
+
 template <typename T, int VB>
 __device__ __forceinline__ Vec<T, VB> ld_vec(const char *p) {
     using R = typename Raw<VB>::type;

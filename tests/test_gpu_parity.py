@@ -162,7 +162,7 @@ def test_profiling_counters():
         plan.spmm(X)
     kt = plan.kernel_times()
     L = plan.info()["levels"]
-    assert kt["calls"] == 3 and kt["segments"]["launches"] == 3 * L and kt["segments"]["ms"] > 0
+    assert kt["calls"] == 3 and 3 <= kt["segments"]["launches"] <= 3 * L and kt["segments"]["ms"] > 0
 
 
 def test_errors_on_device():
