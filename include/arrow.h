@@ -183,6 +183,7 @@ typedef struct {
     double ms[ARROW_K_COUNT];
     int64_t launches[ARROW_K_COUNT];
     int64_t calls;              /* arrow_spmm calls profiled */
+    double launch_ms[16];       /* by position of the launch within a call (first 16 launches) */
 } arrow_kernel_times_t;
 
 arrow_status arrow_plan_set_profiling(arrow_plan plan, int32_t on);   /* on: resets the counters */

@@ -71,7 +71,8 @@ class LevelInfo(ctypes.Structure):
 
 
 class KernelTimes(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 4), ("launches", ctypes.c_int64 * 4), ("calls", ctypes.c_int64)]
+    _fields_ = [("ms", ctypes.c_double * 4), ("launches", ctypes.c_int64 * 4), ("calls", ctypes.c_int64),
+                ("launch_ms", ctypes.c_double * 16)]
 
 
 def lib() -> ctypes.CDLL:
@@ -370,7 +371,9 @@ class Plan:
     def kernel_times(self) -> dict:
         kt = KernelTimes()
         _check(lib().arrow_plan_kernel_times(self._h, ctypes.byref(kt)), "arrow_plan_kernel_times")
-        return {"calls": kt.calls, **{KERNELS[i]: {"ms": kt.ms[i], "launches": kt.launches[i]} for i in range(4)}}
+        c = max(1, kt.calls)
+        return {"calls": kt.calls, "launch_ms": [round(kt.launch_ms[i] / c, 4) for i in range(16) if kt.launch_ms[i] > 0],
+                **{KERNELS[i]: {"ms": kt.ms[i], "launches": kt.launches[i]} for i in range(4)}}
 
     def close(self):
         if self._h:

@@ -42,7 +42,7 @@ constexpr int32_t kDefaultBatchRecords = 256;
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct ProfRec {
-    int kid;
+    int kid, pos;
     cudaEvent_t a, b;
 };
 
@@ -78,6 +78,7 @@ struct arrow_plan_s {
     bool profiling = false;
     std::vector<ProfRec> prof;
     arrow_kernel_times_t prof_acc{};
+    int prof_pos = 0;
     // distributed
     arrow_comm comm = nullptr;
     int64_t local_begin = 0, local_end = 0;
@@ -126,8 +127,11 @@ inline void put_val(std::vector<uint8_t> &dst, int64_t at, arrow_dtype pdt, doub
     }
 }
 
-// Cut the record stream into batches of >= target records, at pseudo records.
+// Cut the record stream into batches of >= target records, at pseudo records.  Small levels get
+// smaller batches (down to 32 records) so that every resident warp has a few batches to take.
 void cut_batches(BuiltLevel &B, int32_t target) {
+    const int64_t warps = 148 * 32;
+    target = (int32_t)std::max<int64_t>(32, std::min<int64_t>(target, (int64_t)B.keys.size() / (warps * 4)));
     B.bstart.clear();
     B.bstart.push_back(0);
     const int64_t m = (int64_t)B.keys.size();
@@ -762,7 +766,7 @@ inline void prof_end(arrow_plan P, cudaStream_t st, int kid, cudaEvent_t a) {
     cudaEvent_t b;
     cudaEventCreate(&b);
     cudaEventRecord(b, st);
-    P->prof.push_back(ProfRec{kid, a, b});
+    P->prof.push_back(ProfRec{kid, P->prof_pos++, a, b});
 }
 }  // namespace
 
@@ -793,6 +797,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
         return ARROW_OK;
     }
     if (P->profiling) P->prof_acc.calls += 1;
+    P->prof_pos = 0;
     CUDA_TRY(cudaMemsetAsync(P->counters, 0, P->levels.size() * sizeof(unsigned), st));
     for (size_t i = 0; i < P->levels.size(); ++i) {
         const DeviceLevel &L = P->levels[i];
@@ -915,6 +920,7 @@ arrow_status arrow_plan_kernel_times(arrow_plan P, arrow_kernel_times_t *out) {
         CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
         P->prof_acc.ms[r.kid] += ms;
         P->prof_acc.launches[r.kid] += 1;
+        if (r.pos < 16) P->prof_acc.launch_ms[r.pos] += ms;
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }

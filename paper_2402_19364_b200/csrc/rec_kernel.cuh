@@ -24,6 +24,16 @@ using ks::kPseudo;
 using ks::kRowMask;
 using ks::Vec;
 
+// acc += a * x with the accumulator as a read-write PTX operand: keeps it in one register set
+// (otherwise ptxas writes the result into the dead slot registers and copies it back at every
+// segment-flush join: 4 MOVs per record).
+__device__ __forceinline__ void fma_inplace(float &acc, float a, float x) {
+    asm("fma.rn.f32 %0, %1, %2, %0;" : "+f"(acc) : "f"(a), "f"(x));
+}
+__device__ __forceinline__ void fma_inplace(double &acc, double a, double x) {
+    asm("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc) : "d"(a), "d"(x));
+}
+
 template <typename T, int NV, int G>
 struct Rows {
     Vec<T, 16> x[G][NV];
@@ -55,7 +65,8 @@ k_rec(const uint32_t *__restrict__ keys, const T *__restrict__ vals, const uint3
     int len = 0, cb = 0;
     uint32_t r0 = 0;
 
-    // issue group g (records [g, g+8) of the batch) into buffer R
+    // issue group g (records [g, g+G) of the batch) into buffer R.  Slots that load nothing (pseudo
+    // records, records past the batch) are zeroed so the FMA below can be unconditional.
     auto issue = [&](Rows<T, NV, G> &R, int g) {
         const bool second = (g - cb) >= 32;          // warp-uniform: which chunk register holds it
         const uint32_t kc = second ? k1 : k0;
@@ -66,41 +77,44 @@ k_rec(const uint32_t *__restrict__ keys, const T *__restrict__ vals, const uint3
             const bool ld = (g + t < len) && !(key & kPseudo);
             const char *p = ((DIST && (key & kAux)) ? dl : xl) + (uint64_t)(key & kRowMask) * RB;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) ks::ldg_vec_pred<T, 16>(ld && act[v], p + v * 512, R.x[t][v]);
+            for (int v = 0; v < NV; ++v) {
+                ks::zero<T, 16>(R.x[t][v]);
+                ks::ldg_vec_pred<T, 16>(ld && act[v], p + v * 512, R.x[t][v]);
+            }
         }
     };
-    // consume group g from buffer R (g always lies in the first chunk register here)
+    // consume group g from buffer R (g always lies in the first chunk register here).  Pseudo
+    // records carry value 0 and a zero slot, so every record does the same FMA; only the flush
+    // at a segment end is a (warp-uniform) branch.
     auto consume = [&](Rows<T, NV, G> &R, int g) {
         const int lb = (g - cb) & 31;
+        const bool full = g + G <= len;
 #pragma unroll
         for (int t = 0; t < G; ++t) {
             const uint32_t key = __shfl_sync(0xffffffffu, k0, lb + t);
             const T a = __shfl_sync(0xffffffffu, v0, lb + t);
-            if (g + t < len) {
-                if (!(key & kPseudo)) {
 #pragma unroll
-                    for (int v = 0; v < NV; ++v)
+            for (int v = 0; v < NV; ++v)
 #pragma unroll
-                        for (int i = 0; i < N; ++i) acc[v].v[i] = fma(a, R.x[t][v].v[i], acc[v].v[i]);
-                } else {
-                    const uint64_t off = (uint64_t)(key & kRowMask) * RB;
+                for (int i = 0; i < N; ++i) fma_inplace(acc[v].v[i], a, R.x[t][v].v[i]);
+            if ((key & kPseudo) && (full || g + t < len)) {
+                const uint64_t off = (uint64_t)(key & kRowMask) * RB;
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        if (!act[v]) continue;
-                        if (key & kAux) {
-                            ks::red_vec<T, 16>(al + off + v * 512, acc[v]);
-                        } else if (MODE == 0) {
-                            ks::st_vec_stream<T, 16>(yl + off + v * 512, acc[v]);
-                        } else {
-                            Vec<T, 16> y = ks::ld_vec_stream<T, 16>(yl + off + v * 512);
+                for (int v = 0; v < NV; ++v) {
+                    if (!act[v]) continue;
+                    if (key & kAux) {
+                        ks::red_vec<T, 16>(al + off + v * 512, acc[v]);
+                    } else if (MODE == 0) {
+                        ks::st_vec_stream<T, 16>(yl + off + v * 512, acc[v]);
+                    } else {
+                        Vec<T, 16> y = ks::ld_vec_stream<T, 16>(yl + off + v * 512);
 #pragma unroll
-                            for (int i = 0; i < N; ++i) y.v[i] += acc[v].v[i];
-                            ks::st_vec_stream<T, 16>(yl + off + v * 512, y);
-                        }
+                        for (int i = 0; i < N; ++i) y.v[i] += acc[v].v[i];
+                        ks::st_vec_stream<T, 16>(yl + off + v * 512, y);
                     }
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) ks::zero<T, 16>(acc[v]);
                 }
+#pragma unroll
+                for (int v = 0; v < NV; ++v) ks::zero<T, 16>(acc[v]);
             }
         }
     };

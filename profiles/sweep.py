@@ -48,6 +48,8 @@ def main():
     st = torch.cuda.Stream()
     for v in args.variants.split(";"):
         o = parse(v)
+        if "ta" in o:
+            os.environ["ARROW_TAIL_ATOMIC"] = str(o["ta"])
         plan = ab.Plan(decomposition=D, dtype=dtype, window_rows=o.get("w", 0), head_chunk=o.get("hc", 0),
                        batch_segments=o.get("bs", 0))
         for _ in range(3):
@@ -66,7 +68,8 @@ def main():
         print(json.dumps({"variant": v, "ms": round(ms, 4), "GBs_alg": round(balg / ms / 1e6, 1),
                           "gflops": round(2 * g.nnz * k / ms / 1e6, 1),
                           "segments_ms": round(kt["segments"]["ms"] / kt["calls"], 4),
-                          "zero_ms": round(kt["head_stage"]["ms"] / kt["calls"], 4)}), flush=True)
+                          "zero_ms": round(kt["head_stage"]["ms"] / kt["calls"], 4),
+                          "launch_ms": kt["launch_ms"]}), flush=True)
         plan.close()
 
 
