@@ -35,7 +35,7 @@ arrow_status fail(arrow_status s, const std::string &msg) {
         if (_e != cudaSuccess) return fail(ARROW_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-constexpr int64_t kDefaultWindowRows = 65536;
+constexpr int64_t kDefaultWindowRows = 16384;
 constexpr int32_t kDefaultHeadChunk = 256;
 constexpr int32_t kDefaultBatchRecords = 256;
 
@@ -67,6 +67,9 @@ struct arrow_plan_s {
     // device memory
     void *arena = nullptr;
     int64_t arena_bytes = 0;
+    std::vector<SegLevel> seg;     // optional descriptor layout (ARROW_SEG=1) for the v2 kernel
+    std::vector<void *> seg_allocs;
+    int seg_bseg = 16;
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
     void *ws = nullptr;          // D0 | C0
     int64_t ws_k = 0;
@@ -85,6 +88,7 @@ struct arrow_plan_s {
     int64_t bytes_alg_fixed = 0, bytes_alg_rows = 0, sum_rows = 0;
 
     ~arrow_plan_s() {
+        for (void *q : seg_allocs) cudaFree(q);
         for (auto &r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
         if (arena) cudaFree(arena);
         if (ws) cudaFree(ws);
@@ -399,8 +403,13 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
     const int64_t n = D.n, b = D.b;
     // levels >= 1: L2 reductions instead of read-modify-write, all of them in one launch
-    bool tail_atomic = !comm;
-    if (const char *e = std::getenv("ARROW_TAIL_ATOMIC")) tail_atomic = tail_atomic && std::atoi(e) != 0;
+    // (measured worse on B200: L2 atomic throughput on 3M body rows > the RMW it saves; off by default)
+    bool tail_atomic = false;
+    if (const char *e = std::getenv("ARROW_TAIL_ATOMIC")) tail_atomic = !comm && std::atoi(e) != 0;
+    // kernel family: "seg" (default, descriptor layout) or "rec"/"stream"/"tma" (record-stream layout)
+    std::string ka = "seg";
+    if (const char *e = std::getenv("ARROW_KA")) ka = e;
+    const bool use_seg = (ka == "seg");
     if (n >= kMaxRows) return fail(ARROW_E_UNSUPPORTED, "n must be < 2^30 (30-bit row keys)");
 
     int dev = 0;
@@ -484,9 +493,9 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         std::vector<std::array<int64_t, 5>> offs(built.size());
         for (size_t i = 0; i < built.size(); ++i) {
             const BuiltLevel &B = built[i];
-            offs[i][0] = reserve((int64_t)B.keys.size() * 4);
-            offs[i][1] = reserve((int64_t)B.vals.size());
-            offs[i][2] = reserve((int64_t)B.bstart.size() * 4);
+            offs[i][0] = reserve(use_seg ? 0 : (int64_t)B.keys.size() * 4);
+            offs[i][1] = reserve(use_seg ? 0 : (int64_t)B.vals.size());
+            offs[i][2] = reserve(use_seg ? 0 : (int64_t)B.bstart.size() * 4);
             offs[i][3] = reserve((int64_t)B.head_rows.size() * 4);
             offs[i][4] = reserve((int64_t)B.zero_rows.size() * 4);
         }
@@ -510,14 +519,55 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
             L.bstart = reinterpret_cast<uint32_t *>(base + offs[i][2]);
             L.head_rows = reinterpret_cast<int32_t *>(base + offs[i][3]);
             L.zero_rows = reinterpret_cast<int32_t *>(base + offs[i][4]);
-            CUDA_TRY(cudaMemcpy(L.keys, B.keys.data(), B.keys.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.vals, B.vals.data(), B.vals.size(), cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.bstart, B.bstart.data(), B.bstart.size() * 4, cudaMemcpyHostToDevice));
+            if (!use_seg) {
+                CUDA_TRY(cudaMemcpy(L.keys, B.keys.data(), B.keys.size() * 4, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(L.vals, B.vals.data(), B.vals.size(), cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(L.bstart, B.bstart.data(), B.bstart.size() * 4, cudaMemcpyHostToDevice));
+            }
             CUDA_TRY(cudaMemcpy(L.head_rows, B.head_rows.data(), B.head_rows.size() * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(L.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
             P->levels.push_back(L);
         }
         P->counters = reinterpret_cast<unsigned *>(base + off_counters);
+    }
+    {
+        if (use_seg) {
+            if (const char *b2 = std::getenv("ARROW_SEG_BS")) P->seg_bseg = std::atoi(b2);
+            const size_t es = P->esize();
+            for (const BuiltLevel &B : built) {
+                std::vector<int32_t> so, ec;
+                std::vector<uint32_t> se;
+                std::vector<uint8_t> ev;
+                ev.reserve(B.vals.size());
+                for (size_t r = 0; r < B.keys.size(); ++r) {
+                    const uint32_t key = B.keys[r];
+                    if (key & kPseudoRec) {
+                        so.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (key & (kAuxRec - 1))));
+                        se.push_back((uint32_t)ec.size());
+                    } else {
+                        ec.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (key & (kAuxRec - 1))));
+                        ev.insert(ev.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
+                    }
+                }
+                SegLevel S;
+                S.nseg = (int64_t)so.size();
+                S.mode = B.mode;
+                auto up = [&](const void *src, size_t bytes) -> void * {
+                    void *d = nullptr;
+                    if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+                    P->seg_allocs.push_back(d);
+                    cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice);
+                    return d;
+                };
+                S.seg_out = (int32_t *)up(so.data(), so.size() * 4);
+                S.seg_end = (uint32_t *)up(se.data(), se.size() * 4);
+                S.ent_col = (int32_t *)up(ec.data(), ec.size() * 4);
+                S.ent_val = up(ev.data(), ev.size());
+                if (!S.seg_out || !S.seg_end || !S.ent_col || !S.ent_val)
+                    return fail(ARROW_E_CUDA, "cudaMalloc(seg layout)");
+                P->seg.push_back(S);
+            }
+        }
     }
     P->local_begin = 0;
     P->local_end = n;
@@ -810,7 +860,10 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
-        e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
+        if (!P->seg.empty())
+            e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->seg_bseg, st);
+        else
+            e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
     }

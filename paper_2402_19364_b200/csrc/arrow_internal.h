@@ -46,6 +46,7 @@ int check_symmetric(int64_t n, const int64_t *row_ptr, const int32_t *col, std::
 //                   body row p >= h_i stored (level 0) or read-modify-written (levels >= 1, S5).
 // Batches (bstart) are record ranges cut at pseudo records.
 constexpr uint32_t kPseudoRec = 0x80000000u;
+constexpr uint32_t kFlag = 0x80000000u;
 constexpr uint32_t kAuxRec = 0x40000000u;
 constexpr int64_t kMaxRows = (int64_t)1 << 30;
 
@@ -59,6 +60,18 @@ struct DeviceLevel {
     int32_t *head_rows = nullptr;  // [head] X/Y row of head vertex j
     int32_t *zero_rows = nullptr;  // [nzero] level 0: Y rows written as 0 before the level runs
 };
+
+// descriptor layout of the earlier K-A ("v2", seg_kernel.cu): entries + per-segment (out, end)
+struct SegLevel {
+    int64_t nseg = 0;
+    int mode = 0;
+    int32_t *seg_out = nullptr;   // [nseg] out row (bit 31: atomic)
+    uint32_t *seg_end = nullptr;  // [nseg] end offset into the entries
+    int32_t *ent_col = nullptr;   // [nnz] X row (bit 31: D0 row)
+    void *ent_val = nullptr;      // [nnz]
+};
+int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+               int num_sms, unsigned *counter, int bseg, void *stream);
 
 struct StreamArgs {
     const uint32_t *keys;

@@ -212,7 +212,7 @@ int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, cons
         if (p && (reinterpret_cast<uintptr_t>(p) % 16) != 0) tma = false;
     // kernel choice: ARROW_KA=rec (default for 16-byte rows <= 1 KiB), tma, stream
     const char *ka = std::getenv("ARROW_KA");
-    const std::string kas = ka ? ka : "rec";
+    const std::string kas = ka ? ka : "seg";
     StreamCfg c = pick_stream_cfg(dtype, k, X, Y, dist ? D0 : nullptr, dist ? C0 : nullptr);
     if (tma && kas == "rec") c = StreamCfg{16, -1, 0, 0};
     else if (tma && kas == "tma") c = StreamCfg{16, 0, 0, 0};

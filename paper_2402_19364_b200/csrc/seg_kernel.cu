@@ -1,0 +1,277 @@
+// seg_kernel.cu -- the earlier descriptor-based K-A ("v2"): per-segment (out, end) descriptors +
+// (col, val) entries, sub-warp batches of LPE segments, end-of-segment bit masks.  Kept as an
+// alternative path (ARROW_SEG=1 at plan creation) for A/B measurements against k_rec; layout is
+// derived from the record stream (arrow_api.cpp::derive_seg).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "arrow_internal.h"
+
+namespace arrow {
+namespace kseg {
+namespace {
+
+template <typename T, int VEC> struct VecT;
+template <> struct VecT<float, 4> { using type = float4; };
+template <> struct VecT<float, 2> { using type = float2; };
+template <> struct VecT<float, 1> { using type = float; };
+template <> struct VecT<double, 2> { using type = double2; };
+template <> struct VecT<double, 1> { using type = double; };
+
+template <typename T, int VEC> struct Frag {
+    T v[VEC];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) v[i] = T(0);
+    }
+};
+
+template <typename T, int VEC>
+__device__ __forceinline__ Frag<T, VEC> ld_x(const T *p) {  // read-only path, 16 B per lane at VEC*sizeof(T)=16
+    using V = typename VecT<T, VEC>::type;
+    V r = __ldg(reinterpret_cast<const V *>(p));
+    Frag<T, VEC> f;
+    static_assert(sizeof(V) == sizeof(f), "frag size");
+    memcpy(&f, &r, sizeof(V));
+    return f;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ Frag<T, VEC> ld_plain(const T *p) {
+    using V = typename VecT<T, VEC>::type;
+    V r = *reinterpret_cast<const V *>(p);
+    Frag<T, VEC> f;
+    memcpy(&f, &r, sizeof(V));
+    return f;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void st_stream(T *p, const Frag<T, VEC> &f) {  // evict-first: Y is write-once
+    using V = typename VecT<T, VEC>::type;
+    V r;
+    memcpy(&r, &f, sizeof(V));
+    __stcs(reinterpret_cast<V *>(p), r);
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void st_plain(T *p, const Frag<T, VEC> &f) {
+    using V = typename VecT<T, VEC>::type;
+    V r;
+    memcpy(&r, &f, sizeof(V));
+    *reinterpret_cast<V *>(p) = r;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
+    if constexpr (sizeof(T) == 4 && VEC == 4) {
+        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(f.v[0], f.v[1], f.v[2], f.v[3]));
+    } else if constexpr (sizeof(T) == 4 && VEC == 2) {
+        atomicAdd(reinterpret_cast<float2 *>(p), make_float2(f.v[0], f.v[1]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) atomicAdd(p + i, f.v[i]);
+    }
+}
+
+// ------------------------------------------------------------------------------------ K-A
+// Segment stream.  A sub-warp of LPE lanes owns a row slab of LPE*VEC elements.  Work is a list
+// of non-empty segments in tile-window order, cut into batches of LPE consecutive segments.
+// Warps grab batches dynamically from a per-launch counter (one atomic per warp per grab), so
+// all resident warps work on a narrow, advancing front of the window-ordered list and the X rows
+// of the current window stay L2-resident while every user of them runs (the IO lemma's "tiles
+// stay resident").  Lane s of a sub-warp holds the output row and end offset of
+// segment s of its batch; the batch's entries are contiguous and are streamed in chunks of LPE
+// (one coalesced load of col and val per lane).  A per-chunk bit mask of segment ends
+// (__reduce_or_sync) tells the accumulate loop where to flush; UNROLL row loads are issued
+// before their FMAs so short rows do not serialise on latency.
+//   out >= 0             : store (MODE 0, level 0) or read-modify-write (MODE 1) Y[out]
+//   out <  0, DIST == 0  : atomic add into Y[out & 0x7fffffff]  (head-row slice of one window)
+//   out <  0, DIST == 1  : atomic add into C0[out & 0x7fffffff] (head partial, reduced over ranks)
+//   col <  0 (DIST only) : the row comes from the head block D0 (broadcast), else from X
+template <typename T, int VEC, int LPE, int MODE, int DIST>
+__global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__ seg_out,
+                                                     const uint32_t *__restrict__ seg_end, int64_t nseg,
+                                                     const int32_t *__restrict__ ent_col,
+                                                     const T *__restrict__ ent_val, const T *__restrict__ X,
+                                                     const T *__restrict__ D0, T *__restrict__ Y,
+                                                     T *__restrict__ C0, int64_t k, unsigned *__restrict__ counter,
+                                                     int bseg) {
+    constexpr int UNROLL = (LPE == 32) ? 8 : 4;
+    constexpr int SLAB = LPE * VEC;
+    constexpr int SUBS = 32 / LPE;
+    const int lane = threadIdx.x & 31;
+    const int sl = lane % LPE;
+    const int sub = lane / LPE;
+    const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (sub * LPE));
+    const int64_t nbatch = (nseg + bseg - 1) / bseg;
+    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
+
+    for (;;) {
+        unsigned wb = 0;
+        if (lane == 0) wb = atomicAdd(counter, 1u);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        const int64_t bt = (int64_t)wb * SUBS + sub;
+        if ((int64_t)wb * SUBS >= nbatch) break;       // warp-uniform exit
+        if (bt >= nbatch) continue;                    // sub-warp idle this round
+        const int64_t s0 = bt * bseg;
+        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
+        const int32_t my_out = (sl < nb) ? __ldg(seg_out + s0 + sl) : 0;
+        const uint32_t my_end = (sl < nb) ? __ldg(seg_end + s0 + sl) : 0xffffffffu;
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(mask, my_end, nb - 1, LPE);
+
+        for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
+            const int64_t col0 = c0 + (int64_t)sl * VEC;
+            const bool active = col0 < k;
+            const char *xlane = reinterpret_cast<const char *>(X + (active ? col0 : 0));
+            const char *dlane = reinterpret_cast<const char *>(D0 + (active ? col0 : 0));
+            Frag<T, VEC> acc;
+            acc.zero();
+            int cur = 0;
+            for (uint32_t cb = e_begin; cb < e_end; cb += LPE) {
+                const int cnt = (e_end - cb < (uint32_t)LPE) ? (int)(e_end - cb) : LPE;
+                int32_t mycol = 0;
+                T myval = T(0);
+                if (sl < cnt) {
+                    mycol = __ldcs(ent_col + cb + sl);
+                    myval = __ldcs(ent_val + cb + sl);
+                }
+                const uint32_t rel = my_end - 1u - cb;  // position of my segment's last entry in this chunk
+                const unsigned endmask = __reduce_or_sync(mask, (rel < (uint32_t)LPE) ? (1u << rel) : 0u);
+#pragma unroll 1
+                for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
+                    Frag<T, VEC> xv[UNROLL];
+                    T av[UNROLL];
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+                        const int idx = u0 + t;
+                        const uint32_t cc = (uint32_t)__shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
+                        const T a = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
+                        const bool ok = idx < cnt;
+                        av[t] = ok ? a : T(0);
+                        const char *p;
+                        if (DIST && (int32_t)cc < 0) p = dlane + (uint64_t)(cc & 0x7fffffffu) * rowbytes;
+                        else p = xlane + (uint64_t)cc * rowbytes;
+                        if (ok && active) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
+                        else xv[t].zero();
+                    }
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        if ((u0 + t < cnt) && ((endmask >> ((u0 + t) & 31)) & 1u)) {   // sub-warp uniform
+                            const int32_t o = __shfl_sync(mask, my_out, cur, LPE);
+                            if (active) {
+                                if (o < 0) {
+                                    T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
+                                    atomic_add_frag<T, VEC>(dst + col0, acc);
+                                } else if (MODE == 0) {
+                                    st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
+                                } else {
+                                    T *py = Y + (int64_t)o * k + col0;
+                                    Frag<T, VEC> y = ld_plain<T, VEC>(py);
+#pragma unroll
+                                    for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                    st_plain<T, VEC>(py, y);
+                                }
+                            }
+                            acc.zero();
+                            ++cur;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// K-Z: zero the listed Y rows (level 0: head rows, which then accumulate head slices atomically,
+// and rows with no entry in B_0, incl. A-isolated vertices).
+
+inline int pick_vec(int dtype, int64_t k, std::initializer_list<const void *> ptrs) {
+    const int es = dtype == 1 ? 8 : 4;
+    int vec = 16 / es;
+    while (vec > 1) {
+        bool ok = (k % vec) == 0;
+        for (const void *p : ptrs) ok = ok && ((reinterpret_cast<uintptr_t>(p) % (vec * es)) == 0);
+        if (ok) break;
+        vec >>= 1;
+    }
+    return vec;
+}
+
+inline int pick_lpe(int64_t k, int vec) {
+    const int64_t need = (k + vec - 1) / vec;
+    int lpe = 1;
+    while (lpe < 32 && lpe < need) lpe <<= 1;
+    return lpe;
+}
+
+template <typename T, int VEC, int LPE, int MODE, int DIST>
+int run_segments(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
+                 unsigned *counter, int bseg, cudaStream_t st) {
+    if (bseg <= 0 || bseg > LPE) bseg = LPE;
+    auto kern = k_segments<T, VEC, LPE, MODE, DIST>;
+    static int bps = 0;
+    if (bps == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+        if (bps <= 0) bps = 1;
+    }
+    const int64_t nbatch = (L.nseg + bseg - 1) / bseg;
+    const int64_t batches_per_block = 8 * (32 / LPE);
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * bps, (nbatch + batches_per_block - 1) / batches_per_block);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
+                                            reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                            reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
+                                            reinterpret_cast<T *>(C0), k, counter, bseg);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int VEC, int MODE, int DIST>
+int run_segments_lpe(int lpe, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+                     int num_sms, unsigned *counter, int bseg, cudaStream_t st) {
+    switch (lpe) {
+        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    }
+}
+
+template <typename T, int VEC>
+int run_segments_mode(int lpe, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0,
+                      int64_t k, int num_sms, unsigned *counter, int bseg, cudaStream_t st) {
+    if (dist) {
+        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st)
+                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    }
+    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st)
+                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+}
+
+
+}  // namespace
+}  // namespace kseg
+
+int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+               int num_sms, unsigned *counter, int bseg, void *stream) {
+    using namespace kseg;
+    if (L.nseg == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
+    const int lpe = pick_lpe(k, vec);
+    if (dtype == 0) {
+        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    }
+    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+}
+
+}  // namespace arrow

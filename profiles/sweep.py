@@ -47,9 +47,14 @@ def main():
     Yd = torch.empty_like(Xd)
     st = torch.cuda.Stream()
     for v in args.variants.split(";"):
+        ka = None
+        if ":" in v:
+            ka, v = v.split(":", 1)
+        os.environ["ARROW_KA"] = ka or "seg"
         o = parse(v)
-        if "ta" in o:
-            os.environ["ARROW_TAIL_ATOMIC"] = str(o["ta"])
+        for key, env in (("ta", "ARROW_TAIL_ATOMIC"), ("sbs", "ARROW_SEG_BS")):
+            if key in o:
+                os.environ[env] = str(o[key])
         plan = ab.Plan(decomposition=D, dtype=dtype, window_rows=o.get("w", 0), head_chunk=o.get("hc", 0),
                        batch_segments=o.get("bs", 0))
         for _ in range(3):
