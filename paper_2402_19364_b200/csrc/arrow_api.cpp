@@ -36,7 +36,7 @@ arrow_status fail(arrow_status s, const std::string &msg) {
     } while (0)
 
 constexpr int64_t kDefaultWindowRows = 16384;
-constexpr int32_t kDefaultHeadChunk = 256;
+constexpr int32_t kDefaultHeadChunk = 128;
 constexpr int32_t kDefaultBatchRecords = 256;
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
