@@ -225,6 +225,15 @@ arrow_status arrow_comm_unique_id(uint8_t id[128]);
 arrow_status arrow_comm_create(int32_t nranks, int32_t rank, const uint8_t id[128], arrow_comm *out);
 arrow_status arrow_comm_destroy(arrow_comm comm);
 
+/* Host-only view of the distributed schedule of `rank` among `nranks` (no GPU, no NCCL): its pi_0
+ * row range lohi[2] = [begin, end) and, if counts != NULL, per arrow level 4*nranks + 4 int64:
+ * rows sent to / received from each rank in the forward exchange (X rows its tiles need), rows
+ * sent to / received from each rank in the reverse exchange (level>=1 results going home), then
+ * entries, segments, head rows owned and zero rows of its local work.  Used to test routing on
+ * CPU (what rank a sends to b must equal what b expects from a). */
+arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nranks, int32_t rank, int64_t window_rows,
+                                 int32_t head_chunk, int64_t *lohi, int64_t *counts);
+
 /* ---------------------------------------------------------------- diagnostics */
 const char *arrow_status_string(arrow_status s);
 const char *arrow_last_error(void);          /* thread-local detail of the last failure ("" if none) */

@@ -34,6 +34,7 @@ SYMBOLS = [
     "arrow_decomposition_export_level", "arrow_decomposition_export_residual", "arrow_decomposition_save",
     "arrow_decomposition_load", "arrow_decomposition_destroy", "arrow_plan_create_from", "arrow_comm_unique_id",
     "arrow_comm_create", "arrow_comm_destroy", "arrow_status_string", "arrow_last_error", "arrow_abi_version",
+    "arrow_dist_schedule",
 ]
 
 
@@ -116,6 +117,7 @@ def lib() -> ctypes.CDLL:
             "arrow_comm_unique_id": [p],
             "arrow_comm_create": [i32, i32, p, p],
             "arrow_comm_destroy": [p],
+            "arrow_dist_schedule": [p, i32, i32, i64, i32, p, p],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -237,6 +239,24 @@ class Decomposition:
 
     def sha256(self) -> str:
         return canonical_sha256([self.export_level(i) for i in range(self.info()["levels"])])
+
+    def dist_schedule(self, nranks: int, rank: int, window_rows: int = 0, head_chunk: int = 0) -> dict:
+        """Host-only distributed schedule of `rank` (arrow_dist_schedule): pi_0 row range and per-level
+        forward/reverse exchange row counts per peer, local entries/segments/heads/zero rows."""
+        L = self.info()["levels"]
+        lohi = np.zeros(2, np.int64)
+        per = 4 * nranks + 4
+        counts = np.zeros(max(1, L * per), np.int64)
+        _check(lib().arrow_dist_schedule(self._h, nranks, rank, window_rows, head_chunk, lohi.ctypes.data,
+                                         counts.ctypes.data), "arrow_dist_schedule")
+        levels = []
+        for i in range(L):
+            c = counts[i * per:(i + 1) * per]
+            G = nranks
+            levels.append({"send": c[0:G].copy(), "recv": c[G:2 * G].copy(), "out": c[2 * G:3 * G].copy(),
+                           "in": c[3 * G:4 * G].copy(), "entries": int(c[4 * G]), "segments": int(c[4 * G + 1]),
+                           "heads": int(c[4 * G + 2]), "zero_rows": int(c[4 * G + 3])})
+        return {"lo": int(lohi[0]), "hi": int(lohi[1]), "levels": levels}
 
     def close(self):
         if self._h:

@@ -17,6 +17,7 @@
 #include "../../include/arrow.h"
 #include "arrow_internal.h"
 #include "comm.h"
+#include "plan.h"
 
 using namespace arrow;
 
@@ -35,79 +36,9 @@ arrow_status fail(arrow_status s, const std::string &msg) {
         if (_e != cudaSuccess) return fail(ARROW_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-constexpr int64_t kDefaultWindowRows = 16384;
-constexpr int32_t kDefaultHeadChunk = 128;
-constexpr int32_t kDefaultBatchRecords = 256;
-
-inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
-
-struct ProfRec {
-    int kid, pos;
-    cudaEvent_t a, b;
-};
-
 }  // namespace
 
-struct arrow_plan_s {
-    int device = 0;
-    int num_sms = 148;
-    arrow_dtype dtype = ARROW_F32;
-    int order = ARROW_ORDER_ORIGINAL;
-    int64_t n = 0, nnz = 0, b = 0;
-    int64_t isolated = 0;
-    int64_t residual_nnz = 0;
-    int64_t max_head = 0;
-    double create_seconds = 0;
-    std::vector<DeviceLevel> levels;  // device launch list: level 0, then levels >= 1 (+ residual), possibly merged
-    std::vector<DeviceLevel> meta;    // per arrow level (+ residual) metadata for introspection
-    int32_t arrow_levels = 0;
-    // host copy of the canonical levels for export
-    std::vector<HostLevel> host_levels;
-    std::vector<std::vector<uint8_t>> host_level_vals;  // per level, plan dtype
-    // device memory
-    void *arena = nullptr;
-    int64_t arena_bytes = 0;
-    std::vector<SegLevel> seg;     // optional descriptor layout (ARROW_SEG=1) for the v2 kernel
-    std::vector<void *> seg_allocs;
-    int seg_bseg = 16;
-    unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
-    void *ws = nullptr;          // D0 | C0
-    int64_t ws_k = 0;
-    void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
-    int64_t host_k = 0;
-    cudaStream_t stream = nullptr;
-    bool poisoned = false;
-    // profiling
-    bool profiling = false;
-    std::vector<ProfRec> prof;
-    arrow_kernel_times_t prof_acc{};
-    int prof_pos = 0;
-    // distributed
-    arrow_comm comm = nullptr;
-    int64_t local_begin = 0, local_end = 0;
-    int64_t bytes_alg_fixed = 0, bytes_alg_rows = 0, sum_rows = 0;
-
-    ~arrow_plan_s() {
-        for (void *q : seg_allocs) cudaFree(q);
-        for (auto &r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
-        if (arena) cudaFree(arena);
-        if (ws) cudaFree(ws);
-        if (host_x) cudaFree(host_x);
-        if (host_y) cudaFree(host_y);
-    }
-    size_t esize() const { return dtype == ARROW_F64 ? 8 : 4; }
-};
-
-// Host decomposition object: canonical levels (values as fp64) + residual triples.
-struct arrow_decomposition_s {
-    int64_t n = 0, b = 0;
-    uint64_t seed = 4;
-    int64_t isolated = 0;
-    std::vector<HostLevel> levels;
-    std::vector<int32_t> res_u, res_v;  // residual entries, original ids, CSR order
-    std::vector<double> res_a;
-    double seconds = 0;
-};
+arrow_status arrow::set_error(arrow_status s, const std::string &msg) { return fail(s, msg); }
 
 // ------------------------------------------------------------------------------------ layout
 namespace {
@@ -485,6 +416,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         built.push_back(std::move(M));
     }
 
+    if (!comm) {
     // upload: one arena for all launch levels
     {
         const size_t es = P->esize();
@@ -530,7 +462,8 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         }
         P->counters = reinterpret_cast<unsigned *>(base + off_counters);
     }
-    {
+    }
+    if (!comm) {
         if (use_seg) {
             if (const char *b2 = std::getenv("ARROW_SEG_BS")) P->seg_bseg = std::atoi(b2);
             const size_t es = P->esize();
@@ -572,7 +505,8 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     P->local_begin = 0;
     P->local_end = n;
     if (comm) {
-        arrow_status cs = comm_attach(P.get(), comm);
+        P->comm = comm;
+        arrow_status cs = dist_build(P.get(), D, comm, window_rows, head_chunk);
         if (cs != ARROW_OK) return cs;
     }
     P->create_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -768,7 +702,6 @@ arrow_status arrow_plan_destroy(arrow_plan plan) {
     if (cur != dev) cudaSetDevice(dev);
     if (plan->stream) cudaStreamSynchronize(plan->stream);
     else cudaDeviceSynchronize();
-    if (plan->comm) comm_detach(plan);
     delete plan;
     if (cur != dev) cudaSetDevice(cur);
     return ARROW_OK;
@@ -835,11 +768,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     const char *xa = (const char *)X, *ya = (const char *)Y;
     if (xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (P->comm) {
-        arrow_status s = ensure_ws(P, k);
-        if (s != ARROW_OK) return s;
-        return comm_spmm(P, X, Y, k, st);
-    }
+    if (P->dist) return dist_spmm(P, X, Y, k, st);
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
     if (P->levels.empty()) {
         int e = launch_zero(Y, bytes, st);

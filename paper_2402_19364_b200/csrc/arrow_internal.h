@@ -101,5 +101,7 @@ int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, in
                          int add, void *Y, void *stream);
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream);
 int launch_zero(void *Y, int64_t bytes, void *stream);
+int launch_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k, int add,
+                void *dst, void *stream);
 
 }  // namespace arrow

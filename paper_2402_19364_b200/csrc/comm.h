@@ -4,6 +4,17 @@
 
 #include "../../include/arrow.h"
 
-arrow_status comm_attach(arrow_plan plan, arrow_comm comm);
-void comm_detach(arrow_plan plan);
-arrow_status comm_spmm(arrow_plan plan, const void *X, void *Y, int64_t k, cudaStream_t st);
+struct arrow_comm_s {
+    void *comm = nullptr;  // ncclComm_t
+    int nranks = 1, rank = 0;
+};
+
+struct arrow_decomposition_s;
+
+namespace arrow {
+arrow_status comm_status(int nccl_result, const char *what);
+// Build this rank's part of a distributed plan (dist.cpp).
+arrow_status dist_build(arrow_plan plan, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
+                        int32_t head_chunk);
+arrow_status dist_spmm(arrow_plan plan, const void *X, void *Y, int64_t k, cudaStream_t st);
+}  // namespace arrow

@@ -269,6 +269,46 @@ int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, in
     return (int)cudaGetLastError();
 }
 
+// generic row mover for the distributed path: dst[didx ? didx[i] : i] (= | +=) src[sidx ? sidx[i] : i]
+namespace {
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_rows(const T *__restrict__ src, const int32_t *__restrict__ sidx,
+                                              const int32_t *__restrict__ didx, int64_t n, int64_t k, int add,
+                                              T *__restrict__ dst) {
+    const int64_t kv = k / VEC, total = n * kv;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / kv, c = (t - i * kv) * VEC;
+        const int64_t si = sidx ? (int64_t)__ldg(sidx + i) : i;
+        const int64_t di = didx ? (int64_t)__ldg(didx + i) : i;
+        Frag<T, VEC> a = ld_plain<T, VEC>(src + si * k + c);
+        T *p = dst + di * k + c;
+        if (add) {
+            Frag<T, VEC> y = ld_plain<T, VEC>(p);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) a.v[q] += y.v[q];
+        }
+        st_plain<T, VEC>(p, a);
+    }
+}
+}  // namespace
+
+int launch_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k, int add,
+                void *dst, void *stream) {
+    if (n == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {src, dst});
+    const unsigned g = grid_for(n * (k / vec));
+    if (dtype == 0) {
+        if (vec == 4) k_rows<float, 4><<<g, 256, 0, st>>>((const float *)src, sidx, didx, n, k, add, (float *)dst);
+        else if (vec == 2) k_rows<float, 2><<<g, 256, 0, st>>>((const float *)src, sidx, didx, n, k, add, (float *)dst);
+        else k_rows<float, 1><<<g, 256, 0, st>>>((const float *)src, sidx, didx, n, k, add, (float *)dst);
+    } else {
+        if (vec == 2) k_rows<double, 2><<<g, 256, 0, st>>>((const double *)src, sidx, didx, n, k, add, (double *)dst);
+        else k_rows<double, 1><<<g, 256, 0, st>>>((const double *)src, sidx, didx, n, k, add, (double *)dst);
+    }
+    return (int)cudaGetLastError();
+}
+
 int launch_zero(void *Y, int64_t bytes, void *stream) {
     if (bytes == 0) return 0;
     return (int)cudaMemsetAsync(Y, 0, (size_t)bytes, reinterpret_cast<cudaStream_t>(stream));

@@ -1,0 +1,101 @@
+// plan.h -- internal definitions of the plan and decomposition objects (shared by arrow_api.cpp
+// and dist.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/arrow.h"
+#include "arrow_internal.h"
+
+namespace arrow {
+
+arrow_status set_error(arrow_status s, const std::string &msg);  // thread-local detail (arrow_last_error)
+
+constexpr int64_t kDefaultWindowRows = 16384;
+constexpr int32_t kDefaultHeadChunk = 128;
+constexpr int32_t kDefaultBatchRecords = 256;
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct ProfRec {
+    int kid, pos;
+    cudaEvent_t a, b;
+};
+
+struct DistState;  // dist.cpp
+void dist_free(DistState *d);
+
+}  // namespace arrow
+
+using arrow::DeviceLevel;
+using arrow::HostLevel;
+using arrow::ProfRec;
+using arrow::SegLevel;
+
+struct arrow_plan_s {
+    int device = 0;
+    int num_sms = 148;
+    arrow_dtype dtype = ARROW_F32;
+    int order = ARROW_ORDER_ORIGINAL;
+    int64_t n = 0, nnz = 0, b = 0;
+    int64_t isolated = 0;
+    int64_t residual_nnz = 0;
+    int64_t max_head = 0;
+    double create_seconds = 0;
+    std::vector<DeviceLevel> levels;  // device launch list: level 0, then levels >= 1 (+ residual), possibly merged
+    std::vector<DeviceLevel> meta;    // per arrow level (+ residual) metadata for introspection
+    int32_t arrow_levels = 0;
+    // host copy of the canonical levels for export
+    std::vector<HostLevel> host_levels;
+    std::vector<std::vector<uint8_t>> host_level_vals;  // per level, plan dtype
+    // device memory
+    void *arena = nullptr;
+    int64_t arena_bytes = 0;
+    std::vector<SegLevel> seg;     // optional descriptor layout (ARROW_SEG=1) for the v2 kernel
+    std::vector<void *> seg_allocs;
+    int seg_bseg = 16;
+    unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
+    void *ws = nullptr;          // D0 | C0
+    int64_t ws_k = 0;
+    void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
+    int64_t host_k = 0;
+    cudaStream_t stream = nullptr;
+    bool poisoned = false;
+    // profiling
+    bool profiling = false;
+    std::vector<ProfRec> prof;
+    arrow_kernel_times_t prof_acc{};
+    int prof_pos = 0;
+    // distributed
+    arrow_comm comm = nullptr;
+    int64_t local_begin = 0, local_end = 0;
+    int64_t bytes_alg_fixed = 0, bytes_alg_rows = 0, sum_rows = 0;
+
+    arrow::DistState *dist = nullptr;
+
+    ~arrow_plan_s() {
+        if (dist) arrow::dist_free(dist);
+        for (void *q : seg_allocs) cudaFree(q);
+        for (auto &r : prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+        if (arena) cudaFree(arena);
+        if (ws) cudaFree(ws);
+        if (host_x) cudaFree(host_x);
+        if (host_y) cudaFree(host_y);
+    }
+    size_t esize() const { return dtype == ARROW_F64 ? 8 : 4; }
+};
+
+// Host decomposition object: canonical levels (values as fp64) + residual triples.
+struct arrow_decomposition_s {
+    int64_t n = 0, b = 0;
+    uint64_t seed = 4;
+    int64_t isolated = 0;
+    std::vector<HostLevel> levels;
+    std::vector<int32_t> res_u, res_v;  // residual entries, original ids, CSR order
+    std::vector<double> res_a;
+    double seconds = 0;
+};
+

@@ -1,0 +1,61 @@
+"""Worker for the multi-GPU parity test: one process per GPU, NCCL comm from arrow_comm_*; each rank
+computes its pi_0 row shard of Y = A X and checks it against the oracle O1 rows (fp64: bitwise on
+dyadic data; fp32: 1e-4 Frobenius).  Run under torchrun or spawned by tests/test_gpu_dist.py."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CASES = [("RMAT(12,8,1)", 64, 16, "f64"), ("RMAT(14,8,2)", 256, 128, "f32"), ("GRID(128,1)", 256, 32, "f64"),
+         ("TREE(5000,3)", 16, 8, "f64"), ("RMAT(10,4,3)", 1024, 4, "f64")]
+
+
+def run(rank, world, port):
+    import torch
+    import torch.distributed as dist
+    import datagen
+    import oracle
+    import paper_2402_19364_b200 as ab
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(port))
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = [ab.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = ab.Comm(world, rank, uid[0])
+    fails = []
+    for spec, b, k, dtype in CASES:
+        g = datagen.make_graph(spec)
+        X = datagen.make_x(g.n, k, dtype=np.float64 if dtype == "f64" else np.float32)
+        plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, b, dtype=dtype, comm=comm)
+        lo, hi = plan.local_begin, plan.local_end
+        perm0 = plan.export_level(0)[0]
+        rows = perm0[lo:hi]
+        Xl = torch.from_numpy(np.ascontiguousarray(X[rows])).cuda()
+        for rep in range(2):
+            Y = plan.spmm(Xl)
+            torch.cuda.synchronize()
+        Y = Y.cpu().numpy().astype(np.float64)
+        ref = oracle.spmm_rows(g.row_ptr, g.col, g.val, X, rows)
+        if dtype == "f64":
+            ok = np.array_equal(Y, ref)
+        else:
+            den = np.linalg.norm(ref)
+            ok = (np.linalg.norm(Y - ref) / den if den > 0 else np.linalg.norm(Y)) <= 1e-4
+        if not ok:
+            fails.append(f"{spec} b={b} k={k} {dtype} rank {rank}: max err {np.abs(Y - ref).max()}")
+        plan.close()
+    comm.close()
+    dist.destroy_process_group()
+    return fails
+
+
+if __name__ == "__main__":
+    r = int(os.environ.get("RANK", "0"))
+    w = int(os.environ.get("WORLD_SIZE", "1"))
+    f = run(r, w, 29511)
+    print("DIST_OK" if not f else "DIST_FAIL " + "; ".join(f), flush=True)
+    sys.exit(0 if not f else 1)
