@@ -758,15 +758,16 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
     if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
     if (k == 0 || P->n == 0) return ARROW_OK;
-    if (!X || !Y) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
+    const int64_t rows = P->local_end - P->local_begin;
+    // a rank of a distributed plan may own no rows but must still take part in the collectives
+    if ((!X || !Y) && !(P->dist && rows == 0)) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
     int cur = 0;
     CUDA_TRY(cudaGetDevice(&cur));
     if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
     if (k * (int64_t)P->esize() >= ((int64_t)1 << 32)) return fail(ARROW_E_UNSUPPORTED, "row of X exceeds 4 GiB");
-    const int64_t rows = P->local_end - P->local_begin;
     const int64_t bytes = rows * k * (int64_t)P->esize();
     const char *xa = (const char *)X, *ya = (const char *)Y;
-    if (xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
+    if (rows > 0 && xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (P->dist) return dist_spmm(P, X, Y, k, st);
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;

@@ -372,9 +372,14 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     auto row = [&](int64_t r) { return ws + (size_t)r * k * es; };
     const char *Xc = reinterpret_cast<const char *>(X);
     char *Yc = reinterpret_cast<char *>(Y);
-    cudaEvent_t ev0 = nullptr;
-    if (P->profiling) { cudaEventCreate(&ev0); cudaEventRecord(ev0, st); }
-
+    // profiling: three intervals (pre-exchange, compute, post-exchange), each with its own event pair
+    cudaEvent_t pe[6] = {};
+    auto mark = [&](int i) {
+        if (!P->profiling) return;
+        cudaEventCreate(&pe[i]);
+        cudaEventRecord(pe[i], st);
+    };
+    mark(0);
     // 1. D0 (owners fill their head rows), C0 = 0, pack the forward rows
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(0), 0, (size_t)(S->d0_rows + S->c0_rows) * k * es, st));
@@ -397,8 +402,8 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         if (!DL.recv_cnt.empty() && DL.send_cnt[me])
             DCUDA(cudaMemcpyAsync(row(DL.o_halo + DL.recv_off[me]), row(DL.o_send + DL.send_off[me]),
                                   (size_t)DL.send_cnt[me] * k * es, cudaMemcpyDeviceToDevice, st));
-    cudaEvent_t ev1 = nullptr;
-    if (P->profiling) { cudaEventCreate(&ev1); cudaEventRecord(ev1, st); }
+    mark(1);
+    mark(2);
 
     // 2. local compute per level
     for (int i = 0; i < nl; ++i) {
@@ -408,8 +413,8 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         void *dst = (i == 0) ? Y : (void *)row(DL.o_out);
         DK(launch_seg(dt, 1, DL.seg, src, row(DL.o_d0), dst, row(DL.o_c0), k, P->num_sms, S->counters + i, S->bseg, st));
     }
-    cudaEvent_t ev2 = nullptr;
-    if (P->profiling) { cudaEventCreate(&ev2); cudaEventRecord(ev2, st); }
+    mark(3);
+    mark(4);
 
     // 3. reverse exchange + head reduction
     DNCCL(ncclGroupStart());
@@ -434,13 +439,11 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         if (DL.in_rows_n) DK(launch_rows(dt, row(DL.o_in), nullptr, DL.in_rows, DL.in_rows_n, k, 1, Y, st));
         DK(launch_rows(dt, row(DL.o_c0), DL.head_j, DL.head_row, DL.nhead_own, k, 1, Y, st));
     }
+    mark(5);
     if (P->profiling) {
-        cudaEvent_t ev3;
-        cudaEventCreate(&ev3);
-        cudaEventRecord(ev3, st);
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, ev0, ev1});
-        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, ev1, ev2});
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, ev2, ev3});
+        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, pe[0], pe[1]});
+        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, pe[2], pe[3]});
+        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, pe[4], pe[5]});
         P->prof_acc.calls += 1;
     }
     (void)Xc;
