@@ -23,6 +23,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -380,6 +382,16 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         cudaEventRecord(pe[i], st);
     };
     mark(0);
+    static const bool trace = std::getenv("ARROW_DIST_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&]() {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.push_back(e);
+    };
+    tmark();
     // 1. D0 (owners fill their head rows), C0 = 0, pack the forward rows
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(0), 0, (size_t)(S->d0_rows + S->c0_rows) * k * es, st));
@@ -387,6 +399,7 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         DK(launch_rows(dt, X, DL.head_row, DL.head_j, DL.nhead_own, k, 0, row(DL.o_d0), st));
         if (DL.send_rows) DK(launch_rows(dt, X, DL.send_idx, nullptr, DL.send_rows, k, 0, row(DL.o_send), st));
     }
+    tmark();  // after memsets, D0 fill, pack
     DNCCL(ncclGroupStart());
     for (auto &DL : S->L) {
         if (DL.recv_cnt.empty()) continue;
@@ -398,10 +411,12 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     }
     DNCCL(ncclAllReduce(row(0), row(0), S->d0_rows * k, nt, ncclSum, S->comm, st));
     DNCCL(ncclGroupEnd());
+    tmark();  // after forward exchange + D0 all-reduce
     for (auto &DL : S->L)
         if (!DL.recv_cnt.empty() && DL.send_cnt[me])
             DCUDA(cudaMemcpyAsync(row(DL.o_halo + DL.recv_off[me]), row(DL.o_send + DL.send_off[me]),
                                   (size_t)DL.send_cnt[me] * k * es, cudaMemcpyDeviceToDevice, st));
+    tmark();  // after self copies
     mark(1);
     mark(2);
 
@@ -415,6 +430,7 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     }
     mark(3);
     mark(4);
+    tmark();  // after compute
 
     // 3. reverse exchange + head reduction
     DNCCL(ncclGroupStart());
@@ -428,6 +444,7 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     }
     DNCCL(ncclAllReduce(row(S->d0_rows), row(S->d0_rows), S->c0_rows * k, nt, ncclSum, S->comm, st));
     DNCCL(ncclGroupEnd());
+    tmark();  // after reverse exchange + C0 all-reduce
     for (auto &DL : S->L)
         if (!DL.out_cnt.empty() && DL.out_cnt[me])
             DCUDA(cudaMemcpyAsync(row(DL.o_in + DL.in_off[me]), row(DL.o_out + DL.out_off[me]),
@@ -440,6 +457,27 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         DK(launch_rows(dt, row(DL.o_c0), DL.head_j, DL.head_row, DL.nhead_own, k, 1, Y, st));
     }
     mark(5);
+    tmark();  // after adds
+    if (trace && !tev.empty()) {
+        cudaEventSynchronize(tev.back());
+        std::string line = "[arrow dist rank " + std::to_string(me) + "] phases ms:";
+        for (size_t i = 1; i < tev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
+            line += " " + std::to_string(ms);
+        }
+        int64_t fs = 0, fr = 0, rs = 0, rr = 0;
+        for (auto &DL : S->L) {
+            for (int g = 0; g < G && !DL.recv_cnt.empty(); ++g) {
+                if (g == me) continue;
+                fs += DL.send_cnt[g]; fr += DL.recv_cnt[g]; rs += DL.out_cnt[g]; rr += DL.in_cnt[g];
+            }
+        }
+        line += " | rows fwd send " + std::to_string(fs) + " recv " + std::to_string(fr) + ", rev send " +
+                std::to_string(rs) + " recv " + std::to_string(rr) + ", d0/c0 rows " + std::to_string(S->d0_rows);
+        fprintf(stderr, "%s\n", line.c_str());
+        for (auto e : tev) cudaEventDestroy(e);
+    }
     if (P->profiling) {
         P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, pe[0], pe[1]});
         P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, pe[2], pe[3]});
