@@ -101,7 +101,11 @@ int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, in
                          int add, void *Y, void *stream);
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream);
 int launch_zero(void *Y, int64_t bytes, void *stream);
+// dst[didx[i]] (= | +=) src[sidx[i]] (identity when an index list is NULL; sidx[i] < 0 writes zero)
 int launch_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k, int add,
                 void *dst, void *stream);
+// dst[drow[r]] += sum of src[sidx[e]] for e in [ptr[r], ptr[r+1]) (CSR of contributions, list order)
+int launch_gather_add(int dtype, const void *src, const int32_t *ptr, const int32_t *sidx, const int32_t *drow,
+                      int64_t n, int64_t k, void *dst, void *stream);
 
 }  // namespace arrow

@@ -5,28 +5,35 @@
 // moves X rows forward to the ranks of the next matrix (permutation pi_{j+1} o pi_j^-1)
 // and the partial results back ("aggregated in reverse order").  Lemma 6.1 / Thm 6.2
 // give the costs; their sorting network is unnecessary here (routes are static and NVSwitch is
-// one hop), so each exchange is one grouped NCCL send/recv with routes computed at plan time.
+// one hop), so each exchange is ONE grouped NCCL send/recv per peer, routes computed at plan time.
 //
 // Layout (ARROW_ORDER_PERMUTED, R18): rank g owns the contiguous pi_0 row range [lo_g, hi_g) of X
 // and Y, made of whole level-0 tiles balanced by cost (A-isolated rows go to the last rank).  For
 // every level i the tiles are split contiguously by cost as well; rank g computes the body rows
 // and the head-row slices B^(0,t) X_t of its level-i tiles (Alg. 1's co-location, R17).
-// Per arrow_spmm call:
-//   1. D0_i = X[head_i] assembled on every rank (owners fill their rows, one all-reduce for all
-//      levels) -- Alg. 1 line 1; the level>=1 rows a rank's tiles need are packed by their home
-//      ranks and exchanged (grouped send/recv) -- Alg. 2 forward propagation.
-//   2. local K-A per level (the descriptor kernel in distributed mode: head columns read D0,
-//      head partials add into C0, body rows are stored locally (level 0) or into a staging buffer
-//      grouped by home rank (levels >= 1)).
-//   3. staging rows go home (grouped send/recv) and all C0 are all-reduced -- Alg. 1 line 3 and
-//      Alg. 2 reverse aggregation; homes add them into Y.
+// Communication buffers are peer-major (for peer g: level 1, level 2, ...), so every exchange is
+// one contiguous send and one contiguous receive per peer; a rank's own rows never leave the GPU
+// (packed straight into its halo, added straight from its staging buffer).
+//
+// Per arrow_spmm call (compute stream S = the caller's, communication stream C):
+//   S: one row-mover launch: D0 rows (owners copy X, others zero), C0 = 0, X rows packed for the
+//      peers and for this rank's own halo; zero Y rows no K-A launch writes                 -> e0
+//   C: all-reduce D0 of level 0 -> e1; grouped send/recv of the forward rows + all-reduce of the
+//      other levels' D0 -> e2                            (Alg. 1 line 1, Alg. 2 forward propagation)
+//   S: wait e1; K-A level 0 (overlaps the forward exchange); wait e2; K-A levels >= 1 into the
+//      peer-major staging buffer -> e3
+//   C: wait e3; grouped send/recv of the staging rows to their homes + all-reduce of every C0
+//      -> e4                                             (Alg. 1 line 3, Alg. 2 reverse aggregation)
+//   S: add this rank's own staging rows (overlaps the reverse exchange); wait e4; add received
+//      rows and owned head partials -- both as CSR gather-adds, contributions in level order.
+// K-A leaves ARROW_DIST_RESERVE_SMS (default 16) SMs' worth of blocks out so that the NCCL kernels
+// can run next to it.
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <numeric>
 #include <string>
 #include <vector>
 
@@ -35,32 +42,11 @@
 
 namespace arrow {
 
-struct DistLevel {
-    int64_t h = 0;
-    SegLevel seg;
-    // forward exchange (levels >= 1)
-    int64_t halo_rows = 0, send_rows = 0;
-    std::vector<int64_t> recv_cnt, recv_off, send_cnt, send_off;
-    int32_t *send_idx = nullptr;
-    // reverse exchange (levels >= 1)
-    int64_t out_rows = 0, in_rows_n = 0;
-    std::vector<int64_t> out_cnt, out_off, in_cnt, in_off;
-    int32_t *in_rows = nullptr;
-    // heads whose home is this rank
-    int64_t nhead_own = 0;
-    int32_t *head_j = nullptr, *head_row = nullptr;
-    // level 0: rows written as zero (entry-less rows of the home range)
-    int64_t nzero = 0;
-    int32_t *zero_rows = nullptr;
-    // row offsets inside the k-dependent workspace
-    int64_t o_d0 = 0, o_c0 = 0, o_halo = 0, o_send = 0, o_out = 0, o_in = 0;
-};
-
 // host side of one rank's part of one level (computed without a GPU; uploaded by dist_build)
 struct DistHostLevel {
     int64_t h = 0;
-    std::vector<int64_t> recv_cnt, send_cnt, out_cnt, in_cnt;
-    std::vector<int32_t> send_idx, in_rows, head_j, head_row, zero_rows;
+    std::vector<int64_t> recv_cnt, send_cnt, out_cnt, in_cnt;  // per peer (levels >= 1)
+    std::vector<int32_t> head_j, head_row, zero_rows;
     std::vector<int32_t> seg_out, ent_col;
     std::vector<uint32_t> seg_end;
     std::vector<uint8_t> ent_val;
@@ -70,39 +56,68 @@ struct DistHost {
     int G = 1, me = 0;
     int64_t lo = 0, hi = 0;
     std::vector<DistHostLevel> L;
+    // peer-major, levels >= 1 concatenated per peer:
+    std::vector<int32_t> send_idx_peers;  // local X rows packed for the peers (peer order, me skipped)
+    std::vector<int32_t> send_idx_self;   // local X rows packed into my own halo chunk
+    std::vector<int32_t> in_rows_peers;   // local Y rows of the received rows (peer order, me skipped)
+    std::vector<int32_t> in_rows_self;    // local Y rows of my own staging chunk
+    std::vector<int64_t> send_peer, recv_peer, out_peer, in_peer;  // per-peer totals (rows)
+    int64_t halo_rows = 0, out_rows = 0;                             // incl. my own chunks
+    int64_t halo_self_off = 0, out_self_off = 0;                     // my own chunks' offsets
 };
 
 struct DistState {
     ncclComm_t comm = nullptr;
     int G = 1, me = 0;
     int64_t lo = 0, hi = 0;
-    std::vector<DistLevel> L;
-    std::vector<void *> allocs;
-    unsigned *counters = nullptr;
-    int64_t d0_rows = 0, c0_rows = 0, ws_rows = 0;
+    int nl = 0;
+    std::vector<int64_t> h, d0_off;  // head rows per level, offset of the level inside D0 / C0
+    int64_t d0_rows = 0;
+    std::vector<SegLevel> seg;
+    std::vector<int64_t> send_peer, recv_peer, out_peer, in_peer;
+    // k-dependent workspace (rows): [D0 | C0 | halo | send | staging | recv]
+    int64_t o_d0 = 0, o_c0 = 0, o_halo = 0, o_send = 0, o_out = 0, o_in = 0, ws_rows = 0;
+    // pre-exchange row mover (src X, dst workspace) and Y rows to zero
+    int32_t *pre_src = nullptr, *pre_dst = nullptr, *zero_rows = nullptr;
+    int64_t n_pre = 0, n_zero = 0;
+    // CSR gather-adds into Y: own staging rows / received rows + head partials (src: workspace rows)
+    int32_t *self_ptr = nullptr, *self_src = nullptr, *self_dst = nullptr;
+    int32_t *post_ptr = nullptr, *post_src = nullptr, *post_dst = nullptr;
+    int64_t n_self = 0, n_post = 0;
     void *ws = nullptr;
     int64_t ws_k = 0;
-    int bseg = 16;
+    std::vector<void *> allocs;
+    unsigned *counters = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[5] = {};
+    int bseg = 16, reserve_sms = 16;
+    int64_t fwd_rows = 0, rev_rows = 0;  // rows exchanged with peers (trace)
 };
 
 void dist_free(DistState *d) {
     if (!d) return;
+    if (d->cs) cudaStreamSynchronize(d->cs);
     for (void *p : d->allocs) cudaFree(p);
     if (d->ws) cudaFree(d->ws);
+    for (auto e : d->ev)
+        if (e) cudaEventDestroy(e);
+    if (d->cs) cudaStreamDestroy(d->cs);
     delete d;
 }
 
 namespace {
 
 template <typename V>
-int32_t *upload(DistState *S, const std::vector<V> &v, bool &ok) {
+int32_t *upload(DistState *S, const V *data, size_t count, bool &ok) {
     void *d = nullptr;
-    const size_t bytes = std::max<size_t>(v.size() * sizeof(V), 16);
+    const size_t bytes = std::max<size_t>(count * sizeof(V), 16);
     if (cudaMalloc(&d, bytes) != cudaSuccess) { ok = false; return nullptr; }
     S->allocs.push_back(d);
-    if (!v.empty() && cudaMemcpy(d, v.data(), v.size() * sizeof(V), cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
+    if (count && cudaMemcpy(d, data, count * sizeof(V), cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
     return reinterpret_cast<int32_t *>(d);
 }
+template <typename V>
+int32_t *upload(DistState *S, const std::vector<V> &v, bool &ok) { return upload(S, v.data(), v.size(), ok); }
 
 // contiguous split of tiles [0, T) into G ranges of ~equal cost; returns G+1 tile boundaries
 std::vector<int64_t> split_tiles(const std::vector<int64_t> &cost, int G) {
@@ -114,8 +129,7 @@ std::vector<int64_t> split_tiles(const std::vector<int64_t> &cost, int G) {
     for (int g = 1; g < G; ++g) {
         const double target = (double)pre[T] * g / G;
         tb[g] = std::lower_bound(pre.begin(), pre.end(), (int64_t)target) - pre.begin();
-        tb[g] = std::max(tb[g], tb[g - 1]);
-        tb[g] = std::min(tb[g], T);
+        tb[g] = std::min(std::max(tb[g], tb[g - 1]), T);
     }
     return tb;
 }
@@ -127,6 +141,26 @@ std::vector<int64_t> tile_costs(const HostLevel &L, int64_t b) {
     for (int64_t j = 0; j < h; ++j)
         for (int64_t e = L.row_ptr[j]; e < L.row_ptr[j + 1]; ++e) cost[L.col[e] / b] += 1;
     return cost;
+}
+
+// CSR of (dst, src) contributions grouped by dst, contributions of one dst kept in list order
+void build_csr(const std::vector<std::pair<int32_t, int32_t>> &c, std::vector<int32_t> &ptr, std::vector<int32_t> &src,
+               std::vector<int32_t> &dst) {
+    std::vector<int32_t> ord(c.size());
+    for (size_t i = 0; i < c.size(); ++i) ord[i] = (int32_t)i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return c[a].first < c[b].first; });
+    ptr.assign(1, 0);
+    src.clear();
+    dst.clear();
+    for (size_t i = 0; i < ord.size(); ++i) {
+        const auto &e = c[ord[i]];
+        if (dst.empty() || dst.back() != e.first) {
+            if (!dst.empty()) ptr.push_back((int32_t)src.size());
+            dst.push_back(e.first);
+        }
+        src.push_back(e.second);
+    }
+    if (!dst.empty()) ptr.push_back((int32_t)src.size());
 }
 
 }  // namespace
@@ -155,78 +189,112 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     H.lo = los[me];
     H.hi = los[me + 1];
     const int64_t lo = H.lo, hi = H.hi;
-    auto owner = [&](int64_t P0) -> int { return (int)(std::upper_bound(los.begin() + 1, los.end() - 1, P0) - (los.begin() + 1)); };
+    auto owner = [&](int64_t P0) -> int {
+        return (int)(std::upper_bound(los.begin() + 1, los.end() - 1, P0) - (los.begin() + 1));
+    };
 
+    // ---- pass 1: tile split and per-peer counts of every level
+    std::vector<std::vector<int64_t>> tbs(nl);
+    auto range = [&](int i, int g, int64_t &qa, int64_t &qb) {
+        const int64_t n_i = D.levels[i].n_i;
+        if (i == 0) { qa = std::min(los[g], n_i); qb = std::min(los[g + 1], n_i); }
+        else { qa = std::min<int64_t>(n_i, tbs[i][g] * b); qb = std::min<int64_t>(n_i, tbs[i][g + 1] * b); }
+    };
+    auto tile_owner = [&](int i, int64_t q) -> int {
+        if (i == 0) return owner(q);
+        return (int)(std::upper_bound(tbs[i].begin() + 1, tbs[i].end() - 1, q / b) - (tbs[i].begin() + 1));
+    };
     H.L.resize(nl);
+    // sl[i][g]: local X rows I own that g's level-i tiles need (g's halo slot order);
+    // il[i][g]: local Y rows of g's level-i body rows whose home is me (g's staging order)
+    std::vector<std::vector<std::vector<int32_t>>> sl(nl), il(nl);
     for (int i = 0; i < nl; ++i) {
         const HostLevel &L = D.levels[i];
         DistHostLevel &DL = H.L[i];
-        const int64_t h = L.head, n_i = L.n_i;
-        DL.h = h;
-        const std::vector<int64_t> tb = (i == 0) ? std::vector<int64_t>() : split_tiles(tile_costs(L, b), G);
-        auto tile_owner = [&](int64_t q) -> int {
-            if (i == 0) return owner(q);
-            return (int)(std::upper_bound(tb.begin() + 1, tb.end() - 1, q / b) - (tb.begin() + 1));
-        };
-        const int64_t qa = (i == 0) ? std::min(lo, n_i) : std::min<int64_t>(n_i, tb[me] * b);
-        const int64_t qb = (i == 0) ? std::min(hi, n_i) : std::min<int64_t>(n_i, tb[me + 1] * b);
-        const int64_t ha = std::max(h, qa);
+        DL.h = L.head;
+        if (i == 0) continue;
+        tbs[i] = split_tiles(tile_costs(L, b), G);
+        int64_t qa, qb;
+        range(i, me, qa, qb);
+        const int64_t h = L.head, ha = std::max(h, qa);
+        DL.recv_cnt.assign(G, 0);
+        DL.out_cnt.assign(G, 0);
+        for (int64_t q = ha; q < qb; ++q) {
+            const int home = owner(pos0[L.perm[q]]);
+            DL.recv_cnt[home]++;
+            if (L.row_ptr[q + 1] > L.row_ptr[q]) DL.out_cnt[home]++;
+        }
+        sl[i].assign(G, {});
+        il[i].assign(G, {});
+        for (int64_t q = h; q < L.n_i; ++q) {
+            const int64_t P0 = pos0[L.perm[q]];
+            if (owner(P0) != me) continue;
+            const int t = tile_owner(i, q);
+            sl[i][t].push_back((int32_t)(P0 - lo));
+            if (L.row_ptr[q + 1] > L.row_ptr[q]) il[i][t].push_back((int32_t)(P0 - lo));
+        }
+        DL.send_cnt.assign(G, 0);
+        DL.in_cnt.assign(G, 0);
+        for (int g = 0; g < G; ++g) {
+            DL.send_cnt[g] = (int64_t)sl[i][g].size();
+            DL.in_cnt[g] = (int64_t)il[i][g].size();
+        }
+    }
+    // ---- peer-major buffer layout: HB / OB = halo / staging offset of (home g, level i)
+    std::vector<std::vector<int64_t>> HB(G, std::vector<int64_t>(nl, 0)), OB(G, std::vector<int64_t>(nl, 0));
+    H.send_peer.assign(G, 0);
+    H.recv_peer.assign(G, 0);
+    H.out_peer.assign(G, 0);
+    H.in_peer.assign(G, 0);
+    int64_t hb = 0, ob = 0;
+    for (int g = 0; g < G; ++g) {
+        if (g == me) { H.halo_self_off = hb; H.out_self_off = ob; }
+        for (int i = 1; i < nl; ++i) {
+            const DistHostLevel &DL = H.L[i];
+            HB[g][i] = hb;
+            OB[g][i] = ob;
+            hb += DL.recv_cnt[g];
+            ob += DL.out_cnt[g];
+            H.send_peer[g] += DL.send_cnt[g];
+            H.recv_peer[g] += DL.recv_cnt[g];
+            H.out_peer[g] += DL.out_cnt[g];
+            H.in_peer[g] += DL.in_cnt[g];
+            auto &s = (g == me) ? H.send_idx_self : H.send_idx_peers;
+            s.insert(s.end(), sl[i][g].begin(), sl[i][g].end());
+            auto &r = (g == me) ? H.in_rows_self : H.in_rows_peers;
+            r.insert(r.end(), il[i][g].begin(), il[i][g].end());
+        }
+    }
+    H.halo_rows = hb;
+    H.out_rows = ob;
 
-        // ---- forward exchange: halo slots of the vertices of my tiles, grouped by home rank
-        std::vector<int32_t> halo_slot;
+    // ---- pass 2: heads, zero rows and descriptor layout of my tiles, per level
+    for (int i = 0; i < nl; ++i) {
+        const HostLevel &L = D.levels[i];
+        DistHostLevel &DL = H.L[i];
+        const int64_t h = L.head;
+        int64_t qa, qb;
+        range(i, me, qa, qb);
+        const int64_t ha = std::max(h, qa);
+        std::vector<int32_t> halo_slot, out_slot;
         if (i > 0) {
-            DL.recv_cnt.assign(G, 0);
-            for (int64_t q = ha; q < qb; ++q) DL.recv_cnt[owner(pos0[L.perm[q]])]++;
-            std::vector<int64_t> cur(G, 0);
-            for (int g = 1; g < G; ++g) cur[g] = cur[g - 1] + DL.recv_cnt[g - 1];
+            std::vector<int64_t> hcur(G), ocur(G);
+            for (int g = 0; g < G; ++g) { hcur[g] = HB[g][i]; ocur[g] = OB[g][i]; }
             halo_slot.resize(std::max<int64_t>(0, qb - ha));
-            for (int64_t q = ha; q < qb; ++q) halo_slot[q - ha] = (int32_t)(cur[owner(pos0[L.perm[q]])]++);
-            // what I send: rows I own that other ranks' tiles need, in their slot order
-            std::vector<std::vector<int32_t>> sl(G);
-            for (int64_t q = h; q < n_i; ++q) {
-                const int64_t P0 = pos0[L.perm[q]];
-                if (owner(P0) == me) sl[tile_owner(q)].push_back((int32_t)(P0 - lo));
-            }
-            DL.send_cnt.assign(G, 0);
-            for (int g = 0; g < G; ++g) {
-                DL.send_cnt[g] = (int64_t)sl[g].size();
-                DL.send_idx.insert(DL.send_idx.end(), sl[g].begin(), sl[g].end());
-            }
-        }
-        // ---- reverse exchange: staging slots of my level>=1 body rows, grouped by home rank
-        std::vector<int32_t> out_slot;
-        if (i > 0) {
-            DL.out_cnt.assign(G, 0);
-            for (int64_t p = ha; p < qb; ++p)
-                if (L.row_ptr[p + 1] > L.row_ptr[p]) DL.out_cnt[owner(pos0[L.perm[p]])]++;
-            std::vector<int64_t> cur(G, 0);
-            for (int g = 1; g < G; ++g) cur[g] = cur[g - 1] + DL.out_cnt[g - 1];
             out_slot.assign(std::max<int64_t>(0, qb - ha), -1);
-            for (int64_t p = ha; p < qb; ++p)
-                if (L.row_ptr[p + 1] > L.row_ptr[p]) out_slot[p - ha] = (int32_t)(cur[owner(pos0[L.perm[p]])]++);
-            // what I receive: rows of all ranks' tiles whose home is me, by source rank, in p order
-            std::vector<std::vector<int32_t>> il(G);
-            for (int64_t p = h; p < n_i; ++p) {
-                if (L.row_ptr[p + 1] == L.row_ptr[p]) continue;
-                const int64_t P0 = pos0[L.perm[p]];
-                if (owner(P0) == me) il[tile_owner(p)].push_back((int32_t)(P0 - lo));
-            }
-            DL.in_cnt.assign(G, 0);
-            for (int g = 0; g < G; ++g) {
-                DL.in_cnt[g] = (int64_t)il[g].size();
-                DL.in_rows.insert(DL.in_rows.end(), il[g].begin(), il[g].end());
+            for (int64_t q = ha; q < qb; ++q) {
+                const int home = owner(pos0[L.perm[q]]);
+                halo_slot[q - ha] = (int32_t)(hcur[home]++);
+                if (L.row_ptr[q + 1] > L.row_ptr[q]) out_slot[q - ha] = (int32_t)(ocur[home]++);
             }
         }
-        // ---- heads whose home is me
         for (int64_t j = 0; j < h; ++j) {
             const int64_t P0 = pos0[L.perm[j]];
             if (owner(P0) == me) { DL.head_j.push_back((int32_t)j); DL.head_row.push_back((int32_t)(P0 - lo)); }
         }
-        // ---- level 0: entry-less rows of my home range (incl. A-isolated vertices) start at zero
-        if (i == 0)
+        if (i == 0)  // level 0: entry-less body rows of my home range (incl. A-isolated vertices)
             for (int64_t p = std::max(lo, h); p < hi; ++p)
                 if (L.row_ptr[p + 1] == L.row_ptr[p]) DL.zero_rows.push_back((int32_t)(p - lo));
-        // ---- descriptor layout of my tiles, window-ordered
         auto colmap = [&](int32_t q) -> int32_t {
             if (q < h) return (int32_t)(kFlag | (uint32_t)q);
             return (i == 0) ? (int32_t)(q - lo) : halo_slot[q - ha];
@@ -263,11 +331,6 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     return ARROW_OK;
 }
 
-static void offsets(const std::vector<int64_t> &cnt, std::vector<int64_t> &off) {
-    off.assign(cnt.size() + 1, 0);
-    for (size_t g = 0; g < cnt.size(); ++g) off[g + 1] = off[g] + cnt[g];
-}
-
 arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
                         int32_t head_chunk) {
     DistHost H;
@@ -280,57 +343,94 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     S->me = H.me;
     S->lo = H.lo;
     S->hi = H.hi;
+    S->nl = (int)H.L.size();
     if (const char *e = std::getenv("ARROW_SEG_BS")) S->bseg = std::atoi(e);
-    const int nl = (int)H.L.size();
+    if (const char *e = std::getenv("ARROW_DIST_RESERVE_SMS")) S->reserve_sms = std::atoi(e);
+    const int nl = S->nl, G = S->G, me = S->me;
+    for (int i = 0; i < nl; ++i) {
+        S->h.push_back(H.L[i].h);
+        S->d0_off.push_back(S->d0_rows);
+        S->d0_rows += H.L[i].h;
+    }
+    S->send_peer = H.send_peer;
+    S->recv_peer = H.recv_peer;
+    S->out_peer = H.out_peer;
+    S->in_peer = H.in_peer;
+    for (int g = 0; g < G; ++g)
+        if (g != me) { S->fwd_rows += H.recv_peer[g]; S->rev_rows += H.out_peer[g]; }
+    // workspace rows: [D0 | C0 | halo | send | staging | recv]
+    const int64_t n_send = (int64_t)H.send_idx_peers.size(), n_in = (int64_t)H.in_rows_peers.size();
+    S->o_d0 = 0;
+    S->o_c0 = S->d0_rows;
+    S->o_halo = 2 * S->d0_rows;
+    S->o_send = S->o_halo + H.halo_rows;
+    S->o_out = S->o_send + n_send;
+    S->o_in = S->o_out + H.out_rows;
+    S->ws_rows = S->o_in + n_in;
+    if (S->ws_rows >= ((int64_t)1 << 31)) return set_error(ARROW_E_UNSUPPORTED, "distributed workspace exceeds 2^31 rows");
+
+    // pre-exchange row mover: D0 (owned heads from X, the rest zero), C0 = 0, pack for peers and self
+    std::vector<int32_t> pre_src, pre_dst, zero = H.L.empty() ? std::vector<int32_t>() : H.L[0].zero_rows;
+    for (int i = 0; i < nl; ++i) {
+        std::vector<int32_t> own(S->h[i], -1);
+        for (size_t m = 0; m < H.L[i].head_j.size(); ++m) own[H.L[i].head_j[m]] = H.L[i].head_row[m];
+        for (int64_t j = 0; j < S->h[i]; ++j) { pre_src.push_back(own[j]); pre_dst.push_back((int32_t)(S->o_d0 + S->d0_off[i] + j)); }
+    }
+    for (int64_t r = 0; r < S->d0_rows; ++r) { pre_src.push_back(-1); pre_dst.push_back((int32_t)(S->o_c0 + r)); }
+    for (int64_t m = 0; m < n_send; ++m) { pre_src.push_back(H.send_idx_peers[m]); pre_dst.push_back((int32_t)(S->o_send + m)); }
+    for (size_t m = 0; m < H.send_idx_self.size(); ++m) {
+        pre_src.push_back(H.send_idx_self[m]);
+        pre_dst.push_back((int32_t)(S->o_halo + H.halo_self_off + (int64_t)m));
+    }
+    // level-0 heads owned here: Y starts at zero, every level adds its head partial afterwards
+    if (nl > 0) zero.insert(zero.end(), H.L[0].head_row.begin(), H.L[0].head_row.end());
+    // gather-adds: own staging rows (before the reverse exchange completes), then received rows and
+    // the head partials of every level (after)
+    std::vector<std::pair<int32_t, int32_t>> cself, cpost;
+    for (size_t m = 0; m < H.in_rows_self.size(); ++m)
+        cself.emplace_back(H.in_rows_self[m], (int32_t)(S->o_out + H.out_self_off + (int64_t)m));
+    for (int64_t m = 0; m < n_in; ++m) cpost.emplace_back(H.in_rows_peers[m], (int32_t)(S->o_in + m));
+    for (int i = 0; i < nl; ++i)
+        for (size_t m = 0; m < H.L[i].head_j.size(); ++m)
+            cpost.emplace_back(H.L[i].head_row[m], (int32_t)(S->o_c0 + S->d0_off[i] + H.L[i].head_j[m]));
+    std::vector<int32_t> sp, ss, sd, pp, ps, pd;
+    build_csr(cself, sp, ss, sd);
+    build_csr(cpost, pp, ps, pd);
+
     bool ok = true;
-    S->L.resize(nl);
     for (int i = 0; i < nl; ++i) {
         DistHostLevel &HL = H.L[i];
-        DistLevel &DL = S->L[i];
-        DL.h = HL.h;
-        DL.recv_cnt = HL.recv_cnt;
-        DL.send_cnt = HL.send_cnt;
-        DL.out_cnt = HL.out_cnt;
-        DL.in_cnt = HL.in_cnt;
-        if (i > 0) {
-            offsets(DL.recv_cnt, DL.recv_off);
-            offsets(DL.send_cnt, DL.send_off);
-            offsets(DL.out_cnt, DL.out_off);
-            offsets(DL.in_cnt, DL.in_off);
-            DL.halo_rows = DL.recv_off.back();
-            DL.send_rows = DL.send_off.back();
-            DL.out_rows = DL.out_off.back();
-            DL.in_rows_n = DL.in_off.back();
-        }
-        DL.send_idx = upload(S, HL.send_idx, ok);
-        DL.in_rows = upload(S, HL.in_rows, ok);
-        DL.nhead_own = (int64_t)HL.head_j.size();
-        DL.head_j = upload(S, HL.head_j, ok);
-        DL.head_row = upload(S, HL.head_row, ok);
-        DL.nzero = (int64_t)HL.zero_rows.size();
-        DL.zero_rows = upload(S, HL.zero_rows, ok);
-        DL.seg.nseg = (int64_t)HL.seg_out.size();
-        DL.seg.mode = 0;  // every output row is written exactly once (local Y at level 0, staging otherwise)
-        DL.seg.seg_out = upload(S, HL.seg_out, ok);
-        DL.seg.seg_end = reinterpret_cast<uint32_t *>(upload(S, HL.seg_end, ok));
-        DL.seg.ent_col = upload(S, HL.ent_col, ok);
-        DL.seg.ent_val = upload(S, HL.ent_val, ok);
+        SegLevel sg;
+        sg.nseg = (int64_t)HL.seg_out.size();
+        sg.mode = 0;  // every output row is written once: local Y (level 0) or the staging buffer
+        sg.seg_out = upload(S, HL.seg_out, ok);
+        sg.seg_end = reinterpret_cast<uint32_t *>(upload(S, HL.seg_end, ok));
+        sg.ent_col = upload(S, HL.ent_col, ok);
+        sg.ent_val = upload(S, HL.ent_val.data(), HL.ent_val.size(), ok);
+        S->seg.push_back(sg);
     }
+    S->n_pre = (int64_t)pre_src.size();
+    S->pre_src = upload(S, pre_src, ok);
+    S->pre_dst = upload(S, pre_dst, ok);
+    S->n_zero = (int64_t)zero.size();
+    S->zero_rows = upload(S, zero, ok);
+    S->n_self = (int64_t)sd.size();
+    S->self_ptr = upload(S, sp, ok);
+    S->self_src = upload(S, ss, ok);
+    S->self_dst = upload(S, sd, ok);
+    S->n_post = (int64_t)pd.size();
+    S->post_ptr = upload(S, pp, ok);
+    S->post_src = upload(S, ps, ok);
+    S->post_dst = upload(S, pd, ok);
     if (!ok) return set_error(ARROW_E_CUDA, "cudaMalloc/cudaMemcpy of the distributed layout failed");
-    // workspace row offsets: [D0 | C0 | halo | send | out | in]
-    int64_t r = 0;
-    for (auto &DL : S->L) { DL.o_d0 = r; r += DL.h; }
-    S->d0_rows = r;
-    for (auto &DL : S->L) { DL.o_c0 = r; r += DL.h; }
-    S->c0_rows = r - S->d0_rows;
-    for (auto &DL : S->L) { DL.o_halo = r; r += DL.halo_rows; }
-    for (auto &DL : S->L) { DL.o_send = r; r += DL.send_rows; }
-    for (auto &DL : S->L) { DL.o_out = r; r += DL.out_rows; }
-    for (auto &DL : S->L) { DL.o_in = r; r += DL.in_rows_n; }
-    S->ws_rows = r;
     if (cudaMalloc(&S->counters, (nl + 1) * sizeof(unsigned)) != cudaSuccess)
         return set_error(ARROW_E_CUDA, "cudaMalloc(counters)");
     S->allocs.push_back(S->counters);
+    if (cudaStreamCreateWithFlags(&S->cs, cudaStreamNonBlocking) != cudaSuccess)
+        return set_error(ARROW_E_CUDA, "cudaStreamCreate(comm stream)");
+    for (auto &e : S->ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return set_error(ARROW_E_CUDA, "cudaEventCreate");
     P->local_begin = S->lo;
     P->local_end = S->hi;
     return ARROW_OK;
@@ -357,13 +457,14 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
     const size_t es = P->esize();
     const ncclDataType_t nt = dt ? ncclDouble : ncclFloat;
-    const int G = S->G, me = S->me, nl = (int)S->L.size();
+    const int G = S->G, me = S->me, nl = S->nl;
     if (nl == 0) {
-        DCUDA(cudaMemsetAsync(Y, 0, (size_t)(S->hi - S->lo) * k * es, st));
+        if (S->hi > S->lo) DCUDA(cudaMemsetAsync(Y, 0, (size_t)(S->hi - S->lo) * k * es, st));
         return ARROW_OK;
     }
     if (k > S->ws_k) {
         DCUDA(cudaStreamSynchronize(st));
+        DCUDA(cudaStreamSynchronize(S->cs));
         if (S->ws) cudaFree(S->ws);
         S->ws = nullptr;
         S->ws_k = 0;
@@ -372,120 +473,112 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     }
     char *ws = reinterpret_cast<char *>(S->ws);
     auto row = [&](int64_t r) { return ws + (size_t)r * k * es; };
-    const char *Xc = reinterpret_cast<const char *>(X);
-    char *Yc = reinterpret_cast<char *>(Y);
-    // profiling: three intervals (pre-exchange, compute, post-exchange), each with its own event pair
-    cudaEvent_t pe[6] = {};
-    auto mark = [&](int i) {
-        if (!P->profiling) return;
-        cudaEventCreate(&pe[i]);
-        cudaEventRecord(pe[i], st);
-    };
-    mark(0);
+    const int sms = std::max(1, P->num_sms - (G > 1 ? S->reserve_sms : 0));
+    // timing marks (profiling counters and ARROW_DIST_TRACE), each interval with its own events
     static const bool trace = std::getenv("ARROW_DIST_TRACE") != nullptr;
+    const bool timed = P->profiling || trace;
     std::vector<cudaEvent_t> tev;
-    auto tmark = [&]() {
-        if (!trace) return;
+    auto mark = [&](cudaStream_t s) {
+        if (!timed) return -1;
         cudaEvent_t e;
         cudaEventCreate(&e);
-        cudaEventRecord(e, st);
+        cudaEventRecord(e, s);
         tev.push_back(e);
+        return (int)tev.size() - 1;
     };
-    tmark();
-    // 1. D0 (owners fill their head rows), C0 = 0, pack the forward rows
+
+    // 1. (S) D0 / C0 / packing, zero rows
+    const int m0 = mark(st);
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
-    DCUDA(cudaMemsetAsync(row(0), 0, (size_t)(S->d0_rows + S->c0_rows) * k * es, st));
-    for (auto &DL : S->L) {
-        DK(launch_rows(dt, X, DL.head_row, DL.head_j, DL.nhead_own, k, 0, row(DL.o_d0), st));
-        if (DL.send_rows) DK(launch_rows(dt, X, DL.send_idx, nullptr, DL.send_rows, k, 0, row(DL.o_send), st));
-    }
-    tmark();  // after memsets, D0 fill, pack
+    DK(launch_rows(dt, X, S->pre_src, S->pre_dst, S->n_pre, k, 0, ws, st));
+    DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, st));
+    const int m1 = mark(st);
+    DCUDA(cudaEventRecord(S->ev[0], st));
+    // 2. (C) D0 of level 0; forward rows + D0 of the other levels
+    DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
+    const int m2 = mark(S->cs);
+    DNCCL(ncclAllReduce(row(S->o_d0), row(S->o_d0), S->h[0] * k, nt, ncclSum, S->comm, S->cs));
+    DCUDA(cudaEventRecord(S->ev[1], S->cs));
     DNCCL(ncclGroupStart());
-    for (auto &DL : S->L) {
-        if (DL.recv_cnt.empty()) continue;
-        for (int g = 0; g < G; ++g) {
-            if (g == me) continue;
-            if (DL.send_cnt[g]) DNCCL(ncclSend(row(DL.o_send + DL.send_off[g]), DL.send_cnt[g] * k, nt, g, S->comm, st));
-            if (DL.recv_cnt[g]) DNCCL(ncclRecv(row(DL.o_halo + DL.recv_off[g]), DL.recv_cnt[g] * k, nt, g, S->comm, st));
-        }
+    int64_t so = 0, ro = 0;
+    for (int g = 0; g < G; ++g) {
+        if (g == me) { ro += S->recv_peer[g]; continue; }
+        if (S->send_peer[g]) DNCCL(ncclSend(row(S->o_send + so), S->send_peer[g] * k, nt, g, S->comm, S->cs));
+        if (S->recv_peer[g]) DNCCL(ncclRecv(row(S->o_halo + ro), S->recv_peer[g] * k, nt, g, S->comm, S->cs));
+        so += S->send_peer[g];
+        ro += S->recv_peer[g];
     }
-    DNCCL(ncclAllReduce(row(0), row(0), S->d0_rows * k, nt, ncclSum, S->comm, st));
+    if (S->d0_rows > S->h[0])
+        DNCCL(ncclAllReduce(row(S->o_d0 + S->h[0]), row(S->o_d0 + S->h[0]), (S->d0_rows - S->h[0]) * k, nt, ncclSum,
+                            S->comm, S->cs));
     DNCCL(ncclGroupEnd());
-    tmark();  // after forward exchange + D0 all-reduce
-    for (auto &DL : S->L)
-        if (!DL.recv_cnt.empty() && DL.send_cnt[me])
-            DCUDA(cudaMemcpyAsync(row(DL.o_halo + DL.recv_off[me]), row(DL.o_send + DL.send_off[me]),
-                                  (size_t)DL.send_cnt[me] * k * es, cudaMemcpyDeviceToDevice, st));
-    tmark();  // after self copies
-    mark(1);
-    mark(2);
-
-    // 2. local compute per level
-    for (int i = 0; i < nl; ++i) {
-        DistLevel &DL = S->L[i];
-        if (i == 0 && DL.nzero) DK(launch_zero_rows(dt, DL.zero_rows, DL.nzero, k, Y, st));
-        const void *src = (i == 0) ? X : (const void *)row(DL.o_halo);
-        void *dst = (i == 0) ? Y : (void *)row(DL.o_out);
-        DK(launch_seg(dt, 1, DL.seg, src, row(DL.o_d0), dst, row(DL.o_c0), k, P->num_sms, S->counters + i, S->bseg, st));
-    }
-    mark(3);
-    mark(4);
-    tmark();  // after compute
-
-    // 3. reverse exchange + head reduction
+    const int m3 = mark(S->cs);
+    DCUDA(cudaEventRecord(S->ev[2], S->cs));
+    // 3. (S) level 0 overlaps the forward exchange; levels >= 1 after it
+    DCUDA(cudaStreamWaitEvent(st, S->ev[1], 0));
+    const int m4 = mark(st);
+    DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(S->o_c0), k, sms, S->counters, S->bseg, st));
+    const int m5 = mark(st);
+    DCUDA(cudaStreamWaitEvent(st, S->ev[2], 0));
+    const int m6 = mark(st);
+    for (int i = 1; i < nl; ++i)
+        DK(launch_seg(dt, 1, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), row(S->o_out),
+                      row(S->o_c0 + S->d0_off[i]), k, sms, S->counters + i, S->bseg, st));
+    const int m7 = mark(st), m7b = mark(st);
+    DCUDA(cudaEventRecord(S->ev[3], st));
+    // 4. (C) staging rows go home, head partials are reduced
+    DCUDA(cudaStreamWaitEvent(S->cs, S->ev[3], 0));
+    const int m8 = mark(S->cs);
     DNCCL(ncclGroupStart());
-    for (auto &DL : S->L) {
-        if (DL.out_cnt.empty()) continue;
-        for (int g = 0; g < G; ++g) {
-            if (g == me) continue;
-            if (DL.out_cnt[g]) DNCCL(ncclSend(row(DL.o_out + DL.out_off[g]), DL.out_cnt[g] * k, nt, g, S->comm, st));
-            if (DL.in_cnt[g]) DNCCL(ncclRecv(row(DL.o_in + DL.in_off[g]), DL.in_cnt[g] * k, nt, g, S->comm, st));
-        }
+    so = 0;
+    ro = 0;
+    for (int g = 0; g < G; ++g) {
+        if (g == me) { so += S->out_peer[g]; continue; }
+        if (S->out_peer[g]) DNCCL(ncclSend(row(S->o_out + so), S->out_peer[g] * k, nt, g, S->comm, S->cs));
+        if (S->in_peer[g]) DNCCL(ncclRecv(row(S->o_in + ro), S->in_peer[g] * k, nt, g, S->comm, S->cs));
+        so += S->out_peer[g];
+        ro += S->in_peer[g];
     }
-    DNCCL(ncclAllReduce(row(S->d0_rows), row(S->d0_rows), S->c0_rows * k, nt, ncclSum, S->comm, st));
+    DNCCL(ncclAllReduce(row(S->o_c0), row(S->o_c0), S->d0_rows * k, nt, ncclSum, S->comm, S->cs));
     DNCCL(ncclGroupEnd());
-    tmark();  // after reverse exchange + C0 all-reduce
-    for (auto &DL : S->L)
-        if (!DL.out_cnt.empty() && DL.out_cnt[me])
-            DCUDA(cudaMemcpyAsync(row(DL.o_in + DL.in_off[me]), row(DL.o_out + DL.out_off[me]),
-                                  (size_t)DL.out_cnt[me] * k * es, cudaMemcpyDeviceToDevice, st));
-    // 4. Y[level-0 heads] = C0_0 (home rank 0), then every level >= 1 adds its rows and head partials
-    DK(launch_rows(dt, row(S->L[0].o_c0), S->L[0].head_j, S->L[0].head_row, S->L[0].nhead_own, k, 0, Y, st));
-    for (int i = 1; i < nl; ++i) {
-        DistLevel &DL = S->L[i];
-        if (DL.in_rows_n) DK(launch_rows(dt, row(DL.o_in), nullptr, DL.in_rows, DL.in_rows_n, k, 1, Y, st));
-        DK(launch_rows(dt, row(DL.o_c0), DL.head_j, DL.head_row, DL.nhead_own, k, 1, Y, st));
-    }
-    mark(5);
-    tmark();  // after adds
-    if (trace && !tev.empty()) {
-        cudaEventSynchronize(tev.back());
-        std::string line = "[arrow dist rank " + std::to_string(me) + "] phases ms:";
-        for (size_t i = 1; i < tev.size(); ++i) {
+    const int m9 = mark(S->cs);
+    DCUDA(cudaEventRecord(S->ev[4], S->cs));
+    // 5. (S) own staging rows (overlaps the exchange), then received rows and owned head partials
+    DK(launch_gather_add(dt, ws, S->self_ptr, S->self_src, S->self_dst, S->n_self, k, Y, st));
+    const int m10 = mark(st);
+    DCUDA(cudaStreamWaitEvent(st, S->ev[4], 0));
+    const int m11 = mark(st);
+    DK(launch_gather_add(dt, ws, S->post_ptr, S->post_src, S->post_dst, S->n_post, k, Y, st));
+    const int m12 = mark(st);
+    if (trace) {
+        cudaEventSynchronize(tev[m12]);
+        auto el = [&](int a, int b) {
             float ms = 0;
-            cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
-            line += " " + std::to_string(ms);
-        }
-        int64_t fs = 0, fr = 0, rs = 0, rr = 0;
-        for (auto &DL : S->L) {
-            for (int g = 0; g < G && !DL.recv_cnt.empty(); ++g) {
-                if (g == me) continue;
-                fs += DL.send_cnt[g]; fr += DL.recv_cnt[g]; rs += DL.out_cnt[g]; rr += DL.in_cnt[g];
-            }
-        }
-        line += " | rows fwd send " + std::to_string(fs) + " recv " + std::to_string(fr) + ", rev send " +
-                std::to_string(rs) + " recv " + std::to_string(rr) + ", d0/c0 rows " + std::to_string(S->d0_rows);
+            cudaEventElapsedTime(&ms, tev[a], tev[b]);
+            return std::to_string(ms);
+        };
+        std::string line = "[arrow dist rank " + std::to_string(me) + "] ms: pre " + el(m0, m1) + " | fwd " +
+                           el(m2, m3) + " (ends at " + el(m0, m3) + ") | K-A L0 " + el(m4, m5) + " (starts at " +
+                           el(m0, m4) + ") | wait " + el(m5, m6) + " | K-A L>=1 " + el(m6, m7) + " | rev " +
+                           el(m8, m9) + " | self-add " + el(m7, m10) + " | wait " + el(m10, m11) + " | post-add " +
+                           el(m11, m12) + " | total " + el(m0, m12) + " | rows fwd " + std::to_string(S->fwd_rows) +
+                           " rev " + std::to_string(S->rev_rows) + " d0 " + std::to_string(S->d0_rows);
         fprintf(stderr, "%s\n", line.c_str());
-        for (auto e : tev) cudaEventDestroy(e);
     }
     if (P->profiling) {
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, pe[0], pe[1]});
-        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, pe[2], pe[3]});
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, pe[4], pe[5]});
+        // compute: both K-A phases; communication: pre-exchange work and the two exchanges
+        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m0], tev[m1]});
+        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m2], tev[m3]});
+        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, tev[m4], tev[m5]});
+        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, tev[m6], tev[m7]});
+        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m8], tev[m9]});
+        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m7b], tev[m12]});
         P->prof_acc.calls += 1;
+        // the remaining marks are not owned by a ProfRec
+        for (int m : {m10, m11}) cudaEventDestroy(tev[m]);
+    } else {
+        for (auto e : tev) cudaEventDestroy(e);
     }
-    (void)Xc;
-    (void)Yc;
     return ARROW_OK;
 }
 

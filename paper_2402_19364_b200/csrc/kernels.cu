@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(256) k_rows(const T *__restrict__ src, const i
         const int64_t i = t / kv, c = (t - i * kv) * VEC;
         const int64_t si = sidx ? (int64_t)__ldg(sidx + i) : i;
         const int64_t di = didx ? (int64_t)__ldg(didx + i) : i;
-        Frag<T, VEC> a = ld_plain<T, VEC>(src + si * k + c);
+        Frag<T, VEC> a;
+        if (si >= 0) a = ld_plain<T, VEC>(src + si * k + c);
+        else a.zero();  // sidx < 0: the destination row is zeroed
         T *p = dst + di * k + c;
         if (add) {
             Frag<T, VEC> y = ld_plain<T, VEC>(p);
@@ -290,7 +292,45 @@ __global__ void __launch_bounds__(256) k_rows(const T *__restrict__ src, const i
         st_plain<T, VEC>(p, a);
     }
 }
+
+// dst[drow[r]] += sum_{e in [ptr[r], ptr[r+1])} src[sidx[e]], contributions summed in list order
+// (deterministic; every destination row appears once, so rows need no atomics).
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_gather_add(const T *__restrict__ src, const int32_t *__restrict__ ptr,
+                                                    const int32_t *__restrict__ sidx, const int32_t *__restrict__ drow,
+                                                    int64_t n, int64_t k, T *__restrict__ dst) {
+    const int64_t kv = k / VEC, total = n * kv;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / kv, c = (t - r * kv) * VEC;
+        T *p = dst + (int64_t)__ldg(drow + r) * k + c;
+        Frag<T, VEC> a = ld_plain<T, VEC>(p);
+        const int e1 = __ldg(ptr + r + 1);
+        for (int e = __ldg(ptr + r); e < e1; ++e) {
+            const Frag<T, VEC> s = ld_plain<T, VEC>(src + (int64_t)__ldg(sidx + e) * k + c);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) a.v[q] += s.v[q];
+        }
+        st_plain<T, VEC>(p, a);
+    }
+}
 }  // namespace
+
+int launch_gather_add(int dtype, const void *src, const int32_t *ptr, const int32_t *sidx, const int32_t *drow,
+                      int64_t n, int64_t k, void *dst, void *stream) {
+    if (n == 0 || k == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {src, dst});
+    const unsigned g = grid_for(n * (k / vec));
+    if (dtype == 0) {
+        if (vec == 4) k_gather_add<float, 4><<<g, 256, 0, st>>>((const float *)src, ptr, sidx, drow, n, k, (float *)dst);
+        else if (vec == 2) k_gather_add<float, 2><<<g, 256, 0, st>>>((const float *)src, ptr, sidx, drow, n, k, (float *)dst);
+        else k_gather_add<float, 1><<<g, 256, 0, st>>>((const float *)src, ptr, sidx, drow, n, k, (float *)dst);
+    } else {
+        if (vec == 2) k_gather_add<double, 2><<<g, 256, 0, st>>>((const double *)src, ptr, sidx, drow, n, k, (double *)dst);
+        else k_gather_add<double, 1><<<g, 256, 0, st>>>((const double *)src, ptr, sidx, drow, n, k, (double *)dst);
+    }
+    return (int)cudaGetLastError();
+}
 
 int launch_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k, int add,
                 void *dst, void *stream) {
