@@ -70,8 +70,32 @@ struct SegLevel {
     int32_t *ent_col = nullptr;   // [nnz] X row (bit 31: D0 row)
     void *ent_val = nullptr;      // [nnz]
 };
+// Peer (NVLink) addressing of the distributed P2P transport: an encoded row is
+// (rank << kPeerShift | row) into the per-rank base pointers of a PeerPtrs; kParityBit marks a row
+// of the double-buffered head partial C0 (shifted by the current call's parity offset).
+constexpr int kMaxPeers = 8;
+constexpr int kPeerShift = 27;
+constexpr uint32_t kPeerRowMask = (1u << kPeerShift) - 1u;
+constexpr uint32_t kParityBit = 0x40000000u;
+constexpr uint32_t kLocalRmwBit = 0x40000000u;  // K-A (dist 2): out row is a local Y row, read-modify-written
+struct PeerPtrs {
+    void *p[kMaxPeers];
+};
+// dist: 0 single GPU, 1 distributed (head columns from D0, head partials into C0), 2 as 1 with
+// body rows stored through `outs` (encoded rows, levels >= 1 of the P2P transport) or, with
+// kLocalRmwBit, added into Y (rows whose home is this rank)
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream);
+               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs = nullptr);
+// dst row enc(didx[i]) of bases = src[sidx[i]] (sidx < 0: zero); grid of `blocks` (0: sized to n)
+int launch_push_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k,
+                     const PeerPtrs &bases, int blocks, void *stream);
+// Y[drow[r]] += sum of row enc(src[e]) of bases (+ par_shift rows when kParityBit), e in [ptr[r], ptr[r+1])
+int launch_gather_add_peers(int dtype, const PeerPtrs &bases, int64_t par_shift, const int32_t *ptr,
+                            const int32_t *src, const int32_t *drow, int64_t n, int64_t k, void *Y, void *stream);
+// cross-GPU barrier: thread g publishes `epoch` into slot `slot` of rank g's flag array, then waits
+// until every rank has published it into this rank's array (system-scope release/acquire; traps
+// after ~60 s so a lost peer cannot hang the GPU)
+int launch_barrier(const PeerPtrs &flags, const unsigned *mine, int slot, unsigned epoch, int me, int G, void *stream);
 
 struct StreamArgs {
     const uint32_t *keys;

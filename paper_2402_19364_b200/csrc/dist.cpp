@@ -64,6 +64,18 @@ struct DistHost {
     std::vector<int64_t> send_peer, recv_peer, out_peer, in_peer;  // per-peer totals (rows)
     int64_t halo_rows = 0, out_rows = 0;                             // incl. my own chunks
     int64_t halo_self_off = 0, out_self_off = 0;                     // my own chunks' offsets
+    // P2P transport (p2p != 0): workspace of rank t = [D0 | C0 x 2 | halo_t | stage_t]; rows
+    // are encoded (rank << kPeerShift | workspace row)
+    int p2p = 0;
+    int64_t d0_rows = 0;
+    int64_t zero_tail_lo = 0, zero_tail_n = 0;  // local Y rows of the A-isolated tail (written as 0)
+    std::vector<int64_t> halo_all, stage_all;           // per rank
+    std::vector<int32_t> d0push_src, d0push_dst;        // my heads -> every rank's D0
+    std::vector<int32_t> halopush_src, halopush_dst;    // my X rows -> every rank's halo (push kernel)
+    std::vector<int32_t> pack_src, pack_dst;            // my X rows -> my send chunks / my own halo (DMA)
+    std::vector<int64_t> send_row, halo_dst_row;        // per peer: my send chunk, its place in the peer's halo
+    int64_t send_rows = 0;
+    std::vector<std::pair<int32_t, int32_t>> post;      // (local Y row, encoded source row)
 };
 
 struct DistState {
@@ -71,32 +83,60 @@ struct DistState {
     int G = 1, me = 0;
     int64_t lo = 0, hi = 0;
     int nl = 0;
+    int p2p = 0;
     std::vector<int64_t> h, d0_off;  // head rows per level, offset of the level inside D0 / C0
     int64_t d0_rows = 0;
     std::vector<SegLevel> seg;
     std::vector<int64_t> send_peer, recv_peer, out_peer, in_peer;
-    // k-dependent workspace (rows): [D0 | C0 | halo | send | staging | recv]
+    // k-dependent workspace (rows).  NCCL: [D0 | C0 | halo | send | staging | recv];
+    // P2P: [D0 | C0 (call parity 0) | C0 (parity 1) | halo | stage], shared with the peers
     int64_t o_d0 = 0, o_c0 = 0, o_halo = 0, o_send = 0, o_out = 0, o_in = 0, ws_rows = 0;
-    // pre-exchange row mover (src X, dst workspace) and Y rows to zero
-    int32_t *pre_src = nullptr, *pre_dst = nullptr, *zero_rows = nullptr;
-    int64_t n_pre = 0, n_zero = 0;
-    // CSR gather-adds into Y: own staging rows / received rows + head partials (src: workspace rows)
+    // NCCL: pre-exchange row mover (src X, dst workspace)
+    int32_t *pre_src = nullptr, *pre_dst = nullptr;
+    int64_t n_pre = 0;
+    // P2P: pushes of my head rows into every D0 and of my X rows into every halo (encoded rows)
+    int32_t *d0push_src = nullptr, *d0push_dst = nullptr, *halopush_src = nullptr, *halopush_dst = nullptr;
+    int64_t n_d0push = 0, n_halopush = 0;
+    // P2P, DMA halo (default; ARROW_DIST_HALO=push uses the push kernel): pack, then one copy-engine
+    // transfer per peer into its halo
+    int halo_dma = 1;
+    int32_t *pack_src = nullptr, *pack_dst = nullptr;
+    int64_t n_pack = 0;
+    std::vector<int64_t> send_row, halo_dst_row;
+    int32_t *zero_rows = nullptr;  // Y rows no K-A launch writes (+ owned level-0 heads)
+    int64_t n_zero = 0;
+    int64_t zero_tail_lo = 0, zero_tail_n = 0;
+    // CSR gather-adds into Y (NCCL: own staging rows / received rows + head partials; P2P: post only)
     int32_t *self_ptr = nullptr, *self_src = nullptr, *self_dst = nullptr;
     int32_t *post_ptr = nullptr, *post_src = nullptr, *post_dst = nullptr;
     int64_t n_self = 0, n_post = 0;
     void *ws = nullptr;
     int64_t ws_k = 0;
+    PeerPtrs ws_peer{}, flags_peer{};  // P2P: every rank's workspace / flag array (mine included)
+    unsigned *flags = nullptr;
+    unsigned epoch[3] = {0, 0, 0};
+    uint64_t calls = 0;
     std::vector<void *> allocs;
     unsigned *counters = nullptr;
     cudaStream_t cs = nullptr;
     cudaEvent_t ev[5] = {};
-    int bseg = 16, reserve_sms = 16;
+    int bseg = 16, reserve_sms = 16, push_blocks = 0;
     int64_t fwd_rows = 0, rev_rows = 0;  // rows exchanged with peers (trace)
 };
+
+namespace {
+void close_peers(DistState *d, PeerPtrs &pp) {
+    for (int g = 0; g < d->G && g < kMaxPeers; ++g)
+        if (g != d->me && pp.p[g]) cudaIpcCloseMemHandle(pp.p[g]);
+    pp = PeerPtrs{};
+}
+}  // namespace
 
 void dist_free(DistState *d) {
     if (!d) return;
     if (d->cs) cudaStreamSynchronize(d->cs);
+    close_peers(d, d->ws_peer);
+    close_peers(d, d->flags_peer);
     for (void *p : d->allocs) cudaFree(p);
     if (d->ws) cudaFree(d->ws);
     for (auto e : d->ev)
@@ -166,9 +206,10 @@ void build_csr(const std::vector<std::pair<int32_t, int32_t>> &c, std::vector<in
 }  // namespace
 
 arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_t window_rows, int32_t head_chunk,
-                           size_t es, DistHost &H) {
+                           size_t es, int p2p, DistHost &H) {
     if (!D.res_u.empty()) return set_error(ARROW_E_UNSUPPORTED, "distributed mode does not support a residual level");
     if (G < 1 || me < 0 || me >= G) return set_error(ARROW_E_INVALID_ARG, "bad nranks/rank");
+    if (p2p && G > kMaxPeers) return set_error(ARROW_E_UNSUPPORTED, "P2P transport supports at most 8 ranks");
     H.G = G;
     H.me = me;
     const int64_t n = D.n, b = D.b;
@@ -180,7 +221,11 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     if (nl > 0) {
         const HostLevel &L0 = D.levels[0];
         for (int64_t p = 0; p < n; ++p) pos0[L0.perm[p]] = (int32_t)p;
-        const std::vector<int64_t> tb = split_tiles(tile_costs(L0, b), G);
+        // A-isolated rows (positions >= n_0, R8) go to the last rank: one pseudo tile costing a
+        // row write each, so that rank takes correspondingly fewer level-0 tiles
+        std::vector<int64_t> cost = tile_costs(L0, b);
+        cost.push_back(n - L0.n_i);
+        const std::vector<int64_t> tb = split_tiles(cost, G);
         for (int g = 0; g <= G; ++g) los[g] = std::min<int64_t>(L0.n_i, tb[g] * b);
         los[G] = n;
     } else {
@@ -205,6 +250,8 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         return (int)(std::upper_bound(tbs[i].begin() + 1, tbs[i].end() - 1, q / b) - (tbs[i].begin() + 1));
     };
     H.L.resize(nl);
+    // RC / OC[i][t * G + h]: rows (all / with entries) of rank t's level-i tiles whose home is h
+    std::vector<std::vector<int64_t>> RC(nl, std::vector<int64_t>((size_t)G * G, 0)), OC = RC;
     // sl[i][g]: local X rows I own that g's level-i tiles need (g's halo slot order);
     // il[i][g]: local Y rows of g's level-i body rows whose home is me (g's staging order)
     std::vector<std::vector<std::vector<int32_t>>> sl(nl), il(nl);
@@ -228,10 +275,13 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         il[i].assign(G, {});
         for (int64_t q = h; q < L.n_i; ++q) {
             const int64_t P0 = pos0[L.perm[q]];
-            if (owner(P0) != me) continue;
-            const int t = tile_owner(i, q);
+            const int home = owner(P0), t = tile_owner(i, q);
+            const bool has = L.row_ptr[q + 1] > L.row_ptr[q];
+            RC[i][(size_t)t * G + home]++;
+            if (has) OC[i][(size_t)t * G + home]++;
+            if (home != me) continue;
             sl[i][t].push_back((int32_t)(P0 - lo));
-            if (L.row_ptr[q + 1] > L.row_ptr[q]) il[i][t].push_back((int32_t)(P0 - lo));
+            if (has) il[i][t].push_back((int32_t)(P0 - lo));
         }
         DL.send_cnt.assign(G, 0);
         DL.in_cnt.assign(G, 0);
@@ -267,6 +317,58 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     }
     H.halo_rows = hb;
     H.out_rows = ob;
+    // P2P layout of every rank: HBt[t][h][i] = halo offset (home-major), SBt[t][s][i] = staging
+    // offset (source-major) inside rank t's buffers
+    H.p2p = p2p;
+    for (int i = 0; i < nl; ++i) H.d0_rows += D.levels[i].head;
+    std::vector<std::vector<std::vector<int64_t>>> HBt, SBt;
+    if (p2p) {
+        HBt.assign(G, std::vector<std::vector<int64_t>>(G, std::vector<int64_t>(nl, 0)));
+        SBt = HBt;
+        H.halo_all.assign(G, 0);
+        H.stage_all.assign(G, 0);
+        for (int t = 0; t < G; ++t)
+            for (int g = 0; g < G; ++g)
+                for (int i = 1; i < nl; ++i) {
+                    HBt[t][g][i] = H.halo_all[t];
+                    H.halo_all[t] += RC[i][(size_t)t * G + g];
+                    SBt[t][g][i] = H.stage_all[t];
+                    if (g != t) H.stage_all[t] += OC[i][(size_t)g * G + t];  // own rows: RMW into Y
+                }
+        const int64_t o_halo = 3 * H.d0_rows;
+        for (int t = 0; t < G; ++t) {
+            if (o_halo + H.halo_all[t] + H.stage_all[t] > (int64_t)kPeerRowMask)
+                return set_error(ARROW_E_UNSUPPORTED, "P2P workspace exceeds 2^27 rows");
+            for (int i = 1; i < nl; ++i)
+                for (size_t m = 0; m < sl[i][t].size(); ++m) {
+                    H.halopush_src.push_back(sl[i][t][m]);
+                    H.halopush_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)(o_halo + HBt[t][me][i] + (int64_t)m)));
+                }
+        }
+        const int64_t o_stage = o_halo + H.halo_all[me];
+        // DMA variant: pack every peer's rows contiguously ([D0 | C0 x 2 | halo | stage | send]),
+        // the rows of my own tiles straight into my halo; the copy engines move the chunks
+        const int64_t o_send = o_stage + H.stage_all[me];
+        H.send_row.assign(G, 0);
+        H.halo_dst_row.assign(G, 0);
+        for (int t = 0; t < G; ++t) {
+            H.send_row[t] = o_send + H.send_rows;
+            H.halo_dst_row[t] = o_halo + (nl > 1 ? HBt[t][me][1] : 0);
+            int64_t m2 = 0;
+            for (int i = 1; i < nl; ++i)
+                for (size_t m = 0; m < sl[i][t].size(); ++m, ++m2) {
+                    H.pack_src.push_back(sl[i][t][m]);
+                    H.pack_dst.push_back((int32_t)(t == me ? o_halo + HBt[me][me][i] + (int64_t)m : o_send + H.send_rows + m2));
+                }
+            if (t != me) H.send_rows += m2;
+        }
+        if (o_send + H.send_rows > (int64_t)kPeerRowMask) return set_error(ARROW_E_UNSUPPORTED, "P2P workspace exceeds 2^27 rows");
+        if (hi - lo > (int64_t)kPeerRowMask) return set_error(ARROW_E_UNSUPPORTED, "P2P transport: more than 2^27 rows per rank");
+        for (int s = 0; s < G; ++s)
+            for (int i = 1; s != me && i < nl; ++i)
+                for (size_t m = 0; m < il[i][s].size(); ++m)
+                    H.post.emplace_back(il[i][s][m], (int32_t)(((uint32_t)me << kPeerShift) | (uint32_t)(o_stage + SBt[me][s][i] + (int64_t)m)));
+    }
 
     // ---- pass 2: heads, zero rows and descriptor layout of my tiles, per level
     for (int i = 0; i < nl; ++i) {
@@ -279,22 +381,44 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         std::vector<int32_t> halo_slot, out_slot;
         if (i > 0) {
             std::vector<int64_t> hcur(G), ocur(G);
-            for (int g = 0; g < G; ++g) { hcur[g] = HB[g][i]; ocur[g] = OB[g][i]; }
+            for (int g = 0; g < G; ++g) {
+                hcur[g] = HB[g][i];
+                // P2P: staging rows are stored straight into the home rank's buffer
+                ocur[g] = p2p ? 3 * H.d0_rows + H.halo_all[g] + SBt[g][me][i] : OB[g][i];
+            }
             halo_slot.resize(std::max<int64_t>(0, qb - ha));
             out_slot.assign(std::max<int64_t>(0, qb - ha), -1);
             for (int64_t q = ha; q < qb; ++q) {
                 const int home = owner(pos0[L.perm[q]]);
                 halo_slot[q - ha] = (int32_t)(hcur[home]++);
-                if (L.row_ptr[q + 1] > L.row_ptr[q]) out_slot[q - ha] = (int32_t)(ocur[home]++);
+                if (L.row_ptr[q + 1] == L.row_ptr[q]) continue;
+                if (p2p && home == me)  // P2P: my own rows are read-modify-written into Y directly
+                    out_slot[q - ha] = (int32_t)(kLocalRmwBit | (uint32_t)(pos0[L.perm[q]] - lo));
+                else
+                    out_slot[q - ha] = (int32_t)((p2p ? ((uint32_t)home << kPeerShift) : 0u) | (uint32_t)(ocur[home]++));
             }
         }
+        int64_t d0_off = 0;
+        for (int i2 = 0; i2 < i; ++i2) d0_off += D.levels[i2].head;
         for (int64_t j = 0; j < h; ++j) {
             const int64_t P0 = pos0[L.perm[j]];
-            if (owner(P0) == me) { DL.head_j.push_back((int32_t)j); DL.head_row.push_back((int32_t)(P0 - lo)); }
+            if (owner(P0) != me) continue;
+            DL.head_j.push_back((int32_t)j);
+            DL.head_row.push_back((int32_t)(P0 - lo));
+            if (p2p)
+                for (int t = 0; t < G; ++t) {
+                    H.d0push_src.push_back((int32_t)(P0 - lo));
+                    H.d0push_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)(d0_off + j)));
+                    H.post.emplace_back((int32_t)(P0 - lo), (int32_t)(((uint32_t)t << kPeerShift) | kParityBit |
+                                                                       (uint32_t)(H.d0_rows + d0_off + j)));
+                }
         }
-        if (i == 0)  // level 0: entry-less body rows of my home range (incl. A-isolated vertices)
-            for (int64_t p = std::max(lo, h); p < hi; ++p)
+        if (i == 0) {  // level 0: entry-less body rows of my home range; the A-isolated tail is a range
+            for (int64_t p = std::max(lo, h); p < std::min(hi, L.n_i); ++p)
                 if (L.row_ptr[p + 1] == L.row_ptr[p]) DL.zero_rows.push_back((int32_t)(p - lo));
+            H.zero_tail_lo = std::max(lo, L.n_i) - lo;
+            H.zero_tail_n = std::max<int64_t>(0, hi - std::max(lo, L.n_i));
+        }
         auto colmap = [&](int32_t q) -> int32_t {
             if (q < h) return (int32_t)(kFlag | (uint32_t)q);
             return (i == 0) ? (int32_t)(q - lo) : halo_slot[q - ha];
@@ -331,111 +455,6 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     return ARROW_OK;
 }
 
-arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
-                        int32_t head_chunk) {
-    DistHost H;
-    arrow_status st = dist_schedule(D, comm->nranks, comm->rank, window_rows, head_chunk, P->esize(), H);
-    if (st != ARROW_OK) return st;
-    auto *S = new DistState();
-    P->dist = S;
-    S->comm = (ncclComm_t)comm->comm;
-    S->G = H.G;
-    S->me = H.me;
-    S->lo = H.lo;
-    S->hi = H.hi;
-    S->nl = (int)H.L.size();
-    if (const char *e = std::getenv("ARROW_SEG_BS")) S->bseg = std::atoi(e);
-    if (const char *e = std::getenv("ARROW_DIST_RESERVE_SMS")) S->reserve_sms = std::atoi(e);
-    const int nl = S->nl, G = S->G, me = S->me;
-    for (int i = 0; i < nl; ++i) {
-        S->h.push_back(H.L[i].h);
-        S->d0_off.push_back(S->d0_rows);
-        S->d0_rows += H.L[i].h;
-    }
-    S->send_peer = H.send_peer;
-    S->recv_peer = H.recv_peer;
-    S->out_peer = H.out_peer;
-    S->in_peer = H.in_peer;
-    for (int g = 0; g < G; ++g)
-        if (g != me) { S->fwd_rows += H.recv_peer[g]; S->rev_rows += H.out_peer[g]; }
-    // workspace rows: [D0 | C0 | halo | send | staging | recv]
-    const int64_t n_send = (int64_t)H.send_idx_peers.size(), n_in = (int64_t)H.in_rows_peers.size();
-    S->o_d0 = 0;
-    S->o_c0 = S->d0_rows;
-    S->o_halo = 2 * S->d0_rows;
-    S->o_send = S->o_halo + H.halo_rows;
-    S->o_out = S->o_send + n_send;
-    S->o_in = S->o_out + H.out_rows;
-    S->ws_rows = S->o_in + n_in;
-    if (S->ws_rows >= ((int64_t)1 << 31)) return set_error(ARROW_E_UNSUPPORTED, "distributed workspace exceeds 2^31 rows");
-
-    // pre-exchange row mover: D0 (owned heads from X, the rest zero), C0 = 0, pack for peers and self
-    std::vector<int32_t> pre_src, pre_dst, zero = H.L.empty() ? std::vector<int32_t>() : H.L[0].zero_rows;
-    for (int i = 0; i < nl; ++i) {
-        std::vector<int32_t> own(S->h[i], -1);
-        for (size_t m = 0; m < H.L[i].head_j.size(); ++m) own[H.L[i].head_j[m]] = H.L[i].head_row[m];
-        for (int64_t j = 0; j < S->h[i]; ++j) { pre_src.push_back(own[j]); pre_dst.push_back((int32_t)(S->o_d0 + S->d0_off[i] + j)); }
-    }
-    for (int64_t r = 0; r < S->d0_rows; ++r) { pre_src.push_back(-1); pre_dst.push_back((int32_t)(S->o_c0 + r)); }
-    for (int64_t m = 0; m < n_send; ++m) { pre_src.push_back(H.send_idx_peers[m]); pre_dst.push_back((int32_t)(S->o_send + m)); }
-    for (size_t m = 0; m < H.send_idx_self.size(); ++m) {
-        pre_src.push_back(H.send_idx_self[m]);
-        pre_dst.push_back((int32_t)(S->o_halo + H.halo_self_off + (int64_t)m));
-    }
-    // level-0 heads owned here: Y starts at zero, every level adds its head partial afterwards
-    if (nl > 0) zero.insert(zero.end(), H.L[0].head_row.begin(), H.L[0].head_row.end());
-    // gather-adds: own staging rows (before the reverse exchange completes), then received rows and
-    // the head partials of every level (after)
-    std::vector<std::pair<int32_t, int32_t>> cself, cpost;
-    for (size_t m = 0; m < H.in_rows_self.size(); ++m)
-        cself.emplace_back(H.in_rows_self[m], (int32_t)(S->o_out + H.out_self_off + (int64_t)m));
-    for (int64_t m = 0; m < n_in; ++m) cpost.emplace_back(H.in_rows_peers[m], (int32_t)(S->o_in + m));
-    for (int i = 0; i < nl; ++i)
-        for (size_t m = 0; m < H.L[i].head_j.size(); ++m)
-            cpost.emplace_back(H.L[i].head_row[m], (int32_t)(S->o_c0 + S->d0_off[i] + H.L[i].head_j[m]));
-    std::vector<int32_t> sp, ss, sd, pp, ps, pd;
-    build_csr(cself, sp, ss, sd);
-    build_csr(cpost, pp, ps, pd);
-
-    bool ok = true;
-    for (int i = 0; i < nl; ++i) {
-        DistHostLevel &HL = H.L[i];
-        SegLevel sg;
-        sg.nseg = (int64_t)HL.seg_out.size();
-        sg.mode = 0;  // every output row is written once: local Y (level 0) or the staging buffer
-        sg.seg_out = upload(S, HL.seg_out, ok);
-        sg.seg_end = reinterpret_cast<uint32_t *>(upload(S, HL.seg_end, ok));
-        sg.ent_col = upload(S, HL.ent_col, ok);
-        sg.ent_val = upload(S, HL.ent_val.data(), HL.ent_val.size(), ok);
-        S->seg.push_back(sg);
-    }
-    S->n_pre = (int64_t)pre_src.size();
-    S->pre_src = upload(S, pre_src, ok);
-    S->pre_dst = upload(S, pre_dst, ok);
-    S->n_zero = (int64_t)zero.size();
-    S->zero_rows = upload(S, zero, ok);
-    S->n_self = (int64_t)sd.size();
-    S->self_ptr = upload(S, sp, ok);
-    S->self_src = upload(S, ss, ok);
-    S->self_dst = upload(S, sd, ok);
-    S->n_post = (int64_t)pd.size();
-    S->post_ptr = upload(S, pp, ok);
-    S->post_src = upload(S, ps, ok);
-    S->post_dst = upload(S, pd, ok);
-    if (!ok) return set_error(ARROW_E_CUDA, "cudaMalloc/cudaMemcpy of the distributed layout failed");
-    if (cudaMalloc(&S->counters, (nl + 1) * sizeof(unsigned)) != cudaSuccess)
-        return set_error(ARROW_E_CUDA, "cudaMalloc(counters)");
-    S->allocs.push_back(S->counters);
-    if (cudaStreamCreateWithFlags(&S->cs, cudaStreamNonBlocking) != cudaSuccess)
-        return set_error(ARROW_E_CUDA, "cudaStreamCreate(comm stream)");
-    for (auto &e : S->ev)
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
-            return set_error(ARROW_E_CUDA, "cudaEventCreate");
-    P->local_begin = S->lo;
-    P->local_end = S->hi;
-    return ARROW_OK;
-}
-
 #define DCUDA(expr)                                                                                 \
     do {                                                                                            \
         cudaError_t _e = (expr);                                                                    \
@@ -452,6 +471,358 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         if (_e) return set_error(ARROW_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString((cudaError_t)_e)); \
     } while (0)
 
+namespace {
+
+// all ranks: every rank's mapping of `local` (a cudaMalloc base) via CUDA IPC; `ok` = this rank
+// could open every peer's handle (callers agree collectively before using the mappings)
+arrow_status share_ptr(DistState *S, void *local, PeerPtrs &out, bool &ok) {
+    out = PeerPtrs{};
+    ok = true;
+    cudaIpcMemHandle_t mine;
+    std::memset(&mine, 0, sizeof(mine));
+    if (cudaIpcGetMemHandle(&mine, local) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+    }
+    const size_t hs = sizeof(cudaIpcMemHandle_t);
+    char *dbuf = nullptr;
+    DCUDA(cudaMalloc(&dbuf, hs * S->G));
+    DCUDA(cudaMemcpy(dbuf + hs * S->me, &mine, hs, cudaMemcpyHostToDevice));
+    DNCCL(ncclAllGather(dbuf + hs * S->me, dbuf, hs, ncclUint8, S->comm, S->cs));
+    DCUDA(cudaStreamSynchronize(S->cs));
+    std::vector<cudaIpcMemHandle_t> all(S->G);
+    DCUDA(cudaMemcpy(all.data(), dbuf, hs * S->G, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    for (int g = 0; g < S->G; ++g) {
+        if (g == S->me) { out.p[g] = local; continue; }
+        if (!ok) continue;
+        if (cudaIpcOpenMemHandle(&out.p[g], all[g], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            out.p[g] = nullptr;
+            ok = false;
+        }
+    }
+    return ARROW_OK;
+}
+
+// all ranks: logical AND of `v` over the ranks
+arrow_status all_true(DistState *S, bool &v) {
+    int *d = nullptr;
+    DCUDA(cudaMalloc(&d, sizeof(int)));
+    const int h = v ? 1 : 0;
+    DCUDA(cudaMemcpy(d, &h, sizeof(int), cudaMemcpyHostToDevice));
+    DNCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, S->comm, S->cs));
+    DCUDA(cudaStreamSynchronize(S->cs));
+    int r = 0;
+    DCUDA(cudaMemcpy(&r, d, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    v = r != 0;
+    return ARROW_OK;
+}
+
+}  // namespace
+
+arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
+                        int32_t head_chunk) {
+    auto *S = new DistState();
+    P->dist = S;
+    S->comm = (ncclComm_t)comm->comm;
+    S->G = comm->nranks;
+    S->me = comm->rank;
+    if (cudaStreamCreateWithFlags(&S->cs, cudaStreamNonBlocking) != cudaSuccess)
+        return set_error(ARROW_E_CUDA, "cudaStreamCreate(comm stream)");
+    for (auto &e : S->ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return set_error(ARROW_E_CUDA, "cudaEventCreate");
+    // transport: P2P (peer memory over NVLink, fused with the kernels) unless ARROW_DIST_TRANSPORT=nccl,
+    // a single rank, or some rank cannot map its peers' memory (decided collectively)
+    const char *tr = std::getenv("ARROW_DIST_TRANSPORT");
+    bool p2p = S->G > 1 && S->G <= kMaxPeers && !(tr && std::string(tr) == "nccl");
+    if (p2p) {
+        DCUDA(cudaMalloc(&S->flags, 3 * kMaxPeers * sizeof(unsigned)));
+        DCUDA(cudaMemset(S->flags, 0, 3 * kMaxPeers * sizeof(unsigned)));
+        DCUDA(cudaDeviceSynchronize());
+        bool ok = true;
+        arrow_status st = share_ptr(S, S->flags, S->flags_peer, ok);
+        if (st != ARROW_OK) return st;
+        st = all_true(S, ok);
+        if (st != ARROW_OK) return st;
+        if (!ok) {
+            close_peers(S, S->flags_peer);
+            p2p = false;
+        }
+        if (std::getenv("ARROW_DIST_TRACE"))
+            fprintf(stderr, "[arrow dist rank %d] transport %s\n", S->me, p2p ? "p2p" : "nccl (peer mapping failed)");
+    }
+    S->p2p = p2p ? 1 : 0;
+    if (S->flags) S->allocs.push_back(S->flags);
+
+    DistHost H;
+    arrow_status st = dist_schedule(D, S->G, S->me, window_rows, head_chunk, P->esize(), S->p2p, H);
+    if (st != ARROW_OK) return st;
+    S->lo = H.lo;
+    S->hi = H.hi;
+    S->nl = (int)H.L.size();
+    if (const char *e = std::getenv("ARROW_SEG_BS")) S->bseg = std::atoi(e);
+    if (const char *e = std::getenv("ARROW_DIST_RESERVE_SMS")) S->reserve_sms = std::atoi(e);
+    if (const char *e = std::getenv("ARROW_DIST_PUSH_BLOCKS")) S->push_blocks = std::atoi(e);
+    const int nl = S->nl, G = S->G, me = S->me;
+    for (int i = 0; i < nl; ++i) {
+        S->h.push_back(H.L[i].h);
+        S->d0_off.push_back(S->d0_rows);
+        S->d0_rows += H.L[i].h;
+    }
+    S->send_peer = H.send_peer;
+    S->recv_peer = H.recv_peer;
+    S->out_peer = H.out_peer;
+    S->in_peer = H.in_peer;
+    for (int g = 0; g < G; ++g)
+        if (g != me) { S->fwd_rows += H.recv_peer[g]; S->rev_rows += H.out_peer[g]; }
+    std::vector<int32_t> zero = H.L.empty() ? std::vector<int32_t>() : H.L[0].zero_rows;
+    // level-0 heads owned here: Y starts at zero, every level adds its head partial afterwards
+    if (nl > 0) zero.insert(zero.end(), H.L[0].head_row.begin(), H.L[0].head_row.end());
+    std::vector<int32_t> pre_src, pre_dst, sp, ss, sd, pp, ps, pd;
+    if (S->p2p) {
+        S->o_d0 = 0;
+        S->o_c0 = S->d0_rows;
+        S->o_halo = 3 * S->d0_rows;
+        S->o_out = S->o_halo + H.halo_all[me];
+        S->ws_rows = S->o_out + H.stage_all[me] + H.send_rows;
+        S->send_row = H.send_row;
+        S->halo_dst_row = H.halo_dst_row;
+        if (const char *e = std::getenv("ARROW_DIST_HALO")) S->halo_dma = std::string(e) != "push";
+        build_csr(H.post, pp, ps, pd);
+    } else {
+        // workspace rows: [D0 | C0 | halo | send | staging | recv]
+        const int64_t n_send = (int64_t)H.send_idx_peers.size(), n_in = (int64_t)H.in_rows_peers.size();
+        S->o_d0 = 0;
+        S->o_c0 = S->d0_rows;
+        S->o_halo = 2 * S->d0_rows;
+        S->o_send = S->o_halo + H.halo_rows;
+        S->o_out = S->o_send + n_send;
+        S->o_in = S->o_out + H.out_rows;
+        S->ws_rows = S->o_in + n_in;
+        if (S->ws_rows >= ((int64_t)1 << 31))
+            return set_error(ARROW_E_UNSUPPORTED, "distributed workspace exceeds 2^31 rows");
+        // pre-exchange row mover: D0 (owned heads from X, the rest zero), C0 = 0, pack for peers and self
+        for (int i = 0; i < nl; ++i) {
+            std::vector<int32_t> own(S->h[i], -1);
+            for (size_t m = 0; m < H.L[i].head_j.size(); ++m) own[H.L[i].head_j[m]] = H.L[i].head_row[m];
+            for (int64_t j = 0; j < S->h[i]; ++j) { pre_src.push_back(own[j]); pre_dst.push_back((int32_t)(S->o_d0 + S->d0_off[i] + j)); }
+        }
+        for (int64_t r = 0; r < S->d0_rows; ++r) { pre_src.push_back(-1); pre_dst.push_back((int32_t)(S->o_c0 + r)); }
+        for (int64_t m = 0; m < n_send; ++m) { pre_src.push_back(H.send_idx_peers[m]); pre_dst.push_back((int32_t)(S->o_send + m)); }
+        for (size_t m = 0; m < H.send_idx_self.size(); ++m) {
+            pre_src.push_back(H.send_idx_self[m]);
+            pre_dst.push_back((int32_t)(S->o_halo + H.halo_self_off + (int64_t)m));
+        }
+        // gather-adds: own staging rows (before the reverse exchange completes), then received rows
+        // and the head partials of every level (after)
+        std::vector<std::pair<int32_t, int32_t>> cself, cpost;
+        for (size_t m = 0; m < H.in_rows_self.size(); ++m)
+            cself.emplace_back(H.in_rows_self[m], (int32_t)(S->o_out + H.out_self_off + (int64_t)m));
+        for (int64_t m = 0; m < n_in; ++m) cpost.emplace_back(H.in_rows_peers[m], (int32_t)(S->o_in + m));
+        for (int i = 0; i < nl; ++i)
+            for (size_t m = 0; m < H.L[i].head_j.size(); ++m)
+                cpost.emplace_back(H.L[i].head_row[m], (int32_t)(S->o_c0 + S->d0_off[i] + H.L[i].head_j[m]));
+        build_csr(cself, sp, ss, sd);
+        build_csr(cpost, pp, ps, pd);
+    }
+
+    bool ok = true;
+    for (int i = 0; i < nl; ++i) {
+        DistHostLevel &HL = H.L[i];
+        SegLevel sg;
+        sg.nseg = (int64_t)HL.seg_out.size();
+        sg.mode = 0;  // every output row is written once: local Y (level 0) or a staging buffer
+        sg.seg_out = upload(S, HL.seg_out, ok);
+        sg.seg_end = reinterpret_cast<uint32_t *>(upload(S, HL.seg_end, ok));
+        sg.ent_col = upload(S, HL.ent_col, ok);
+        sg.ent_val = upload(S, HL.ent_val.data(), HL.ent_val.size(), ok);
+        S->seg.push_back(sg);
+    }
+    S->n_pre = (int64_t)pre_src.size();
+    S->pre_src = upload(S, pre_src, ok);
+    S->pre_dst = upload(S, pre_dst, ok);
+    S->n_d0push = (int64_t)H.d0push_src.size();
+    S->d0push_src = upload(S, H.d0push_src, ok);
+    S->d0push_dst = upload(S, H.d0push_dst, ok);
+    S->n_pack = (int64_t)H.pack_src.size();
+    S->pack_src = upload(S, H.pack_src, ok);
+    S->pack_dst = upload(S, H.pack_dst, ok);
+    S->n_halopush = (int64_t)H.halopush_src.size();
+    S->halopush_src = upload(S, H.halopush_src, ok);
+    S->halopush_dst = upload(S, H.halopush_dst, ok);
+    S->n_zero = (int64_t)zero.size();
+    S->zero_rows = upload(S, zero, ok);
+    S->zero_tail_lo = H.zero_tail_lo;
+    S->zero_tail_n = H.zero_tail_n;
+    S->n_self = (int64_t)sd.size();
+    S->self_ptr = upload(S, sp, ok);
+    S->self_src = upload(S, ss, ok);
+    S->self_dst = upload(S, sd, ok);
+    S->n_post = (int64_t)pd.size();
+    S->post_ptr = upload(S, pp, ok);
+    S->post_src = upload(S, ps, ok);
+    S->post_dst = upload(S, pd, ok);
+    if (!ok) return set_error(ARROW_E_CUDA, "cudaMalloc/cudaMemcpy of the distributed layout failed");
+    if (cudaMalloc(&S->counters, (nl + 1) * sizeof(unsigned)) != cudaSuccess)
+        return set_error(ARROW_E_CUDA, "cudaMalloc(counters)");
+    S->allocs.push_back(S->counters);
+    P->local_begin = S->lo;
+    P->local_end = S->hi;
+    return ARROW_OK;
+}
+
+namespace {
+
+// (re)allocate the k-dependent workspace; P2P: collectively, then map every peer's workspace
+arrow_status ensure_ws(arrow_plan P, DistState *S, int64_t k, cudaStream_t st) {
+    if (k <= S->ws_k) return ARROW_OK;
+    const size_t es = P->esize();
+    DCUDA(cudaStreamSynchronize(st));
+    DCUDA(cudaStreamSynchronize(S->cs));
+    if (S->p2p) {
+        close_peers(S, S->ws_peer);
+        bool dummy = true;  // every rank has unmapped the old workspaces before any is freed
+        arrow_status s = all_true(S, dummy);
+        if (s != ARROW_OK) return s;
+    }
+    if (S->ws) cudaFree(S->ws);
+    S->ws = nullptr;
+    S->ws_k = 0;
+    DCUDA(cudaMalloc(&S->ws, (size_t)std::max<int64_t>(S->ws_rows, 1) * k * es));
+    S->ws_k = k;
+    if (S->p2p) {
+        bool ok = true;
+        arrow_status s = share_ptr(S, S->ws, S->ws_peer, ok);
+        if (s != ARROW_OK) return s;
+        s = all_true(S, ok);
+        if (s != ARROW_OK) return s;
+        if (!ok) return set_error(ARROW_E_CUDA, "mapping a peer's workspace (CUDA IPC) failed");
+    }
+    return ARROW_OK;
+}
+
+struct Marks {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    int operator()(cudaStream_t s) {
+        if (!on) return -1;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+        return (int)ev.size() - 1;
+    }
+    std::string el(int a, int b) const {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[a], ev[b]);
+        return std::to_string(ms);
+    }
+};
+
+// hand interval [a, b] to the profiling counters (the record owns both events)
+void prof_rec(arrow_plan P, Marks &M, int kid, int a, int b) {
+    P->prof.push_back(ProfRec{kid, P->prof_pos++, M.ev[a], M.ev[b]});
+    M.ev[a] = M.ev[b] = nullptr;
+}
+void marks_done(Marks &M) {
+    for (auto e : M.ev)
+        if (e) cudaEventDestroy(e);
+}
+
+// P2P transport: pushes and staging stores go straight into the peers' memory over NVLink;
+// three cross-GPU flag barriers order them (slot 0: every D0 complete; slot 1: every halo complete;
+// slot 2: every staging row and head partial complete).
+arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, int64_t k, cudaStream_t st) {
+    const int dt = P->dtype == ARROW_F64 ? 1 : 0;
+    const size_t es = P->esize();
+    const int G = S->G, me = S->me, nl = S->nl;
+    char *ws = reinterpret_cast<char *>(S->ws);
+    auto row = [&](int64_t r) { return ws + (size_t)r * k * es; };
+    const int par = (int)(S->calls & 1);
+    S->calls++;
+    const int64_t c0 = S->o_c0 + par * S->d0_rows;  // this call's C0
+    const int sms = std::max(1, P->num_sms - (S->halo_dma ? 0 : S->reserve_sms));
+    static const bool trace = std::getenv("ARROW_DIST_TRACE") != nullptr;
+    Marks M;
+    M.on = P->profiling || trace;
+
+    // S: the previous call (and the caller's writes of X) precede everything.  My head rows go into
+    // every rank's D0 first (level 0 needs only them), then C0 = 0 and the zero rows; DMA halo: the
+    // rows for the peers are packed, and C moves one chunk per peer with the copy engines while
+    // the SMs run level 0.  Push halo: C pushes the rows with a kernel next to level 0.
+    const int m0 = M(st);
+    DK(launch_push_rows(dt, X, S->d0push_src, S->d0push_dst, S->n_d0push, k, S->ws_peer, 0, st));
+    DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
+    DCUDA(cudaMemsetAsync(row(c0), 0, (size_t)S->d0_rows * k * es, st));
+    DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, st));
+    if (S->halo_dma) DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, st));
+    const int m0p = M(st);
+    DCUDA(cudaEventRecord(S->ev[0], st));
+    DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
+    const int m0c = M(S->cs);
+    if (S->halo_dma) {
+        for (int g = 0; g < G; ++g)
+            if (g != me && S->send_peer[g])
+                DCUDA(cudaMemcpyAsync(reinterpret_cast<char *>(S->ws_peer.p[g]) + (size_t)S->halo_dst_row[g] * k * es,
+                                      row(S->send_row[g]), (size_t)S->send_peer[g] * k * es, cudaMemcpyDeviceToDevice,
+                                      S->cs));
+    } else {
+        DK(launch_push_rows(dt, X, S->halopush_src, S->halopush_dst, S->n_halopush, k, S->ws_peer,
+                            S->push_blocks > 0 ? S->push_blocks : 8 * S->reserve_sms, S->cs));
+    }
+    const int m1c = M(S->cs);
+    DK(launch_barrier(S->flags_peer, S->flags, 1, ++S->epoch[1], me, G, S->cs));
+    const int m2c = M(S->cs);
+    DCUDA(cudaEventRecord(S->ev[1], S->cs));
+    // S: every D0 complete -> level 0
+    DK(launch_barrier(S->flags_peer, S->flags, 0, ++S->epoch[0], me, G, st));
+    const int m1 = M(st), m1b = M(st);
+    DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(c0), k, sms, S->counters, S->bseg, st));
+    const int m2 = M(st);
+    // levels >= 1 once every halo is complete; body rows are stored into their home rank's stage
+    DCUDA(cudaStreamWaitEvent(st, S->ev[1], 0));
+    const int m3 = M(st);
+    for (int i = 1; i < nl; ++i)
+        DK(launch_seg(dt, 2, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), Y, row(c0 + S->d0_off[i]),
+                      k, sms, S->counters + i, S->bseg, st, &S->ws_peer));
+    const int m4 = M(st), m4b = M(st);
+    // the A-isolated tail of Y (no level writes it) is zeroed while the other ranks finish
+    if (S->zero_tail_n)
+        DCUDA(cudaMemsetAsync(reinterpret_cast<char *>(Y) + (size_t)S->zero_tail_lo * k * es, 0,
+                              (size_t)S->zero_tail_n * k * es, st));
+    DK(launch_barrier(S->flags_peer, S->flags, 2, ++S->epoch[2], me, G, st));
+    const int m5 = M(st);
+    DK(launch_gather_add_peers(dt, S->ws_peer, S->d0_rows * par, S->post_ptr, S->post_src, S->post_dst, S->n_post, k,
+                               Y, st));
+    const int m6 = M(st);
+    if (trace) {
+        cudaEventSynchronize(M.ev[m6]);
+        std::string line = "[arrow dist rank " + std::to_string(me) + " p2p] ms: halo " +
+                           std::string(S->halo_dma ? "D0+zero+pack " + M.el(m0, m0p) + " dma " : "push ") + M.el(m0c, m1c) +
+                           " + barrier " + M.el(m1c, m2c) + " (done at " + M.el(m0, m2c) + ") | barrier0 " +
+                           M.el(m0p, m1) + " | K-A L0 " + M.el(m1, m2) + " | wait " + M.el(m2, m3) + " | K-A L>=1 " +
+                           M.el(m3, m4) + " | barrier " + M.el(m4, m5) + " | gather-add " + M.el(m5, m6) +
+                           " | total " + M.el(m0, m6) + " | rows fwd " + std::to_string(S->fwd_rows) + " rev " +
+                           std::to_string(S->rev_rows) + " d0 " + std::to_string(S->d0_rows);
+        fprintf(stderr, "%s\n", line.c_str());
+    }
+    if (P->profiling) {
+        prof_rec(P, M, ARROW_K_COMM, m0c, m2c);
+        prof_rec(P, M, ARROW_K_COMM, m0, m1);
+        prof_rec(P, M, ARROW_K_SEGMENTS, m1b, m2);
+        prof_rec(P, M, ARROW_K_SEGMENTS, m3, m4);
+        prof_rec(P, M, ARROW_K_COMM, m4b, m6);
+        P->prof_acc.calls += 1;
+    }
+    marks_done(M);
+    return ARROW_OK;
+}
+
+}  // namespace
+
 arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st) {
     DistState *S = P->dist;
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
@@ -462,41 +833,29 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         if (S->hi > S->lo) DCUDA(cudaMemsetAsync(Y, 0, (size_t)(S->hi - S->lo) * k * es, st));
         return ARROW_OK;
     }
-    if (k > S->ws_k) {
-        DCUDA(cudaStreamSynchronize(st));
-        DCUDA(cudaStreamSynchronize(S->cs));
-        if (S->ws) cudaFree(S->ws);
-        S->ws = nullptr;
-        S->ws_k = 0;
-        DCUDA(cudaMalloc(&S->ws, (size_t)std::max<int64_t>(S->ws_rows, 1) * k * es));
-        S->ws_k = k;
-    }
+    arrow_status wst = ensure_ws(P, S, k, st);
+    if (wst != ARROW_OK) return wst;
+    if (S->p2p) return dist_spmm_p2p(P, S, X, Y, k, st);
     char *ws = reinterpret_cast<char *>(S->ws);
     auto row = [&](int64_t r) { return ws + (size_t)r * k * es; };
     const int sms = std::max(1, P->num_sms - (G > 1 ? S->reserve_sms : 0));
-    // timing marks (profiling counters and ARROW_DIST_TRACE), each interval with its own events
     static const bool trace = std::getenv("ARROW_DIST_TRACE") != nullptr;
-    const bool timed = P->profiling || trace;
-    std::vector<cudaEvent_t> tev;
-    auto mark = [&](cudaStream_t s) {
-        if (!timed) return -1;
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        cudaEventRecord(e, s);
-        tev.push_back(e);
-        return (int)tev.size() - 1;
-    };
+    Marks M;
+    M.on = P->profiling || trace;
 
     // 1. (S) D0 / C0 / packing, zero rows
-    const int m0 = mark(st);
+    const int m0 = M(st);
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DK(launch_rows(dt, X, S->pre_src, S->pre_dst, S->n_pre, k, 0, ws, st));
     DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, st));
-    const int m1 = mark(st);
+    if (S->zero_tail_n)
+        DCUDA(cudaMemsetAsync(reinterpret_cast<char *>(Y) + (size_t)S->zero_tail_lo * k * es, 0,
+                              (size_t)S->zero_tail_n * k * es, st));
+    const int m1 = M(st);
     DCUDA(cudaEventRecord(S->ev[0], st));
     // 2. (C) D0 of level 0; forward rows + D0 of the other levels
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
-    const int m2 = mark(S->cs);
+    const int m2 = M(S->cs);
     DNCCL(ncclAllReduce(row(S->o_d0), row(S->o_d0), S->h[0] * k, nt, ncclSum, S->comm, S->cs));
     DCUDA(cudaEventRecord(S->ev[1], S->cs));
     DNCCL(ncclGroupStart());
@@ -512,23 +871,23 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         DNCCL(ncclAllReduce(row(S->o_d0 + S->h[0]), row(S->o_d0 + S->h[0]), (S->d0_rows - S->h[0]) * k, nt, ncclSum,
                             S->comm, S->cs));
     DNCCL(ncclGroupEnd());
-    const int m3 = mark(S->cs);
+    const int m3 = M(S->cs);
     DCUDA(cudaEventRecord(S->ev[2], S->cs));
     // 3. (S) level 0 overlaps the forward exchange; levels >= 1 after it
     DCUDA(cudaStreamWaitEvent(st, S->ev[1], 0));
-    const int m4 = mark(st);
+    const int m4 = M(st);
     DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(S->o_c0), k, sms, S->counters, S->bseg, st));
-    const int m5 = mark(st);
+    const int m5 = M(st);
     DCUDA(cudaStreamWaitEvent(st, S->ev[2], 0));
-    const int m6 = mark(st);
+    const int m6 = M(st);
     for (int i = 1; i < nl; ++i)
         DK(launch_seg(dt, 1, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), row(S->o_out),
                       row(S->o_c0 + S->d0_off[i]), k, sms, S->counters + i, S->bseg, st));
-    const int m7 = mark(st), m7b = mark(st);
+    const int m7 = M(st), m7b = M(st);
     DCUDA(cudaEventRecord(S->ev[3], st));
     // 4. (C) staging rows go home, head partials are reduced
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[3], 0));
-    const int m8 = mark(S->cs);
+    const int m8 = M(S->cs);
     DNCCL(ncclGroupStart());
     so = 0;
     ro = 0;
@@ -541,44 +900,37 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     }
     DNCCL(ncclAllReduce(row(S->o_c0), row(S->o_c0), S->d0_rows * k, nt, ncclSum, S->comm, S->cs));
     DNCCL(ncclGroupEnd());
-    const int m9 = mark(S->cs);
+    const int m9 = M(S->cs);
     DCUDA(cudaEventRecord(S->ev[4], S->cs));
     // 5. (S) own staging rows (overlaps the exchange), then received rows and owned head partials
     DK(launch_gather_add(dt, ws, S->self_ptr, S->self_src, S->self_dst, S->n_self, k, Y, st));
-    const int m10 = mark(st);
+    const int m10 = M(st);
     DCUDA(cudaStreamWaitEvent(st, S->ev[4], 0));
-    const int m11 = mark(st);
+    const int m11 = M(st);
     DK(launch_gather_add(dt, ws, S->post_ptr, S->post_src, S->post_dst, S->n_post, k, Y, st));
-    const int m12 = mark(st);
+    const int m12 = M(st);
     if (trace) {
-        cudaEventSynchronize(tev[m12]);
-        auto el = [&](int a, int b) {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, tev[a], tev[b]);
-            return std::to_string(ms);
-        };
-        std::string line = "[arrow dist rank " + std::to_string(me) + "] ms: pre " + el(m0, m1) + " | fwd " +
-                           el(m2, m3) + " (ends at " + el(m0, m3) + ") | K-A L0 " + el(m4, m5) + " (starts at " +
-                           el(m0, m4) + ") | wait " + el(m5, m6) + " | K-A L>=1 " + el(m6, m7) + " | rev " +
-                           el(m8, m9) + " | self-add " + el(m7, m10) + " | wait " + el(m10, m11) + " | post-add " +
-                           el(m11, m12) + " | total " + el(m0, m12) + " | rows fwd " + std::to_string(S->fwd_rows) +
-                           " rev " + std::to_string(S->rev_rows) + " d0 " + std::to_string(S->d0_rows);
+        cudaEventSynchronize(M.ev[m12]);
+        std::string line = "[arrow dist rank " + std::to_string(me) + " nccl] ms: pre " + M.el(m0, m1) + " | fwd " +
+                           M.el(m2, m3) + " (ends at " + M.el(m0, m3) + ") | K-A L0 " + M.el(m4, m5) + " (starts at " +
+                           M.el(m0, m4) + ") | wait " + M.el(m5, m6) + " | K-A L>=1 " + M.el(m6, m7) + " | rev " +
+                           M.el(m8, m9) + " | self-add " + M.el(m7, m10) + " | wait " + M.el(m10, m11) +
+                           " | post-add " + M.el(m11, m12) + " | total " + M.el(m0, m12) + " | rows fwd " +
+                           std::to_string(S->fwd_rows) + " rev " + std::to_string(S->rev_rows) + " d0 " +
+                           std::to_string(S->d0_rows);
         fprintf(stderr, "%s\n", line.c_str());
     }
     if (P->profiling) {
-        // compute: both K-A phases; communication: pre-exchange work and the two exchanges
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m0], tev[m1]});
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m2], tev[m3]});
-        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, tev[m4], tev[m5]});
-        P->prof.push_back(ProfRec{ARROW_K_SEGMENTS, P->prof_pos++, tev[m6], tev[m7]});
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m8], tev[m9]});
-        P->prof.push_back(ProfRec{ARROW_K_COMM, P->prof_pos++, tev[m7b], tev[m12]});
+        // compute: both K-A phases; communication: pre-exchange work, the two exchanges, the adds
+        prof_rec(P, M, ARROW_K_COMM, m0, m1);
+        prof_rec(P, M, ARROW_K_COMM, m2, m3);
+        prof_rec(P, M, ARROW_K_SEGMENTS, m4, m5);
+        prof_rec(P, M, ARROW_K_SEGMENTS, m6, m7);
+        prof_rec(P, M, ARROW_K_COMM, m8, m9);
+        prof_rec(P, M, ARROW_K_COMM, m7b, m12);
         P->prof_acc.calls += 1;
-        // the remaining marks are not owned by a ProfRec
-        for (int m : {m10, m11}) cudaEventDestroy(tev[m]);
-    } else {
-        for (auto e : tev) cudaEventDestroy(e);
     }
+    marks_done(M);
     return ARROW_OK;
 }
 
@@ -589,7 +941,7 @@ extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nrank
     if (!d || !lohi) return arrow::set_error(ARROW_E_INVALID_ARG, "NULL argument");
     arrow::DistHost H;
     arrow_status st = arrow::dist_schedule(*d, nranks, rank, window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
-                                           head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, H);
+                                           head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, 0, H);
     if (st != ARROW_OK) return st;
     lohi[0] = H.lo;
     lohi[1] = H.hi;
@@ -605,7 +957,7 @@ extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nrank
             c[4 * G + 0] = (int64_t)L.ent_col.size();
             c[4 * G + 1] = (int64_t)L.seg_out.size();
             c[4 * G + 2] = (int64_t)L.head_j.size();
-            c[4 * G + 3] = (int64_t)L.zero_rows.size();
+            c[4 * G + 3] = (int64_t)L.zero_rows.size() + (&L == &H.L[0] ? H.zero_tail_n : 0);
             c += 4 * G + 4;
         }
     }

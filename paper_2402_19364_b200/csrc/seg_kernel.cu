@@ -90,6 +90,9 @@ __device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
 //   out <  0, DIST == 0  : atomic add into Y[out & 0x7fffffff]  (head-row slice of one window)
 //   out <  0, DIST == 1  : atomic add into C0[out & 0x7fffffff] (head partial, reduced over ranks)
 //   col <  0 (DIST only) : the row comes from the head block D0 (broadcast), else from X
+//   DIST == 2            : out >= 0 encodes (rank << kPeerShift | row): the row is stored into
+//                          rank's staging buffer outs.p[rank] -- over NVLink for a peer rank;
+//                          with kLocalRmwBit it is added into Y[row] (a row homed on this GPU)
 template <typename T, int VEC, int LPE, int MODE, int DIST>
 __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__ seg_out,
                                                      const uint32_t *__restrict__ seg_end, int64_t nseg,
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
                                                      const T *__restrict__ ent_val, const T *__restrict__ X,
                                                      const T *__restrict__ D0, T *__restrict__ Y,
                                                      T *__restrict__ C0, int64_t k, unsigned *__restrict__ counter,
-                                                     int bseg) {
+                                                     int bseg, const PeerPtrs outs) {
     constexpr int UNROLL = (LPE == 32) ? 8 : 4;
     constexpr int SLAB = LPE * VEC;
     constexpr int SUBS = 32 / LPE;
@@ -167,6 +170,15 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
                                 if (o < 0) {
                                     T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
                                     atomic_add_frag<T, VEC>(dst + col0, acc);
+                                } else if (DIST == 2 && (o & kLocalRmwBit)) {
+                                    T *py = Y + (int64_t)(o & kPeerRowMask) * k + col0;
+                                    Frag<T, VEC> y = ld_plain<T, VEC>(py);
+#pragma unroll
+                                    for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                    st_plain<T, VEC>(py, y);
+                                } else if (DIST == 2) {
+                                    T *base = reinterpret_cast<T *>(outs.p[(uint32_t)o >> kPeerShift]);
+                                    st_stream<T, VEC>(base + (int64_t)(o & kPeerRowMask) * k + col0, acc);
                                 } else if (MODE == 0) {
                                     st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
                                 } else {
@@ -211,7 +223,7 @@ inline int pick_lpe(int64_t k, int vec) {
 
 template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segments(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-                 unsigned *counter, int bseg, cudaStream_t st) {
+                 unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
     if (bseg <= 0 || bseg > LPE) bseg = LPE;
     auto kern = k_segments<T, VEC, LPE, MODE, DIST>;
     static int bps = 0;
@@ -226,32 +238,33 @@ int run_segments(const SegLevel &L, const void *X, const void *D0, void *Y, void
     kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
                                             reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
                                             reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
-                                            reinterpret_cast<T *>(C0), k, counter, bseg);
+                                            reinterpret_cast<T *>(C0), k, counter, bseg, outs);
     return (int)cudaGetLastError();
 }
 
 template <typename T, int VEC, int MODE, int DIST>
 int run_segments_lpe(int lpe, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                     int num_sms, unsigned *counter, int bseg, cudaStream_t st) {
+                     int num_sms, unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
     switch (lpe) {
-        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
     }
 }
 
 template <typename T, int VEC>
 int run_segments_mode(int lpe, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                      int64_t k, int num_sms, unsigned *counter, int bseg, cudaStream_t st) {
+                      int64_t k, int num_sms, unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
+    if (dist == 2) return run_segments_lpe<T, VEC, 0, 2>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
     if (dist) {
-        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st)
-                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st)
+                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
     }
-    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st)
-                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st)
+                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
 }
 
 
@@ -259,19 +272,24 @@ int run_segments_mode(int lpe, int dist, const SegLevel &L, const void *X, const
 }  // namespace kseg
 
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream) {
+               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs) {
     using namespace kseg;
     if (L.nseg == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
+    PeerPtrs po{};
+    if (outs) po = *outs;
+    if (dist == 2 && !outs) return (int)cudaErrorInvalidValue;
+    int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
+    if (dist == 2)
+        for (const void *p : po.p) vec = std::min(vec, pick_vec(dtype, k, {p}));
     const int lpe = pick_lpe(k, vec);
     if (dtype == 0) {
-        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
+        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
+        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
     }
-    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
-    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, st);
+    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
+    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
 }
 
 }  // namespace arrow
