@@ -100,6 +100,7 @@ struct DistState {
     // P2P, DMA halo (default; ARROW_DIST_HALO=push uses the push kernel): pack, then one copy-engine
     // transfer per peer into its halo
     int halo_dma = 1;
+    int pack_on_comm = 0;  // ARROW_DIST_PACK=comm: pack on the communication stream, next to level 0
     int32_t *pack_src = nullptr, *pack_dst = nullptr;
     int64_t n_pack = 0;
     std::vector<int64_t> send_row, halo_dst_row;
@@ -119,7 +120,11 @@ struct DistState {
     std::vector<void *> allocs;
     unsigned *counters = nullptr;
     cudaStream_t cs = nullptr;
-    cudaEvent_t ev[5] = {};
+    cudaEvent_t ev[6] = {};
+    // P2P DMA halo: one copy stream per peer, so the transfers to different peers run on
+    // different copy engines concurrently
+    std::vector<cudaStream_t> ds;
+    std::vector<cudaEvent_t> ds_ev;
     int bseg = 16, reserve_sms = 16, push_blocks = 0;
     int64_t fwd_rows = 0, rev_rows = 0;  // rows exchanged with peers (trace)
 };
@@ -141,6 +146,8 @@ void dist_free(DistState *d) {
     if (d->ws) cudaFree(d->ws);
     for (auto e : d->ev)
         if (e) cudaEventDestroy(e);
+    for (auto e : d->ds_ev) cudaEventDestroy(e);
+    for (auto s : d->ds) cudaStreamDestroy(s);
     if (d->cs) cudaStreamDestroy(d->cs);
     delete d;
 }
@@ -591,6 +598,17 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         S->send_row = H.send_row;
         S->halo_dst_row = H.halo_dst_row;
         if (const char *e = std::getenv("ARROW_DIST_HALO")) S->halo_dma = std::string(e) != "push";
+        if (const char *e = std::getenv("ARROW_DIST_PACK")) S->pack_on_comm = std::string(e) == "comm";
+        for (int g = 0; g < G; ++g) {
+            if (g == me) continue;
+            cudaStream_t q;
+            cudaEvent_t e;
+            if (cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return set_error(ARROW_E_CUDA, "cudaStreamCreate/cudaEventCreate (copy streams)");
+            S->ds.push_back(q);
+            S->ds_ev.push_back(e);
+        }
         build_csr(H.post, pp, ps, pd);
     } else {
         // workspace rows: [D0 | C0 | halo | send | staging | recv]
@@ -758,17 +776,26 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(c0), 0, (size_t)S->d0_rows * k * es, st));
     DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, st));
-    if (S->halo_dma) DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, st));
+    if (S->halo_dma && !S->pack_on_comm) DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, st));
     const int m0p = M(st);
     DCUDA(cudaEventRecord(S->ev[0], st));
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
     const int m0c = M(S->cs);
+    if (S->halo_dma && S->pack_on_comm) DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, S->cs));
     if (S->halo_dma) {
-        for (int g = 0; g < G; ++g)
-            if (g != me && S->send_peer[g])
+        DCUDA(cudaEventRecord(S->ev[5], S->cs));
+        for (int g = 0, q = 0; g < G; ++g) {
+            if (g == me) continue;
+            cudaStream_t d = S->ds[q];
+            DCUDA(cudaStreamWaitEvent(d, S->ev[5], 0));
+            if (S->send_peer[g])
                 DCUDA(cudaMemcpyAsync(reinterpret_cast<char *>(S->ws_peer.p[g]) + (size_t)S->halo_dst_row[g] * k * es,
                                       row(S->send_row[g]), (size_t)S->send_peer[g] * k * es, cudaMemcpyDeviceToDevice,
-                                      S->cs));
+                                      d));
+            DCUDA(cudaEventRecord(S->ds_ev[q], d));
+            DCUDA(cudaStreamWaitEvent(S->cs, S->ds_ev[q], 0));
+            ++q;
+        }
     } else {
         DK(launch_push_rows(dt, X, S->halopush_src, S->halopush_dst, S->n_halopush, k, S->ws_peer,
                             S->push_blocks > 0 ? S->push_blocks : 8 * S->reserve_sms, S->cs));
