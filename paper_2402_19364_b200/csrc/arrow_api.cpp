@@ -485,6 +485,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
                 SegLevel S;
                 S.nseg = (int64_t)so.size();
                 S.mode = B.mode;
+                S.max_x_row = P->n;  // entries reference rows of X [n, k]
                 auto up = [&](const void *src, size_t bytes) -> void * {
                     void *d = nullptr;
                     if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;

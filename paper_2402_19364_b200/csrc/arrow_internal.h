@@ -69,6 +69,7 @@ struct SegLevel {
     uint32_t *seg_end = nullptr;  // [nseg] end offset into the entries
     int32_t *ent_col = nullptr;   // [nnz] X row (bit 31: D0 row)
     void *ent_val = nullptr;      // [nnz]
+    int64_t max_x_row = (int64_t)1 << 40;  // bound on the X rows referenced (enables 32-bit offsets)
 };
 // Peer (NVLink) addressing of the distributed P2P transport: an encoded row is
 // (rank << kPeerShift | row) into the per-rank base pointers of a PeerPtrs; kParityBit marks a row

@@ -652,6 +652,8 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         DistHostLevel &HL = H.L[i];
         SegLevel sg;
         sg.nseg = (int64_t)HL.seg_out.size();
+        // level 0 reads the local X rows, levels >= 1 the halo inside the workspace
+        sg.max_x_row = (i == 0) ? std::max<int64_t>(S->hi - S->lo, S->d0_rows) : S->ws_rows;
         sg.mode = 0;  // every output row is written once: local Y (level 0) or a staging buffer
         sg.seg_out = upload(S, HL.seg_out, ok);
         sg.seg_end = reinterpret_cast<uint32_t *>(upload(S, HL.seg_end, ok));

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "arrow_internal.h"
 
@@ -199,8 +200,6 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
     }
 }
 
-// K-Z: zero the listed Y rows (level 0: head rows, which then accumulate head slices atomically,
-// and rows with no entry in B_0, incl. A-isolated vertices).
 
 inline int pick_vec(int dtype, int64_t k, std::initializer_list<const void *> ptrs) {
     const int es = dtype == 1 ? 8 : 4;
@@ -219,6 +218,168 @@ inline int pick_lpe(int64_t k, int vec) {
     int lpe = 1;
     while (lpe < 32 && lpe < need) lpe <<= 1;
     return lpe;
+}
+
+// ------------------------------------------------------------------------------------ K-A (full warp)
+// The same segment stream as k_segments, specialised for full-warp rows (LPE = 32, k a multiple
+// of 32*VEC -- k = 128 fp32 / 64 fp64 and up): per 32-entry chunk every lane stages one (col, val)
+// pair into a warp-private shared-memory slot, after which an entry costs one broadcast LDS, one
+// address IMAD, one 16-byte LDG and VEC FFMAs.  Groups of 8 entries with no segment end (long rows,
+// head-row chunks) run without per-entry end tests; only a batch's last group is predicated.
+template <typename T> struct StagedEnt;
+template <> struct alignas(8) StagedEnt<float> { int32_t col; float val; };
+template <> struct alignas(16) StagedEnt<double> { int32_t col; int32_t pad; double val; };
+
+template <typename T, int VEC, int MODE, int DIST>
+__device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T *Y, T *C0, int64_t k, int64_t col0,
+                                          const PeerPtrs &outs) {
+    if (o < 0) {
+        T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
+        atomic_add_frag<T, VEC>(dst + col0, acc);
+    } else if (DIST == 2 && (o & kLocalRmwBit)) {
+        T *py = Y + (int64_t)(o & kPeerRowMask) * k + col0;
+        Frag<T, VEC> y = ld_plain<T, VEC>(py);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+        st_plain<T, VEC>(py, y);
+    } else if (DIST == 2) {
+        T *base = reinterpret_cast<T *>(outs.p[(uint32_t)o >> kPeerShift]);
+        st_stream<T, VEC>(base + (int64_t)(o & kPeerRowMask) * k + col0, acc);
+    } else if (MODE == 0) {
+        st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
+    } else {
+        T *py = Y + (int64_t)o * k + col0;
+        Frag<T, VEC> y = ld_plain<T, VEC>(py);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+        st_plain<T, VEC>(py, y);
+    }
+}
+
+template <typename T> struct Seg32Unroll { static constexpr int value = sizeof(T) == 4 ? 8 : 4; };
+
+template <typename T, int VEC, int MODE, int DIST, bool OFF32>
+__device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int n, unsigned grp, const char *Xc,
+                                            const char *Dc, uint32_t rowbytes, uint32_t lane_off, Frag<T, VEC> &acc,
+                                            int &cur, int32_t my_out, T *Y, T *C0, int64_t k, int64_t col0,
+                                            const PeerPtrs &outs) {
+    constexpr int UNROLL = Seg32Unroll<T>::value;
+    Frag<T, VEC> xv[UNROLL];
+    T av[UNROLL];
+#pragma unroll
+    for (int t = 0; t < UNROLL; ++t) {
+        const int32_t col = __shfl_sync(0xffffffffu, mycol, (u0 + t) & 31);
+        av[t] = __shfl_sync(0xffffffffu, myval, (u0 + t) & 31);
+        const char *p;
+        if (DIST && col < 0) p = Dc + (uint64_t)((uint32_t)col & 0x7fffffffu) * rowbytes + lane_off;
+        else if (OFF32) p = Xc + (uint32_t)((uint32_t)col * rowbytes + lane_off);
+        else p = Xc + (uint64_t)(uint32_t)col * rowbytes + lane_off;
+        if (t < n) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
+    }
+    if (n == UNROLL && grp == 0u) {  // warp-uniform: no segment ends in this group
+#pragma unroll
+        for (int t = 0; t < UNROLL; ++t)
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+        return;
+    }
+#pragma unroll
+    for (int t = 0; t < UNROLL; ++t) {
+        if (t < n) {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+        }
+        if ((grp >> t) & 1u) {  // (only set for t < n)
+            const int32_t o = __shfl_sync(0xffffffffu, my_out, cur);
+            flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
+            acc.zero();
+            ++cur;
+        }
+    }
+}
+
+template <typename T, int VEC, int MODE, int DIST, bool OFF32>
+__global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ seg_out,
+                                                  const uint32_t *__restrict__ seg_end, int64_t nseg,
+                                                  const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
+                                                  const T *__restrict__ X, const T *__restrict__ D0,
+                                                  T *__restrict__ Y, T *__restrict__ C0, int64_t k,
+                                                  unsigned *__restrict__ counter, int bseg, const PeerPtrs outs) {
+    constexpr int UNROLL = Seg32Unroll<T>::value;
+    const int lane = threadIdx.x & 31;
+    const int64_t nbatch = (nseg + bseg - 1) / bseg;
+    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
+    const char *Xc = reinterpret_cast<const char *>(X);
+    const char *Dc = reinterpret_cast<const char *>(D0);
+
+    for (;;) {
+        unsigned wb = 0;
+        if (lane == 0) wb = atomicAdd(counter, 1u);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if ((int64_t)wb >= nbatch) break;
+        const int64_t s0 = (int64_t)wb * bseg;
+        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
+        const int32_t my_out = (lane < nb) ? __ldg(seg_out + s0 + lane) : 0;
+        const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+
+        for (int64_t c0 = 0; c0 < k; c0 += 32 * VEC) {
+            const int64_t col0 = c0 + (int64_t)lane * VEC;
+            const uint32_t lane_off = (uint32_t)(col0 * (int64_t)sizeof(T));
+            Frag<T, VEC> acc;
+            acc.zero();
+            int cur = 0;
+            for (uint32_t cb = e_begin; cb < e_end; cb += 32) {
+                const int cnt = (e_end - cb < 32u) ? (int)(e_end - cb) : 32;
+                int32_t mycol = 0;
+                T myval = T(0);
+                if (lane < cnt) {
+                    mycol = __ldcs(ent_col + cb + lane);
+                    myval = __ldcs(ent_val + cb + lane);
+                }
+                const uint32_t rel = my_end - 1u - cb;
+                const unsigned endmask = __reduce_or_sync(0xffffffffu, (rel < 32u) ? (1u << rel) : 0u);
+#pragma unroll 1
+                for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
+                    const unsigned grp = (endmask >> u0) & ((1u << UNROLL) - 1u);
+                    seg32_group<T, VEC, MODE, DIST, OFF32>(mycol, myval, u0, min(cnt - u0, UNROLL), grp, Xc, Dc,
+                                                           rowbytes, lane_off, acc, cur, my_out, Y, C0, k, col0, outs);
+                }
+            }
+        }
+    }
+}
+
+template <typename T, int VEC, int MODE, int DIST>
+int run_seg32(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
+              unsigned *counter, int bseg, const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    if (bseg <= 0 || bseg > 32) bseg = 32;
+    auto kern = off32 ? k_seg32<T, VEC, MODE, DIST, true> : k_seg32<T, VEC, MODE, DIST, false>;
+    static int bps[2] = {0, 0};
+    int &b = bps[off32 ? 1 : 0];
+    if (b == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
+        if (b <= 0) b = 1;
+    }
+    const int64_t nbatch = (L.nseg + bseg - 1) / bseg;
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (nbatch + 7) / 8);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
+                                           reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                           reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
+                                           reinterpret_cast<T *>(C0), k, counter, bseg, outs);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int VEC>
+int run_seg32_mode(int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+                   int num_sms, unsigned *counter, int bseg, const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    if (dist == 2) return run_seg32<T, VEC, 0, 2>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st);
+    if (dist) return L.mode == 0 ? run_seg32<T, VEC, 0, 1>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st)
+                                 : run_seg32<T, VEC, 1, 1>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st);
+    return L.mode == 0 ? run_seg32<T, VEC, 0, 0>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st)
+                       : run_seg32<T, VEC, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st);
 }
 
 template <typename T, int VEC, int LPE, int MODE, int DIST>
@@ -283,6 +444,16 @@ int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void
     if (dist == 2)
         for (const void *p : po.p) vec = std::min(vec, pick_vec(dtype, k, {p}));
     const int lpe = pick_lpe(k, vec);
+    // full-warp rows: the staged-entry kernel (ARROW_SEG32=0 keeps the generic one)
+    static const bool seg32 = !(std::getenv("ARROW_SEG32") && std::getenv("ARROW_SEG32")[0] == '0');
+    if (seg32 && lpe == 32 && k % (32 * vec) == 0) {
+        // 32-bit X offsets when every X row offset (and D0's) fits
+        const bool off32 = (uint64_t)L.max_x_row * (uint64_t)k * (dtype == 1 ? 8u : 4u) < (1ull << 32) - (1ull << 20);
+        if (dtype == 0 && vec == 4)
+            return run_seg32_mode<float, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
+        if (dtype == 1 && vec == 2)
+            return run_seg32_mode<double, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
+    }
     if (dtype == 0) {
         if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
         if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
