@@ -784,10 +784,28 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
         const DeviceLevel &L = P->levels[i];
         cudaEvent_t a = nullptr;
         int e = 0;
+        bool joined = true;
         if (L.nzero > 0) {  // S0/S3 single GPU: head rows and entry-less rows of level 0 start at zero
+            // ARROW_KZ_OVERLAP=1: head rows (the first L.head zero rows) before level 0, which adds into
+            // them; the rest on a side stream next to level 0, joined before level 1 (measured slower on
+            // config R: 4.0 vs 3.1 ms -- a small side grid cannot keep enough stores in flight)
+            static const bool overlap = std::getenv("ARROW_KZ_OVERLAP") && std::getenv("ARROW_KZ_OVERLAP")[0] == '1';  // measured slower
+            const int64_t nh = (overlap && i == 0 && L.nzero > L.head) ? L.head : L.nzero;
             prof_begin(P, st, a);
-            e = launch_zero_rows(dt, L.zero_rows, L.nzero, k, Y, st);
+            e = launch_zero_rows(dt, L.zero_rows, nh, k, Y, st);
             prof_end(P, st, ARROW_K_HEAD_STAGE, a);
+            if (!e && nh < L.nzero) {
+                if (!P->side) {
+                    CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+                    CUDA_TRY(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
+                    CUDA_TRY(cudaEventCreateWithFlags(&P->join_ev, cudaEventDisableTiming));
+                }
+                CUDA_TRY(cudaEventRecord(P->fork_ev, st));
+                CUDA_TRY(cudaStreamWaitEvent(P->side, P->fork_ev, 0));
+                e = launch_zero_rows(dt, L.zero_rows + nh, L.nzero - nh, k, Y, P->side, P->num_sms);
+                CUDA_TRY(cudaEventRecord(P->join_ev, P->side));
+                joined = false;
+            }
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
@@ -796,6 +814,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
         else
             e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
+        if (!joined) CUDA_TRY(cudaStreamWaitEvent(st, P->join_ev, 0));
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
     }
     return ARROW_OK;

@@ -124,7 +124,7 @@ int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_
                       void *D0, void *C0, void *stream);
 int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k,
                          int add, void *Y, void *stream);
-int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream);
+int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream, int blocks = 0);
 int launch_zero(void *Y, int64_t bytes, void *stream);
 // dst[didx[i]] (= | +=) src[sidx[i]] (identity when an index list is NULL; sidx[i] < 0 writes zero)
 int launch_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k, int add,

@@ -220,11 +220,12 @@ int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, cons
     return dtype == 1 ? launch_stream_f64(a, c, st) : launch_stream_f32(a, c, st);
 }
 
-int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream) {
+int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream, int blocks) {
     if (nrows == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int vec = pick_vec(dtype, k, {Y});
-    const unsigned g = grid_for(nrows * (k / vec));
+    unsigned g = grid_for(nrows * (k / vec));
+    if (blocks > 0 && (unsigned)blocks < g) g = (unsigned)blocks;
     if (dtype == 0) {
         if (vec == 4) k_zero_rows<float, 4><<<g, 256, 0, st>>>(rows, nrows, k, (float *)Y);
         else if (vec == 2) k_zero_rows<float, 2><<<g, 256, 0, st>>>(rows, nrows, k, (float *)Y);

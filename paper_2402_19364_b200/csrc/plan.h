@@ -63,6 +63,10 @@ struct arrow_plan_s {
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
     cudaStream_t stream = nullptr;
+    // single GPU: the level-0 zero rows that K-A does not touch (entry-less / A-isolated rows) are
+    // written on a side stream next to level 0 (HBM writes under an L2-bound kernel)
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool poisoned = false;
     // profiling
     bool profiling = false;
@@ -84,6 +88,9 @@ struct arrow_plan_s {
         if (ws) cudaFree(ws);
         if (host_x) cudaFree(host_x);
         if (host_y) cudaFree(host_y);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
+        if (side) cudaStreamDestroy(side);
     }
     size_t esize() const { return dtype == ARROW_F64 ? 8 : 4; }
 };

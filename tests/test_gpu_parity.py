@@ -144,8 +144,10 @@ def test_host_entry_point_and_repeat():
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f32")
     Yh = plan.spmm_host(X)
     Yd = run(plan, X)
-    assert np.array_equal(Yh, Yd)
+    # fp32 head-row partials are added atomically (order not fixed), so two calls agree to rounding
+    np.testing.assert_allclose(Yh, Yd, rtol=1e-5, atol=1e-5)
     check_fp32(g, Yh, X)
+    check_fp32(g, Yd, X)
     # repeated calls are deterministic in fp64 and k may change between calls
     p64 = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f64")
     for k in (8, 64, 8):
