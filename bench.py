@@ -141,6 +141,34 @@ def cpu_oracle_baseline(g, X, k, budget_s=12.0, max_reps=10):
                       f"1 warm-up), oracle/spmm_ref.c with OpenMP over rows"}
 
 
+def cusparse_baseline(g, Xd, k, flop, stream, reps=10):
+    """Library comparator (SURVEY §8 acceptance 5): the same Y = A X with cuSPARSE CSR SpMM through
+    torch.sparse.mm on the same device-resident X, timed with CUDA events like our own step."""
+    import torch
+    try:
+        dev = Xd.device
+        A = torch.sparse_csr_tensor(torch.from_numpy(g.row_ptr.astype(np.int64)).to(dev),
+                                    torch.from_numpy(g.col.astype(np.int64)).to(dev),
+                                    torch.from_numpy(g.val.astype(np.float32 if Xd.dtype == torch.float32 else np.float64)).to(dev),
+                                    size=(g.n, g.n))
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                Y = torch.sparse.mm(A, Xd)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                Y = torch.sparse.mm(A, Xd)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        del A, Y
+        torch.cuda.empty_cache()
+        return {"impl": "cuSPARSE CSR SpMM via torch.sparse.mm (same X, device-resident)", "ms_per_step": round(ms, 4),
+                "value": round(flop / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "steps": reps}
+    except Exception as e:  # a comparator, not the product: report why it did not run
+        return {"impl": "cuSPARSE via torch.sparse.mm", "unavailable": str(e)[:200]}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the oracle as it stands, on this arm's config and metric (rank 0 only)."""
     if rank != 0:
@@ -184,6 +212,7 @@ def main():
     ap.add_argument("--impl", default="arrow", choices=["arrow", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lib-baseline", action="store_true", help="skip the cuSPARSE (torch.sparse) comparator")
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
     ap.add_argument("--batch-segments", type=int, default=0)
@@ -300,6 +329,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(g, X, k)
+    lib = None
+    if rank == 0 and world == 1 and not args.no_lib_baseline:
+        lib = cusparse_baseline(g, Xd, k, flop, stream)
 
     if rank == 0:
         traffic = load_traffic(args.config, k, dtype)
@@ -315,7 +347,7 @@ def main():
                              "frac_of_measured": round(b_alg / (ms_per_step * 1e-3) / 1e9 / peak, 4),
                              "frac_of_8TBs": round(b_alg / (ms_per_step * 1e-3) / 8e12, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k_segments (K-A)",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "K-A (k_seg32 for full-warp rows, else k_segments)",
                          "bytes_per_step": ka_bytes, "launches_per_step": ka_launches,
                          "ms_per_step": round(ka_ms_per_step, 4), "share_of_step": round(step_share, 4),
                          "peak_source": peak_src},
@@ -325,6 +357,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "library_baseline": lib,
             "create_seconds": round(info["create_seconds"], 2),
         }
         print(json.dumps(line), flush=True)
