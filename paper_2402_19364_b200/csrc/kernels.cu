@@ -94,12 +94,19 @@ __device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
 template <typename T, int VEC>
 __global__ void __launch_bounds__(256) k_zero_rows(const int32_t *__restrict__ rows, int64_t nrows, int64_t k,
                                                    T *__restrict__ Y) {
-    const int64_t kv = k / VEC, total = nrows * kv;
+    // one warp per row, 4 rows per warp pass (streaming stores)
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     Frag<T, VEC> z;
     z.zero();
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = t / kv, c = (t - j * kv) * VEC;
-        st_stream<T, VEC>(Y + (int64_t)__ldg(rows + j) * k + c, z);
+    for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; r0 < nrows; r0 += nw * 4) {
+        int64_t row[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) row[t] = (r0 + t < nrows) ? (int64_t)__ldg(rows + r0 + t) : -1;
+        for (int64_t c = (int64_t)lane * VEC; c < k; c += 32 * VEC)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (row[t] >= 0) st_stream<T, VEC>(Y + row[t] * k + c, z);
     }
 }
 
@@ -224,7 +231,9 @@ int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, v
     if (nrows == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int vec = pick_vec(dtype, k, {Y});
-    unsigned g = grid_for(nrows * (k / vec));
+    int64_t gw = (nrows + 31) / 32;  // 8 warps x 4 rows per block pass
+    if (gw > 148 * 8) gw = 148 * 8;
+    unsigned g = (unsigned)std::max<int64_t>(gw, 1);
     if (blocks > 0 && (unsigned)blocks < g) g = (unsigned)blocks;
     if (dtype == 0) {
         if (vec == 4) k_zero_rows<float, 4><<<g, 256, 0, st>>>(rows, nrows, k, (float *)Y);

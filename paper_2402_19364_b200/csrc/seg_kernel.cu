@@ -478,14 +478,20 @@ int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void
     const int lpe = pick_lpe(k, vec);
     // full-warp rows: the staged-entry kernel (ARROW_SEG32=0 keeps the generic one)
     static const bool seg32 = !(std::getenv("ARROW_SEG32") && std::getenv("ARROW_SEG32")[0] == '0');
+    // 32-bit X offsets when every X row offset (and D0's) fits
+    const bool off32 = (uint64_t)L.max_x_row * (uint64_t)k * (dtype == 1 ? 8u : 4u) < (1ull << 32) - (1ull << 20);
     if (seg32 && lpe == 32 && k % (32 * vec) == 0) {
-        // 32-bit X offsets when every X row offset (and D0's) fits
-        const bool off32 = (uint64_t)L.max_x_row * (uint64_t)k * (dtype == 1 ? 8u : 4u) < (1ull << 32) - (1ull << 20);
         if (dtype == 0 && vec == 4)
             return run_seg32_mode<float, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
         if (dtype == 1 && vec == 2)
             return run_seg32_mode<double, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
     }
+    // fp32 rows of 32 or 64 elements: one row per warp with 4- or 8-byte lanes (one 128/256-byte
+    // request per entry) instead of 8/16-lane sub-warps that run different batches in lockstep
+    static const bool narrow = !(std::getenv("ARROW_SEG_NARROW") && std::getenv("ARROW_SEG_NARROW")[0] == '0');
+    if (seg32 && narrow && dtype == 0 && (k == 32 || k == 64) && vec >= k / 32)
+        return k == 64 ? run_seg32_mode<float, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st)
+                       : run_seg32_mode<float, 1>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
     if (dtype == 0) {
         if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
         if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
