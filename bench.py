@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--impl", default="arrow", choices=["arrow", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--order", default="original", choices=["original", "permuted"],
+                    help="X/Y row order: original vertex ids, or pi_0 order (R18; forced when distributed)")
     ap.add_argument("--no-lib-baseline", action="store_true", help="skip the cuSPARSE (torch.sparse) comparator")
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
@@ -245,10 +247,11 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         comm = ab.Comm(world, rank, uid[0])
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm,
+                   order=("permuted" if comm is not None else args.order),
                    window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments)
     info = plan.info()
     lo, hi = plan.local_begin, plan.local_end
-    if comm is not None:
+    if comm is not None or args.order == "permuted":
         perm0 = plan.export_level(0)[0]
         Xl = X[perm0[lo:hi]]
     else:
@@ -342,6 +345,7 @@ def main():
             "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}",
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
+                       "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",
                        "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},
             "hbm_roofline": {"bytes_alg_per_step": b_alg, "achieved_GBs": round(b_alg / (ms_per_step * 1e-3) / 1e9, 1),
                              "frac_of_measured": round(b_alg / (ms_per_step * 1e-3) / 1e9 / peak, 4),

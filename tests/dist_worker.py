@@ -9,8 +9,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CASES = [("RMAT(12,8,1)", 64, 16, "f64"), ("RMAT(14,8,2)", 256, 128, "f32"), ("GRID(128,1)", 256, 32, "f64"),
-         ("TREE(5000,3)", 16, 8, "f64"), ("RMAT(10,4,3)", 1024, 4, "f64")]
+# (graph, b, widths used in successive calls, dtype): the width changes between calls re-allocate
+# (and, for the P2P transport, re-share) the workspaces; every call uses a fresh X
+CASES = [("RMAT(12,8,1)", 64, (16, 16, 16), "f64"), ("RMAT(14,8,2)", 256, (128, 128, 128), "f32"),
+         ("RMAT(13,8,4)", 128, (64, 128, 64), "f64"), ("RMAT(13,8,5)", 512, (32, 64, 32), "f32"),
+         ("GRID(128,1)", 256, (32, 32), "f64"), ("TREE(5000,3)", 16, (8, 8), "f64"),
+         ("RMAT(10,4,3)", 1024, (4, 4), "f64"), ("PATH(3000,1)", 8, (3, 5), "f64")]
 
 
 def run(rank, world, port):
@@ -27,26 +31,26 @@ def run(rank, world, port):
     dist.broadcast_object_list(uid, src=0)
     comm = ab.Comm(world, rank, uid[0])
     fails = []
-    for spec, b, k, dtype in CASES:
+    for spec, b, ks, dtype in CASES:
         g = datagen.make_graph(spec)
-        X = datagen.make_x(g.n, k, dtype=np.float64 if dtype == "f64" else np.float32)
         plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, b, dtype=dtype, comm=comm)
         lo, hi = plan.local_begin, plan.local_end
         perm0 = plan.export_level(0)[0]
         rows = perm0[lo:hi]
-        Xl = torch.from_numpy(np.ascontiguousarray(X[rows])).cuda()
-        for rep in range(2):
+        for rep, k in enumerate(ks):
+            X = datagen.make_x(g.n, k, s_x=3 + rep, dtype=np.float64 if dtype == "f64" else np.float32)
+            Xl = torch.from_numpy(np.ascontiguousarray(X[rows])).cuda()
             Y = plan.spmm(Xl)
             torch.cuda.synchronize()
-        Y = Y.cpu().numpy().astype(np.float64)
-        ref = oracle.spmm_rows(g.row_ptr, g.col, g.val, X, rows)
-        if dtype == "f64":
-            ok = np.array_equal(Y, ref)
-        else:
-            den = np.linalg.norm(ref)
-            ok = (np.linalg.norm(Y - ref) / den if den > 0 else np.linalg.norm(Y)) <= 1e-4
-        if not ok:
-            fails.append(f"{spec} b={b} k={k} {dtype} rank {rank}: max err {np.abs(Y - ref).max()}")
+            Y = Y.cpu().numpy().astype(np.float64)
+            ref = oracle.spmm_rows(g.row_ptr, g.col, g.val, X, rows)
+            if dtype == "f64":
+                ok = np.array_equal(Y, ref)
+            else:
+                den = np.linalg.norm(ref)
+                ok = (np.linalg.norm(Y - ref) / den if den > 0 else np.linalg.norm(Y)) <= 1e-4
+            if not ok:
+                fails.append(f"{spec} b={b} k={k} call {rep} {dtype} rank {rank}: max err {np.abs(Y - ref).max()}")
         plan.close()
     comm.close()
     dist.destroy_process_group()
