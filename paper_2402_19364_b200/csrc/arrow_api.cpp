@@ -754,29 +754,8 @@ inline void prof_end(arrow_plan P, cudaStream_t st, int kid, cudaEvent_t a) {
 }
 }  // namespace
 
-arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void *stream) {
-    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
-    if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
-    if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
-    if (k == 0 || P->n == 0) return ARROW_OK;
-    const int64_t rows = P->local_end - P->local_begin;
-    // a rank of a distributed plan may own no rows but must still take part in the collectives
-    if ((!X || !Y) && !(P->dist && rows == 0)) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
-    int cur = 0;
-    CUDA_TRY(cudaGetDevice(&cur));
-    if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
-    if (k * (int64_t)P->esize() >= ((int64_t)1 << 32)) return fail(ARROW_E_UNSUPPORTED, "row of X exceeds 4 GiB");
-    const int64_t bytes = rows * k * (int64_t)P->esize();
-    const char *xa = (const char *)X, *ya = (const char *)Y;
-    if (rows > 0 && xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (P->dist) return dist_spmm(P, X, Y, k, st);
+static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st) {
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
-    if (P->levels.empty()) {
-        int e = launch_zero(Y, bytes, st);
-        if (e) return fail(ARROW_E_CUDA, cudaGetErrorString((cudaError_t)e));
-        return ARROW_OK;
-    }
     if (P->profiling) P->prof_acc.calls += 1;
     P->prof_pos = 0;
     CUDA_TRY(cudaMemsetAsync(P->counters, 0, P->levels.size() * sizeof(unsigned), st));
@@ -818,6 +797,67 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
     }
     return ARROW_OK;
+}
+
+arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void *stream) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
+    if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
+    if (k == 0 || P->n == 0) return ARROW_OK;
+    const int64_t rows = P->local_end - P->local_begin;
+    // a rank of a distributed plan may own no rows but must still take part in the collectives
+    if ((!X || !Y) && !(P->dist && rows == 0)) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
+    int cur = 0;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
+    if (k * (int64_t)P->esize() >= ((int64_t)1 << 32)) return fail(ARROW_E_UNSUPPORTED, "row of X exceeds 4 GiB");
+    const int64_t bytes = rows * k * (int64_t)P->esize();
+    const char *xa = (const char *)X, *ya = (const char *)Y;
+    if (rows > 0 && xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (P->dist) return dist_spmm(P, X, Y, k, st);
+    const int dt = P->dtype == ARROW_F64 ? 1 : 0;
+    if (P->levels.empty()) {
+        int e = launch_zero(Y, bytes, st);
+        if (e) return fail(ARROW_E_CUDA, cudaGetErrorString((cudaError_t)e));
+        return ARROW_OK;
+    }
+    // Single GPU: the whole call (memset + K-Z + one K-A launch per level) is captured once into a
+    // CUDA graph per (X, Y, k, stream) and replayed -- one launch instead of ~10 for the
+    // launch-bound small configs.  Off while profiling (per-kernel events) or on the legacy stream.
+    static const bool graphs = !(std::getenv("ARROW_GRAPHS") && std::getenv("ARROW_GRAPHS")[0] == '0');
+    if (graphs && !P->profiling && st != nullptr) {
+        if (P->gexec && P->g_x == X && P->g_y == Y && P->g_k == k && P->g_stream == st) {
+            CUDA_TRY(cudaGraphLaunch(P->gexec, st));
+            return ARROW_OK;
+        }
+        if (P->gexec) {
+            cudaGraphExecDestroy(P->gexec);
+            P->gexec = nullptr;
+        }
+        CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        arrow_status s = enqueue_single(P, X, Y, k, st);
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (s != ARROW_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return s;
+        }
+        if (ce != cudaSuccess) return fail(ARROW_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&P->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) {
+            P->gexec = nullptr;
+            return fail(ARROW_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+        }
+        P->g_x = X;
+        P->g_y = Y;
+        P->g_k = k;
+        P->g_stream = st;
+        CUDA_TRY(cudaGraphLaunch(P->gexec, st));
+        return ARROW_OK;
+    }
+    return enqueue_single(P, X, Y, k, st);
 }
 
 arrow_status arrow_spmm(arrow_plan plan, const void *X, void *Y, int64_t k) {

@@ -67,6 +67,12 @@ struct arrow_plan_s {
     // written on a side stream next to level 0 (HBM writes under an L2-bound kernel)
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // CUDA graph of the single-GPU call, keyed by (X, Y, k, stream)
+    cudaGraphExec_t gexec = nullptr;
+    const void *g_x = nullptr;
+    void *g_y = nullptr;
+    int64_t g_k = 0;
+    cudaStream_t g_stream = nullptr;
     bool poisoned = false;
     // profiling
     bool profiling = false;
@@ -88,6 +94,7 @@ struct arrow_plan_s {
         if (ws) cudaFree(ws);
         if (host_x) cudaFree(host_x);
         if (host_y) cudaFree(host_y);
+        if (gexec) cudaGraphExecDestroy(gexec);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (join_ev) cudaEventDestroy(join_ev);
         if (side) cudaStreamDestroy(side);

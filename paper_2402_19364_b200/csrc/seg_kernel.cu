@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 
 #include "arrow_internal.h"
 
@@ -414,6 +415,190 @@ int run_seg32_mode(int dist, const SegLevel &L, const void *X, const void *D0, v
                        : run_seg32<T, VEC, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st);
 }
 
+// ------------------------------------------------------------------------------------ K-A (short rows)
+// Rows of LPE < 32 lanes (k = 8/16/32 fp32 with 16-byte lanes): the warp still works on ONE batch,
+// and each step hands G = 32/LPE consecutive entries to its G sub-warps (one entry each), so a
+// warp instruction gathers G rows.  Sub-warps keep private partial sums while no segment ends in
+// a step; in a step with ends, the partials are folded (butterfly over the sub-warps), the step's
+// products are combined by a segmented inclusive scan across the sub-warps, and every sub-warp
+// whose entry closes a segment flushes that row -- several rows per step, in parallel.
+template <typename T, int VEC>
+__device__ __forceinline__ Frag<T, VEC> shfl_frag(const Frag<T, VEC> &f, int src_or_delta, int mode) {
+    Frag<T, VEC> r;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+        if (mode == 0) r.v[i] = __shfl_xor_sync(0xffffffffu, f.v[i], src_or_delta);
+        else r.v[i] = __shfl_up_sync(0xffffffffu, f.v[i], src_or_delta);
+    }
+    return r;
+}
+
+template <typename T, int VEC, int LPE, int MODE, int DIST, bool OFF32>
+__global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__ seg_out,
+                                                     const uint32_t *__restrict__ seg_end, int64_t nseg,
+                                                     const int32_t *__restrict__ ent_col,
+                                                     const T *__restrict__ ent_val, const T *__restrict__ X,
+                                                     const T *__restrict__ D0, T *__restrict__ Y, T *__restrict__ C0,
+                                                     int64_t k, unsigned *__restrict__ counter, int bseg,
+                                                     const PeerPtrs outs) {
+    constexpr int G = 32 / LPE;
+    constexpr int U = (32 / G) < 4 ? (32 / G) : 4;  // steps whose rows are loaded together
+    const int lane = threadIdx.x & 31;
+    const int q = lane / LPE;   // sub-warp: entry slot within a step
+    const int sl = lane % LPE;  // 16-byte slice of the row
+    const int64_t col0 = (int64_t)sl * VEC;
+    const uint32_t lane_off = (uint32_t)(col0 * (int64_t)sizeof(T));
+    const int64_t nbatch = (nseg + bseg - 1) / bseg;
+    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
+    const char *Xc = reinterpret_cast<const char *>(X);
+    const char *Dc = reinterpret_cast<const char *>(D0);
+
+    for (;;) {
+        unsigned wb = 0;
+        if (lane == 0) wb = atomicAdd(counter, 1u);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if ((int64_t)wb >= nbatch) break;
+        const int64_t s0 = (int64_t)wb * bseg;
+        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
+        const int32_t my_out = (lane < nb) ? __ldg(seg_out + s0 + lane) : 0;
+        const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+
+        Frag<T, VEC> acc;
+        acc.zero();
+        int cur = 0;  // segments of the batch closed so far
+        for (uint32_t cb = e_begin; cb < e_end; cb += 32) {
+            const int cnt = (e_end - cb < 32u) ? (int)(e_end - cb) : 32;
+            int32_t mycol = 0;
+            T myval = T(0);
+            if (lane < cnt) {
+                mycol = __ldcs(ent_col + cb + lane);
+                myval = __ldcs(ent_val + cb + lane);
+            }
+            const uint32_t rel = my_end - 1u - cb;
+            const unsigned endmask = __reduce_or_sync(0xffffffffu, (rel < 32u) ? (1u << rel) : 0u);
+#pragma unroll 1
+            for (int g0 = 0; g0 < cnt; g0 += G * U) {
+                // U steps' rows are requested before the first is used (memory-level parallelism)
+                Frag<T, VEC> xs[U];
+                T vals[U];
+#pragma unroll
+                for (int t = 0; t < U; ++t) {
+                    const int e = g0 + t * G + q;
+                    const int32_t col = __shfl_sync(0xffffffffu, mycol, e & 31);
+                    vals[t] = __shfl_sync(0xffffffffu, myval, e & 31);
+                    const char *p;
+                    if (DIST && col < 0) p = Dc + (uint64_t)((uint32_t)col & 0x7fffffffu) * rowbytes + lane_off;
+                    else if (OFF32) p = Xc + (uint32_t)((uint32_t)col * rowbytes + lane_off);
+                    else p = Xc + (uint64_t)(uint32_t)col * rowbytes + lane_off;
+                    if (e < cnt) xs[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
+                    else xs[t].zero();
+                }
+#pragma unroll
+                for (int t = 0; t < U; ++t) {
+                    const int u0 = g0 + t * G;
+                    if (u0 >= cnt) break;  // warp-uniform
+                    Frag<T, VEC> v;
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) v.v[i] = vals[t] * xs[t].v[i];
+                    const unsigned ends = (endmask >> u0) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
+                    if (ends == 0u) {  // warp-uniform: every entry of the step continues the open segment
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc.v[i] += v.v[i];
+                        continue;
+                    }
+                    if (__popc(ends) == 1) {  // warp-uniform, the common case: one segment closes at slot e
+                        const int e = __ffs(ends) - 1;
+                        // total = every partial + the products of slots <= e; slots > e open the next one
+                        Frag<T, VEC> w = acc;
+                        if (q <= e) {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) w.v[i] += v.v[i];
+                        }
+#pragma unroll
+                        for (int o = LPE; o < 32; o <<= 1) {
+                            const Frag<T, VEC> tt = shfl_frag<T, VEC>(w, o, 0);
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) w.v[i] += tt.v[i];
+                        }
+                        const int32_t o1 = __shfl_sync(0xffffffffu, my_out, cur & 31);
+                        if (q == 0) flush_row<T, VEC, MODE, DIST>(o1, w, Y, C0, k, col0, outs);
+                        cur += 1;
+                        if (q > e) acc = v;
+                        else acc.zero();
+                        continue;
+                    }
+                    // fold the sub-warps' partials of the open segment into slot 0's product
+#pragma unroll
+                    for (int o = LPE; o < 32; o <<= 1) {
+                        const Frag<T, VEC> tt = shfl_frag<T, VEC>(acc, o, 0);
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc.v[i] += tt.v[i];
+                    }
+                    if (q == 0) {
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) v.v[i] += acc.v[i];
+                    }
+                    // segmented inclusive scan over the G slots; slot q starts a segment if q-1 ended one
+                    bool f = q > 0 && ((ends >> (q - 1)) & 1u);
+#pragma unroll
+                    for (int d = 1; d < G; d <<= 1) {
+                        const Frag<T, VEC> tt = shfl_frag<T, VEC>(v, d * LPE, 1);
+                        const bool tf = __shfl_up_sync(0xffffffffu, f, d * LPE);
+                        if (q >= d && !f) {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) v.v[i] += tt.v[i];
+                            f = tf;
+                        }
+                    }
+                    // slots that close a segment flush it (segment index cur + closed ends before them)
+                    const bool closes = (ends >> q) & 1u;
+                    const int sidx = cur + __popc(ends & ((1u << q) - 1u));
+                    const int32_t o = __shfl_sync(0xffffffffu, my_out, sidx & 31);
+                    if (closes) flush_row<T, VEC, MODE, DIST>(o, v, Y, C0, k, col0, outs);
+                    cur += __popc(ends);
+                    // the open segment continues with the scanned value of the last valid slot
+                    const int last = min(G, cnt - u0) - 1;
+                    acc.zero();
+                    if (q == last && !closes) acc = v;
+                }
+            }
+        }
+    }
+}
+
+template <typename T, int VEC, int LPE, int MODE, int DIST>
+int run_segsmall(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
+                 unsigned *counter, const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    const int bseg = 32;
+    auto kern = off32 ? k_segsmall<T, VEC, LPE, MODE, DIST, true> : k_segsmall<T, VEC, LPE, MODE, DIST, false>;
+    static int bps[2] = {0, 0};
+    int &b = bps[off32 ? 1 : 0];
+    if (b == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
+        if (b <= 0) b = 1;
+    }
+    const int64_t nbatch = (L.nseg + bseg - 1) / bseg;
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (nbatch + 7) / 8);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
+                                           reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                           reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
+                                           reinterpret_cast<T *>(C0), k, counter, bseg, outs);
+    return (int)cudaGetLastError();
+}
+
+template <typename T, int VEC, int LPE>
+int run_segsmall_mode(int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
+                      int num_sms, unsigned *counter, const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    if (dist == 2) return run_segsmall<T, VEC, LPE, 0, 2>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st);
+    if (dist) return L.mode == 0 ? run_segsmall<T, VEC, LPE, 0, 1>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st)
+                                 : run_segsmall<T, VEC, LPE, 1, 1>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st);
+    return L.mode == 0 ? run_segsmall<T, VEC, LPE, 0, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st)
+                       : run_segsmall<T, VEC, LPE, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st);
+}
+
 template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segments(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
                  unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
@@ -464,6 +649,11 @@ int run_segments_mode(int lpe, int dist, const SegLevel &L, const void *X, const
 }  // namespace
 }  // namespace kseg
 
+static bool narrow_k32() {
+    static const bool v = std::getenv("ARROW_SEG_K32") && std::string(std::getenv("ARROW_SEG_K32")) == "narrow";
+    return v;
+}
+
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
                int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs) {
     using namespace kseg;
@@ -485,6 +675,24 @@ int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void
             return run_seg32_mode<float, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
         if (dtype == 1 && vec == 2)
             return run_seg32_mode<double, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
+    }
+    // short rows (k = 8/16/32 fp32 -- 32 one row per warp with ARROW_SEG_K32=narrow --, 4/8/16/32
+    // fp64 with 16-byte lanes): G entries per warp step,
+    // segmented scan across the sub-warps (ARROW_SEG_SMALL=0 disables)
+    static const bool small = !(std::getenv("ARROW_SEG_SMALL") && std::getenv("ARROW_SEG_SMALL")[0] == '0');
+    if (seg32 && small && lpe < 32 && lpe >= 2 && k == (int64_t)lpe * vec && vec == 16 / (dtype == 1 ? 8 : 4) &&
+        !(dtype == 0 && lpe == 8 && narrow_k32())) {
+        if (dtype == 0) {
+            if (lpe == 16) return run_segsmall_mode<float, 4, 16>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 8) return run_segsmall_mode<float, 4, 8>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 4) return run_segsmall_mode<float, 4, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            return run_segsmall_mode<float, 4, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+        } else {
+            if (lpe == 16) return run_segsmall_mode<double, 2, 16>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 8) return run_segsmall_mode<double, 2, 8>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 4) return run_segsmall_mode<double, 2, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            return run_segsmall_mode<double, 2, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+        }
     }
     // fp32 rows of 32 or 64 elements: one row per warp with 4- or 8-byte lanes (one 128/256-byte
     // request per entry) instead of 8/16-lane sub-warps that run different batches in lockstep
