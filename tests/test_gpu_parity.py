@@ -222,3 +222,21 @@ def test_config_R_sampled():
     Y64 = p64.spmm(torch.from_numpy(datagen.make_x(g.n, 128)).cuda())
     torch.cuda.synchronize()
     assert hashlib.sha256(Y64.cpu().numpy().astype("<f8").tobytes()).hexdigest() == inst["sha_y"]
+
+
+def test_graph_replay_on_a_stream():
+    """On a non-default stream a single-GPU call is captured once into a CUDA graph and replayed;
+    new X contents, a new Y buffer and a new k must all give the oracle's result (fp64, bitwise)."""
+    g = datagen.rmat(12, 8, 6)
+    plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, 128, dtype="f64")
+    s = torch.cuda.Stream()
+    for k, reps in ((16, 3), (8, 2), (16, 2)):
+        Y = torch.empty((g.n, k), dtype=torch.float64, device="cuda")
+        Xd = torch.empty((g.n, k), dtype=torch.float64, device="cuda")
+        for r in range(reps):
+            X = datagen.make_x(g.n, k, s_x=10 + r)
+            Xd.copy_(torch.from_numpy(X))
+            torch.cuda.synchronize()
+            plan.spmm(Xd, Y, stream=s)
+            s.synchronize()
+            assert np.array_equal(Y.cpu().numpy(), oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)), (k, r)
