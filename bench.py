@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order", default="original", choices=["original", "permuted"],
                     help="X/Y row order: original vertex ids, or pi_0 order (R18; forced when distributed)")
+    ap.add_argument("--iterate", type=int, default=10, help="iterations of the fused-ReLU iterate timing (0: skip)")
     ap.add_argument("--no-lib-baseline", action="store_true", help="skip the cuSPARSE (torch.sparse) comparator")
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
@@ -339,6 +340,23 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_baseline(g, X, k)
+    # NEXT-1: iterated X_{t+1} = relu(A X_t) with the activation fused into K-A (same plan, same X)
+    it = None
+    if world == 1 and args.iterate > 0:
+        Xi = Xd.clone()
+        Yi = torch.empty_like(Xd)
+        with torch.cuda.stream(stream):
+            plan.spmm_iterate(Xi, 2, "relu", Yi, stream=stream)
+            i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            Xi.copy_(Xd)
+            i0.record(stream)
+            plan.spmm_iterate(Xi, args.iterate, "relu", Yi, stream=stream)
+            i1.record(stream)
+        torch.cuda.synchronize()
+        ms_it = i0.elapsed_time(i1) / args.iterate
+        it = {"activation": "relu", "iters": args.iterate, "ms_per_iter": round(ms_it, 4),
+              "value": round(flop / (ms_it * 1e-3) / 1e9, 3), "unit": "GFLOP/s"}
+        del Xi, Yi
     lib = None
     if rank == 0 and world == 1 and not args.no_lib_baseline:
         lib = cusparse_baseline(g, Xd, k, flop, stream)
@@ -369,6 +387,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "library_baseline": lib,
+            "iterate": it,
             "create_seconds": round(info["create_seconds"], 2),
         }
         print(json.dumps(line), flush=True)

@@ -126,6 +126,20 @@ arrow_status arrow_spmm_ex(arrow_plan plan, const void *X, void *Y, int64_t k, v
  * Device staging buffers are owned by the plan and reused. */
 arrow_status arrow_spmm_host(arrow_plan plan, const void *X_host, void *Y_host, int64_t k, void *stream);
 
+/* Iterated SpMM with a fused activation (the paper's use case of repeated
+ * products with the rows left in pi_0 order):  X_{t+1} = act(A X_t), t = 0..iters-1.
+ * X and Y are both n x k device buffers of the plan's dtype (row order of the plan: original,
+ * or pi_0 with ARROW_ORDER_PERMUTED) and are used as a ping-pong pair: X holds X_0 on entry and
+ * both are overwritten; *result_in_y (may be NULL) is set to 1 if X_iters ends in Y (iters odd),
+ * 0 if it ends in X.  activation: ARROW_ACT_NONE or ARROW_ACT_RELU.  The activation is applied
+ * inside K-A when a row's last segment is flushed (kFinalBit, computed at plan time); rows last
+ * written by head-row partials get one small pass per iteration.  Single-GPU plans only
+ * (ARROW_E_UNSUPPORTED for distributed plans); iters < 1 or an unknown activation ->
+ * ARROW_E_INVALID_ARG; stream-ordered on `stream` (NULL = legacy default stream). */
+enum { ARROW_ACT_NONE = 0, ARROW_ACT_RELU = 1 };
+arrow_status arrow_spmm_iterate(arrow_plan plan, void *X, void *Y, int64_t k, int32_t iters, int32_t activation,
+                                void *stream, int32_t *result_in_y);
+
 /* Pre-size the k-dependent workspaces (head block D0, head accumulator C0) for k <= k_max so
  * that later arrow_spmm calls allocate nothing (CUDA-graph capture safe). */
 arrow_status arrow_plan_reserve(arrow_plan plan, int64_t k_max);

@@ -34,7 +34,7 @@ SYMBOLS = [
     "arrow_decomposition_export_level", "arrow_decomposition_export_residual", "arrow_decomposition_save",
     "arrow_decomposition_load", "arrow_decomposition_destroy", "arrow_plan_create_from", "arrow_comm_unique_id",
     "arrow_comm_create", "arrow_comm_destroy", "arrow_status_string", "arrow_last_error", "arrow_abi_version",
-    "arrow_dist_schedule",
+    "arrow_dist_schedule", "arrow_spmm_iterate",
 ]
 
 
@@ -118,6 +118,7 @@ def lib() -> ctypes.CDLL:
             "arrow_comm_create": [i32, i32, p, p],
             "arrow_comm_destroy": [p],
             "arrow_dist_schedule": [p, i32, i32, i64, i32, p, p],
+            "arrow_spmm_iterate": [p, p, p, i64, i32, i32, p, p],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -372,6 +373,22 @@ class Plan:
         s = (stream or torch.cuda.current_stream(X.device)).cuda_stream
         self.spmm_ptr(xp, yp, k, s)
         return Y
+
+    def spmm_iterate(self, X, iters: int, activation: str = "relu", Y=None, stream=None):
+        """X_{t+1} = act(A X_t) for t < iters (arrow_spmm_iterate).  X (device tensor, n x k) holds
+        X_0 and is overwritten, as is Y (allocated if None); returns the tensor that holds X_iters."""
+        import torch
+        rows = self.local_end - self.local_begin
+        k = X.shape[1]
+        if Y is None:
+            Y = torch.empty((rows, k), dtype=X.dtype, device=X.device)
+        xp = _torch_ptr(X, self.dtype_code, rows, k)
+        yp = _torch_ptr(Y, self.dtype_code, rows, k)
+        act = {"none": 0, "relu": 1}[activation]
+        s = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        in_y = ctypes.c_int32()
+        _check(lib().arrow_spmm_iterate(self._h, xp, yp, k, iters, act, s, ctypes.byref(in_y)), "arrow_spmm_iterate")
+        return Y if in_y.value else X
 
     def spmm_host(self, X: np.ndarray, Y: Optional[np.ndarray] = None, stream_ptr: int = 0) -> np.ndarray:
         """End-to-end call with host buffers (H2D, kernels, D2H inside arrow_spmm_host)."""

@@ -467,6 +467,18 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         if (use_seg) {
             if (const char *b2 = std::getenv("ARROW_SEG_BS")) P->seg_bseg = std::atoi(b2);
             const size_t es = P->esize();
+            // last launch that writes each Y row: 2*launch + (1 if as a head-row partial); a body
+            // segment in its row's last launch is marked final (kFinalBit, arrow_spmm_iterate
+            // applies the activation when it is flushed); rows last written by head partials are
+            // listed for a post pass
+            std::vector<int32_t> last((size_t)P->n, -1);
+            for (size_t li = 0; li < built.size(); ++li)
+                for (const uint32_t key : built[li].keys)
+                    if (key & kPseudoRec) last[key & (kAuxRec - 1)] = (int32_t)(2 * li + ((key & kAuxRec) ? 1 : 0));
+            std::vector<int32_t> post_rows;
+            for (int64_t r = 0; r < P->n; ++r)
+                if (last[r] >= 0 && (last[r] & 1)) post_rows.push_back((int32_t)r);
+            size_t li = 0;
             for (const BuiltLevel &B : built) {
                 std::vector<int32_t> so, ec;
                 std::vector<uint32_t> se;
@@ -475,7 +487,9 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
                 for (size_t r = 0; r < B.keys.size(); ++r) {
                     const uint32_t key = B.keys[r];
                     if (key & kPseudoRec) {
-                        so.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (key & (kAuxRec - 1))));
+                        const uint32_t row = key & (kAuxRec - 1);
+                        const bool fin = !(key & kAuxRec) && last[row] == (int32_t)(2 * li);
+                        so.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (fin ? kFinalBit : 0u) | row));
                         se.push_back((uint32_t)ec.size());
                     } else {
                         ec.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (key & (kAuxRec - 1))));
@@ -500,6 +514,13 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
                 if (!S.seg_out || !S.seg_end || !S.ent_col || !S.ent_val)
                     return fail(ARROW_E_CUDA, "cudaMalloc(seg layout)");
                 P->seg.push_back(S);
+                ++li;
+            }
+            P->n_post = (int64_t)post_rows.size();
+            if (P->n_post) {
+                if (cudaMalloc(&P->post_rows, post_rows.size() * 4) != cudaSuccess)
+                    return fail(ARROW_E_CUDA, "cudaMalloc(post rows)");
+                cudaMemcpy(P->post_rows, post_rows.data(), post_rows.size() * 4, cudaMemcpyHostToDevice);
             }
         }
     }
@@ -754,7 +775,7 @@ inline void prof_end(arrow_plan P, cudaStream_t st, int kid, cudaEvent_t a) {
 }
 }  // namespace
 
-static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st) {
+static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st, int act = 0) {
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
     if (P->profiling) P->prof_acc.calls += 1;
     P->prof_pos = 0;
@@ -789,12 +810,17 @@ static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t
         }
         prof_begin(P, st, a);
         if (!P->seg.empty())
-            e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->seg_bseg, st);
+            e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->seg_bseg, st,
+                           nullptr, act);
         else
             e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (!joined) CUDA_TRY(cudaStreamWaitEvent(st, P->join_ev, 0));
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
+    }
+    if (act && P->n_post) {  // iterate mode: rows last written by head-row partials
+        const int e = launch_act_rows(dt, P->post_rows, P->n_post, k, act, Y, st);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("activation pass: ") + cudaGetErrorString((cudaError_t)e)); }
     }
     return ARROW_OK;
 }
@@ -863,6 +889,39 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
 arrow_status arrow_spmm(arrow_plan plan, const void *X, void *Y, int64_t k) {
     if (!plan) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
     return arrow_spmm_ex(plan, X, Y, k, plan->stream);
+}
+
+arrow_status arrow_spmm_iterate(arrow_plan P, void *X, void *Y, int64_t k, int32_t iters, int32_t activation,
+                                void *stream, int32_t *result_in_y) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
+    if (iters < 1) return fail(ARROW_E_INVALID_ARG, "iters < 1");
+    if (activation < ARROW_ACT_NONE || activation > ARROW_ACT_RELU) return fail(ARROW_E_INVALID_ARG, "unknown activation");
+    if (P->dist) return fail(ARROW_E_UNSUPPORTED, "arrow_spmm_iterate: distributed plans are not supported");
+    if (P->seg.empty() && !P->levels.empty())
+        return fail(ARROW_E_UNSUPPORTED, "arrow_spmm_iterate needs the segment-descriptor layout (default)");
+    if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
+    if (result_in_y) *result_in_y = (iters & 1) ? 1 : 0;
+    if (k == 0 || P->n == 0) return ARROW_OK;
+    if (!X || !Y) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
+    const int64_t bytes = P->n * k * (int64_t)P->esize();
+    const char *xa = (const char *)X, *ya = (const char *)Y;
+    if (xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
+    int cur = 0;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    for (int32_t t = 0; t < iters; ++t) {  // X_{t+1} = act(A X_t), ping-pong between X and Y
+        const void *src = (t & 1) ? Y : X;
+        void *dst = (t & 1) ? X : Y;
+        if (P->levels.empty()) {
+            CUDA_TRY(cudaMemsetAsync(dst, 0, (size_t)bytes, st));
+            continue;
+        }
+        arrow_status s = enqueue_single(P, src, dst, k, st, activation);
+        if (s != ARROW_OK) return s;
+    }
+    return ARROW_OK;
 }
 
 arrow_status arrow_spmm_host(arrow_plan P, const void *Xh, void *Yh, int64_t k, void *stream) {

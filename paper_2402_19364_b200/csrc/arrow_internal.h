@@ -81,12 +81,19 @@ constexpr uint32_t kParityBit = 0x40000000u;
 constexpr uint32_t kLocalRmwBit = 0x40000000u;  // K-A (dist 2): out row is a local Y row, read-modify-written
 struct PeerPtrs {
     void *p[kMaxPeers];
+    int act = 0;  // K-A only: activation applied when a row's final segment is flushed (iterate mode)
 };
+// single GPU: a body segment whose row receives no later contribution (arrow_spmm_iterate's
+// activation is applied when it is flushed); activations: 0 identity, 1 ReLU
+constexpr uint32_t kFinalBit = 0x40000000u;
+constexpr uint32_t kRowMask30 = 0x3fffffffu;
 // dist: 0 single GPU, 1 distributed (head columns from D0, head partials into C0), 2 as 1 with
 // body rows stored through `outs` (encoded rows, levels >= 1 of the P2P transport) or, with
 // kLocalRmwBit, added into Y (rows whose home is this rank)
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs = nullptr);
+               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs = nullptr, int act = 0);
+// Y[rows[i]] = act(Y[rows[i]]) (rows whose last contribution is a head-row partial)
+int launch_act_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, int act, void *Y, void *stream);
 // dst row enc(didx[i]) of bases = src[sidx[i]] (sidx < 0: zero); grid of `blocks` (0: sized to n)
 int launch_push_rows(int dtype, const void *src, const int32_t *sidx, const int32_t *didx, int64_t n, int64_t k,
                      const PeerPtrs &bases, int blocks, void *stream);

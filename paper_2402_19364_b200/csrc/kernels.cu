@@ -482,6 +482,40 @@ int launch_barrier(const PeerPtrs &flags, const unsigned *mine, int slot, unsign
     return (int)cudaGetLastError();
 }
 
+namespace {
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_act_rows(const int32_t *__restrict__ rows, int64_t nrows, int64_t k, int act,
+                                                  T *__restrict__ Y) {
+    const int64_t kv = k / VEC, total = nrows * kv;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / kv, c = (t - j * kv) * VEC;
+        T *p = Y + (int64_t)__ldg(rows + j) * k + c;
+        Frag<T, VEC> y = ld_plain<T, VEC>(p);
+        if (act == 1) {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) y.v[i] = y.v[i] > T(0) ? y.v[i] : T(0);
+        }
+        st_plain<T, VEC>(p, y);
+    }
+}
+}  // namespace
+
+int launch_act_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, int act, void *Y, void *stream) {
+    if (nrows == 0 || k == 0 || act == 0) return 0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int vec = pick_vec(dtype, k, {Y});
+    const unsigned g = grid_for(nrows * (k / vec));
+    if (dtype == 0) {
+        if (vec == 4) k_act_rows<float, 4><<<g, 256, 0, st>>>(rows, nrows, k, act, (float *)Y);
+        else if (vec == 2) k_act_rows<float, 2><<<g, 256, 0, st>>>(rows, nrows, k, act, (float *)Y);
+        else k_act_rows<float, 1><<<g, 256, 0, st>>>(rows, nrows, k, act, (float *)Y);
+    } else {
+        if (vec == 2) k_act_rows<double, 2><<<g, 256, 0, st>>>(rows, nrows, k, act, (double *)Y);
+        else k_act_rows<double, 1><<<g, 256, 0, st>>>(rows, nrows, k, act, (double *)Y);
+    }
+    return (int)cudaGetLastError();
+}
+
 int launch_gather_add(int dtype, const void *src, const int32_t *ptr, const int32_t *sidx, const int32_t *drow,
                       int64_t n, int64_t k, void *dst, void *stream) {
     if (n == 0 || k == 0) return 0;

@@ -54,7 +54,9 @@ struct arrow_plan_s {
     // device memory
     void *arena = nullptr;
     int64_t arena_bytes = 0;
-    std::vector<SegLevel> seg;     // optional descriptor layout (ARROW_SEG=1) for the v2 kernel
+    std::vector<SegLevel> seg;     // segment-descriptor layout of the K-A kernels (default)
+    int32_t *post_rows = nullptr;  // rows last written by a head-row partial (iterate's activation pass)
+    int64_t n_post = 0;
     std::vector<void *> seg_allocs;
     int seg_bseg = 16;
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
@@ -95,6 +97,7 @@ struct arrow_plan_s {
         if (host_x) cudaFree(host_x);
         if (host_y) cudaFree(host_y);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (post_rows) cudaFree(post_rows);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (join_ev) cudaEventDestroy(join_ev);
         if (side) cudaStreamDestroy(side);

@@ -77,6 +77,14 @@ __device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
     }
 }
 
+template <typename T, int VEC>
+__device__ __forceinline__ void apply_act(Frag<T, VEC> &f, int act) {
+    if (act == 1) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) f.v[i] = f.v[i] > T(0) ? f.v[i] : T(0);
+    }
+}
+
 // ------------------------------------------------------------------------------------ K-A
 // Segment stream.  A sub-warp of LPE lanes owns a row slab of LPE*VEC elements.  Work is a list
 // of non-empty segments in tile-window order, cut into batches of LPE consecutive segments.
@@ -181,14 +189,18 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
                                 } else if (DIST == 2) {
                                     T *base = reinterpret_cast<T *>(outs.p[(uint32_t)o >> kPeerShift]);
                                     st_stream<T, VEC>(base + (int64_t)(o & kPeerRowMask) * k + col0, acc);
-                                } else if (MODE == 0) {
-                                    st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
                                 } else {
-                                    T *py = Y + (int64_t)o * k + col0;
-                                    Frag<T, VEC> y = ld_plain<T, VEC>(py);
+                                    const bool fin = DIST == 0 && (o & kFinalBit) && outs.act;
+                                    T *py = Y + (int64_t)(DIST == 0 ? (o & kRowMask30) : o) * k + col0;
+                                    Frag<T, VEC> y = acc;
+                                    if (MODE != 0) {
+                                        y = ld_plain<T, VEC>(py);
 #pragma unroll
-                                    for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
-                                    st_plain<T, VEC>(py, y);
+                                        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                    }
+                                    if (fin) apply_act<T, VEC>(y, outs.act);
+                                    if (MODE == 0) st_stream<T, VEC>(py, y);
+                                    else st_plain<T, VEC>(py, y);
                                 }
                             }
                             acc.zero();
@@ -246,14 +258,19 @@ __device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T 
     } else if (DIST == 2) {
         T *base = reinterpret_cast<T *>(outs.p[(uint32_t)o >> kPeerShift]);
         st_stream<T, VEC>(base + (int64_t)(o & kPeerRowMask) * k + col0, acc);
-    } else if (MODE == 0) {
-        st_stream<T, VEC>(Y + (int64_t)o * k + col0, acc);
     } else {
-        T *py = Y + (int64_t)o * k + col0;
-        Frag<T, VEC> y = ld_plain<T, VEC>(py);
+        // single GPU: bit 30 marks the row's final segment (iterate mode applies the activation)
+        const bool fin = DIST == 0 && (o & kFinalBit) && outs.act;
+        T *py = Y + (int64_t)(DIST == 0 ? (o & kRowMask30) : o) * k + col0;
+        Frag<T, VEC> y = acc;
+        if (MODE != 0) {
+            y = ld_plain<T, VEC>(py);
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
-        st_plain<T, VEC>(py, y);
+            for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+        }
+        if (fin) apply_act<T, VEC>(y, outs.act);
+        if (MODE == 0) st_stream<T, VEC>(py, y);
+        else st_plain<T, VEC>(py, y);
     }
 }
 
@@ -655,12 +672,13 @@ static bool narrow_k32() {
 }
 
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs) {
+               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs, int act) {
     using namespace kseg;
     if (L.nseg == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     PeerPtrs po{};
     if (outs) po = *outs;
+    po.act = act;
     if (dist == 2 && !outs) return (int)cudaErrorInvalidValue;
     int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
     if (dist == 2)

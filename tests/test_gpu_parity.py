@@ -240,3 +240,39 @@ def test_graph_replay_on_a_stream():
             plan.spmm(Xd, Y, stream=s)
             s.synchronize()
             assert np.array_equal(Y.cpu().numpy(), oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)), (k, r)
+
+
+@pytest.mark.parametrize("order", ["original", "permuted"])
+def test_iterate_relu(order):
+    """NEXT-1: X_{t+1} = relu(A X_t) with the activation fused into K-A, against the oracle applied
+    step by step (fp64; one iteration is exact on dyadic data, more within 1e-12)."""
+    g = datagen.rmat(13, 8, 7)
+    rng = np.random.default_rng(5)
+    # signed values so that ReLU is not the identity: a(u,v) -> +-a(u,v), symmetric
+    S = g.to_scipy().tocoo()
+    sign = np.where(((S.row.astype(np.int64) * 1315423911 + S.col) ^ (S.col.astype(np.int64) * 1315423911 + S.row)) & 4, -1.0, 1.0)
+    S.data = S.data * sign
+    S = S.tocsr()
+    S.sort_indices()
+    plan = ab.Plan(g.n, S.indptr, S.indices, S.data, 128, dtype="f64", order=order)
+    perm0 = plan.export_level(0)[0] if order == "permuted" else np.arange(g.n)
+    k = 16
+    X0 = datagen.make_x(g.n, k) - 0.5
+    for iters, exact in ((1, True), (2, False), (4, False)):
+        ref = X0.copy()
+        for _ in range(iters):
+            ref = np.maximum(oracle.spmm(g.n, S.indptr, S.indices, S.data, ref), 0.0)
+        Xd = torch.from_numpy(np.ascontiguousarray(X0[perm0])).cuda()
+        out = plan.spmm_iterate(Xd, iters, "relu")
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        want = ref[perm0]
+        if exact:
+            assert np.array_equal(got, want), (iters, np.abs(got - want).max())
+        else:
+            assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-12
+    # identity activation == repeated arrow_spmm
+    Xd = torch.from_numpy(np.ascontiguousarray(X0[perm0])).cuda()
+    out = plan.spmm_iterate(Xd, 1, "none")
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.spmm(g.n, S.indptr, S.indices, S.data, X0)[perm0])
