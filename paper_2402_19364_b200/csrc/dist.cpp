@@ -176,6 +176,8 @@ std::vector<int64_t> split_tiles(const std::vector<int64_t> &cost, int G) {
     for (int g = 1; g < G; ++g) {
         const double target = (double)pre[T] * g / G;
         tb[g] = std::lower_bound(pre.begin(), pre.end(), (int64_t)target) - pre.begin();
+        // the boundary whose prefix cost is nearest the target (lower_bound alone favours the left)
+        if (tb[g] > 0 && tb[g] <= T && target - (double)pre[tb[g] - 1] < (double)pre[tb[g]] - target) tb[g] -= 1;
         tb[g] = std::min(std::max(tb[g], tb[g - 1]), T);
     }
     return tb;
@@ -246,15 +248,24 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     };
 
     // ---- pass 1: tile split and per-peer counts of every level
+    // level i >= 1: contiguous chunks c of tiles [tbs[i][c], tbs[i][c+1]); chunk c goes to rank
+    // rk[i][c] (cr[i][g] = chunk of rank g): per level the heaviest chunk goes to the rank with the
+    // least work so far over the previous levels (LPT), so per-level rounding does not pile up
     std::vector<std::vector<int64_t>> tbs(nl);
+    std::vector<std::vector<int>> rk(nl), cr(nl);
+    std::vector<int64_t> load(G, 0);
     auto range = [&](int i, int g, int64_t &qa, int64_t &qb) {
         const int64_t n_i = D.levels[i].n_i;
         if (i == 0) { qa = std::min(los[g], n_i); qb = std::min(los[g + 1], n_i); }
-        else { qa = std::min<int64_t>(n_i, tbs[i][g] * b); qb = std::min<int64_t>(n_i, tbs[i][g + 1] * b); }
+        else {
+            const int c = cr[i][g];
+            qa = std::min<int64_t>(n_i, tbs[i][c] * b);
+            qb = std::min<int64_t>(n_i, tbs[i][c + 1] * b);
+        }
     };
     auto tile_owner = [&](int i, int64_t q) -> int {
         if (i == 0) return owner(q);
-        return (int)(std::upper_bound(tbs[i].begin() + 1, tbs[i].end() - 1, q / b) - (tbs[i].begin() + 1));
+        return rk[i][std::upper_bound(tbs[i].begin() + 1, tbs[i].end() - 1, q / b) - (tbs[i].begin() + 1)];
     };
     H.L.resize(nl);
     // RC / OC[i][t * G + h]: rows (all / with entries) of rank t's level-i tiles whose home is h
@@ -267,7 +278,24 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         DistHostLevel &DL = H.L[i];
         DL.h = L.head;
         if (i == 0) continue;
-        tbs[i] = split_tiles(tile_costs(L, b), G);
+        {
+            const std::vector<int64_t> cost = tile_costs(L, b);
+            tbs[i] = split_tiles(cost, G);
+            std::vector<int64_t> cc(G, 0);
+            for (int c = 0; c < G; ++c)
+                for (int64_t t = tbs[i][c]; t < tbs[i][c + 1]; ++t) cc[c] += cost[t];
+            std::vector<int> co(G), ro(G);
+            for (int c = 0; c < G; ++c) co[c] = ro[c] = c;
+            std::stable_sort(co.begin(), co.end(), [&](int a, int z) { return cc[a] > cc[z]; });
+            std::stable_sort(ro.begin(), ro.end(), [&](int a, int z) { return load[a] < load[z]; });
+            rk[i].assign(G, 0);
+            cr[i].assign(G, 0);
+            for (int j = 0; j < G; ++j) {
+                rk[i][co[j]] = ro[j];
+                cr[i][ro[j]] = co[j];
+                load[ro[j]] += cc[co[j]];
+            }
+        }
         int64_t qa, qb;
         range(i, me, qa, qb);
         const int64_t h = L.head, ha = std::max(h, qa);
