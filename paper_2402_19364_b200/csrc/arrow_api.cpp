@@ -230,6 +230,94 @@ arrow_status validate_args(const arrow_csr *A, int64_t b, int32_t levels) {
 }  // namespace
 
 // ------------------------------------------------------------------------------------ ABI
+
+// Single GPU, "staged tail": the levels >= 1 run as ONE launch, concurrently with level 0 (which
+// is bound by the L1/TEX data pipe while the tail is latency-bound), writing each body row into
+// its own staging row (plain stores, no read-modify-write) and each head-row partial into a
+// per-(level, head) staging row (atomics); one CSR gather-add then adds every staged row into
+// Y in level order.  Segment lists are concatenated level by level (window order inside each).
+static arrow_status build_stage_tail(arrow_plan P, const std::vector<std::vector<int32_t>> &so,
+                                     const std::vector<std::vector<uint32_t>> &se,
+                                     const std::vector<std::vector<int32_t>> &ec,
+                                     const std::vector<std::vector<uint8_t>> &ev) {
+    const int nl = (int)so.size();
+    // staging rows: one per (level, head row) for the head partials (zeroed every call), then one
+    // per (level, body row)
+    std::vector<int32_t> stamp((size_t)P->n, -1), hidx((size_t)P->n, -1), hrow;
+    for (int i = 0; i < nl; ++i)
+        for (int32_t o : so[i])
+            if (o < 0) {
+                const int32_t r = o & 0x7fffffff;
+                if (stamp[r] != i) { stamp[r] = i; hrow.push_back(r); }
+            }
+    const int64_t nhead = (int64_t)hrow.size();
+    std::fill(stamp.begin(), stamp.end(), -1);
+    std::vector<int32_t> mso, mec;
+    std::vector<uint32_t> mse;
+    std::vector<uint8_t> mev;
+    std::vector<std::pair<int32_t, int32_t>> contrib;  // (Y row, staging row), level order
+    int64_t nbody = 0, ebase = 0, nh = 0;
+    for (int i = 0; i < nl; ++i) {
+        for (size_t t = 0; t < so[i].size(); ++t) {
+            const int32_t o = so[i][t];
+            if (o < 0) {  // head-row partial of one window: atomically into its (level, row) staging row
+                const int32_t r = o & 0x7fffffff;
+                if (stamp[r] != i) { stamp[r] = i; hidx[r] = (int32_t)nh++; }
+                mso.push_back((int32_t)(kFlag | (uint32_t)hidx[r]));
+            } else {  // body row: stored into its own staging row
+                const int32_t sr = (int32_t)(nhead + nbody++);
+                mso.push_back(sr);
+                contrib.emplace_back((int32_t)(o & (int32_t)kRowMask30), sr);
+            }
+            mse.push_back((uint32_t)(ebase + se[i][t]));
+        }
+        mec.insert(mec.end(), ec[i].begin(), ec[i].end());
+        mev.insert(mev.end(), ev[i].begin(), ev[i].end());
+        ebase += (int64_t)ec[i].size();
+    }
+    for (int64_t h = 0; h < nhead; ++h) contrib.emplace_back(hrow[h], (int32_t)h);
+    if (ebase >= ((int64_t)1 << 32)) return fail(ARROW_E_UNSUPPORTED, "staged tail exceeds 2^32 entries");
+    if (nhead + nbody >= ((int64_t)1 << 30)) return fail(ARROW_E_UNSUPPORTED, "staged tail exceeds 2^30 rows");
+    // CSR of contributions by Y row; within a row: body rows in level order, then head partials
+    std::stable_sort(contrib.begin(), contrib.end(),
+                     [](const std::pair<int32_t, int32_t> &a, const std::pair<int32_t, int32_t> &b) { return a.first < b.first; });
+    std::vector<int32_t> ptr(1, 0), src, dst;
+    for (const auto &c : contrib) {
+        if (dst.empty() || dst.back() != c.first) {
+            if (!dst.empty()) ptr.push_back((int32_t)src.size());
+            dst.push_back(c.first);
+        }
+        src.push_back(c.second);
+    }
+    if (!dst.empty()) ptr.push_back((int32_t)src.size());
+    auto up = [&](const void *data, size_t bytes) -> void * {
+        void *d = nullptr;
+        if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+        P->seg_allocs.push_back(d);
+        if (bytes) cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice);
+        return d;
+    };
+    SegLevel T;
+    T.nseg = (int64_t)mso.size();
+    T.mode = 0;
+    T.max_x_row = P->n;
+    T.seg_out = (int32_t *)up(mso.data(), mso.size() * 4);
+    T.seg_end = (uint32_t *)up(mse.data(), mse.size() * 4);
+    T.ent_col = (int32_t *)up(mec.data(), mec.size() * 4);
+    T.ent_val = up(mev.data(), mev.size());
+    P->tail_ptr = (int32_t *)up(ptr.data(), ptr.size() * 4);
+    P->tail_src = (int32_t *)up(src.data(), src.size() * 4);
+    P->tail_dst = (int32_t *)up(dst.data(), dst.size() * 4);
+    if (!T.seg_out || !T.seg_end || !T.ent_col || !T.ent_val || !P->tail_ptr || !P->tail_src || !P->tail_dst)
+        return fail(ARROW_E_CUDA, "cudaMalloc(staged tail)");
+    P->tail = T;
+    P->tail_on = true;
+    P->tail_nhead = nhead;
+    P->tail_rows = nhead + nbody;
+    P->tail_ndst = (int64_t)dst.size();
+    return ARROW_OK;
+}
+
 extern "C" {
 
 const char *arrow_status_string(arrow_status s) {
@@ -475,6 +563,14 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
             for (size_t li = 0; li < built.size(); ++li)
                 for (const uint32_t key : built[li].keys)
                     if (key & kPseudoRec) last[key & (kAuxRec - 1)] = (int32_t)(2 * li + ((key & kAuxRec) ? 1 : 0));
+            // levels >= 1 as one staged launch next to level 0 (ARROW_TAIL=stage; see build_stage_tail).
+            // Measured at config R: level 0 + tail 2.70 ms together (vs 2.84 ms in sequence) but the
+            // final gather-add costs 0.47 ms -- off by default.
+            const char *tenv = std::getenv("ARROW_TAIL");
+            const bool stage_tail = built.size() > 2 && tenv && std::string(tenv) == "stage";
+            std::vector<std::vector<int32_t>> tail_so, tail_ec;
+            std::vector<std::vector<uint32_t>> tail_se;
+            std::vector<std::vector<uint8_t>> tail_ev;
             std::vector<int32_t> post_rows;
             for (int64_t r = 0; r < P->n; ++r)
                 if (last[r] >= 0 && (last[r] & 1)) post_rows.push_back((int32_t)r);
@@ -514,7 +610,17 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
                 if (!S.seg_out || !S.seg_end || !S.ent_col || !S.ent_val)
                     return fail(ARROW_E_CUDA, "cudaMalloc(seg layout)");
                 P->seg.push_back(S);
+                if (stage_tail && li > 0) {
+                    tail_so.push_back(std::move(so));
+                    tail_se.push_back(std::move(se));
+                    tail_ec.push_back(std::move(ec));
+                    tail_ev.push_back(std::move(ev));
+                }
                 ++li;
+            }
+            if (stage_tail) {
+                arrow_status st2 = build_stage_tail(P.get(), tail_so, tail_se, tail_ec, tail_ev);
+                if (st2 != ARROW_OK) return st2;
             }
             P->n_post = (int64_t)post_rows.size();
             if (P->n_post) {
@@ -780,6 +886,42 @@ static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t
     if (P->profiling) P->prof_acc.calls += 1;
     P->prof_pos = 0;
     CUDA_TRY(cudaMemsetAsync(P->counters, 0, P->levels.size() * sizeof(unsigned), st));
+    if (P->tail_on && act == 0 && P->stage && P->stage_k >= k) {
+        // K-Z, then level 0 (main stream) next to the staged tail (side stream), then the gather-add
+        const DeviceLevel &L0 = P->levels[0];
+        const size_t es = P->esize();
+        cudaEvent_t a = nullptr, a2 = nullptr;
+        int e = 0;
+        if (L0.nzero > 0) {
+            prof_begin(P, st, a);
+            e = launch_zero_rows(dt, L0.zero_rows, L0.nzero, k, Y, st);
+            prof_end(P, st, ARROW_K_HEAD_STAGE, a);
+            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
+        }
+        if (!P->side) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&P->join_ev, cudaEventDisableTiming));
+        }
+        static const int tail_sms_env = std::getenv("ARROW_TAIL_SMS") ? std::atoi(std::getenv("ARROW_TAIL_SMS")) : 0;
+        const int tail_sms = tail_sms_env > 0 ? tail_sms_env : std::max(1, P->num_sms / 4);
+        prof_begin(P, st, a2);  // K-A: from the fork to the join (level 0 and the tail run together)
+        CUDA_TRY(cudaEventRecord(P->fork_ev, st));
+        CUDA_TRY(cudaStreamWaitEvent(P->side, P->fork_ev, 0));
+        CUDA_TRY(cudaMemsetAsync(P->stage, 0, (size_t)P->tail_nhead * k * es, P->side));
+        e = launch_seg(dt, 0, P->tail, X, nullptr, P->stage, nullptr, k, tail_sms, P->counters + 1, P->seg_bseg, P->side);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A tail: ") + cudaGetErrorString((cudaError_t)e)); }
+        CUDA_TRY(cudaEventRecord(P->join_ev, P->side));
+        e = launch_seg(dt, 0, P->seg[0], X, nullptr, Y, nullptr, k, P->num_sms, P->counters, P->seg_bseg, st);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
+        CUDA_TRY(cudaStreamWaitEvent(st, P->join_ev, 0));
+        prof_end(P, st, ARROW_K_SEGMENTS, a2);
+        prof_begin(P, st, a);
+        e = launch_gather_add(dt, P->stage, P->tail_ptr, P->tail_src, P->tail_dst, P->tail_ndst, k, Y, st);
+        prof_end(P, st, ARROW_K_HEAD_EPI, a);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("tail add: ") + cudaGetErrorString((cudaError_t)e)); }
+        return ARROW_OK;
+    }
     for (size_t i = 0; i < P->levels.size(); ++i) {
         const DeviceLevel &L = P->levels[i];
         cudaEvent_t a = nullptr;
@@ -851,6 +993,14 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     // Single GPU: the whole call (memset + K-Z + one K-A launch per level) is captured once into a
     // CUDA graph per (X, Y, k, stream) and replayed -- one launch instead of ~10 for the
     // launch-bound small configs.  Off while profiling (per-kernel events) or on the legacy stream.
+    if (P->tail_on && P->stage_k < k) {  // staging rows of the staged tail (allocated outside any capture)
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (P->stage) cudaFree(P->stage);
+        P->stage = nullptr;
+        P->stage_k = 0;
+        CUDA_TRY(cudaMalloc(&P->stage, (size_t)std::max<int64_t>(P->tail_rows, 1) * k * P->esize()));
+        P->stage_k = k;
+    }
     static const bool graphs = !(std::getenv("ARROW_GRAPHS") && std::getenv("ARROW_GRAPHS")[0] == '0');
     if (graphs && !P->profiling && st != nullptr) {
         if (P->gexec && P->g_x == X && P->g_y == Y && P->g_k == k && P->g_stream == st) {

@@ -57,6 +57,14 @@ struct arrow_plan_s {
     std::vector<SegLevel> seg;     // segment-descriptor layout of the K-A kernels (default)
     int32_t *post_rows = nullptr;  // rows last written by a head-row partial (iterate's activation pass)
     int64_t n_post = 0;
+    // staged tail (single GPU): levels >= 1 as one launch into staging rows next to level 0, then
+    // one CSR gather-add into Y (arrow_api.cpp::build_stage_tail)
+    bool tail_on = false;
+    SegLevel tail;
+    int64_t tail_nhead = 0, tail_rows = 0, tail_ndst = 0;
+    int32_t *tail_ptr = nullptr, *tail_src = nullptr, *tail_dst = nullptr;
+    void *stage = nullptr;
+    int64_t stage_k = 0;
     std::vector<void *> seg_allocs;
     int seg_bseg = 16;
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
@@ -98,6 +106,7 @@ struct arrow_plan_s {
         if (host_y) cudaFree(host_y);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (post_rows) cudaFree(post_rows);
+        if (stage) cudaFree(stage);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (join_ev) cudaEventDestroy(join_ev);
         if (side) cudaStreamDestroy(side);
