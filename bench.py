@@ -294,7 +294,23 @@ def main():
         uid = [ab.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = ab.Comm(world, rank, uid[0])
-    plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm,
+    dec = None
+    if world > 1:
+        # one host decomposition for the node: rank 0 computes and checkpoints it, the others load it
+        # (arrow_decomposition_save/load), instead of G processes decomposing the same A at once
+        import tempfile
+        path = [os.path.join(tempfile.gettempdir(), f"arrow_bench_{os.getpid()}.dec") if rank == 0 else None]
+        dist.broadcast_object_list(path, src=0)
+        if rank == 0:
+            dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"])
+            dec.save(path[0])
+        dist.barrier()
+        if rank != 0:
+            dec = ab.Decomposition.load(path[0])
+        dist.barrier()
+        if rank == 0:
+            os.remove(path[0])
+    plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
                    window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments)
     info = plan.info()
@@ -407,6 +423,25 @@ def main():
         it = {"activation": "relu", "iters": args.iterate, "ms_per_iter": round(ms_it, 4),
               "value": round(flop / (ms_it * 1e-3) / 1e9, 3), "unit": "GFLOP/s"}
         del Xi, Yi
+    # alpha-beta ledger: the rows this rank actually exchanges (plan-time
+    # routes) against the survey's prediction 2 (sum_{i>=1} n_i - h_i) k s (G-1)/G^2 + sum_i h_i k s
+    nvl = None
+    if world > 1 and dec is not None:
+        sch = dec.dist_schedule(world, rank)
+        f_send = sum(int(l["send"].sum() - l["send"][rank]) for l in sch["levels"][1:])
+        f_recv = sum(int(l["recv"].sum() - l["recv"][rank]) for l in sch["levels"][1:])
+        r_send = sum(int(l["out"].sum() - l["out"][rank]) for l in sch["levels"][1:])
+        r_recv = sum(int(l["in"].sum() - l["in"][rank]) for l in sch["levels"][1:])
+        heads = sum(dec.level_info(i)["head"] for i in range(dec.info()["levels"]))
+        body1 = sum(dec.level_info(i)["n_i"] - dec.level_info(i)["head"] for i in range(1, dec.info()["levels"]))
+        row_b = k * es
+        mine = torch.tensor([max(f_send + r_send, f_recv + r_recv) * row_b + heads * row_b], dtype=torch.float64, device=dev)
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+        pred = 2 * body1 * row_b * (world - 1) / world ** 2 + heads * row_b
+        nvl = {"rows_fwd_send": f_send, "rows_fwd_recv": f_recv, "rows_rev_send": r_send, "rows_rev_recv": r_recv,
+               "bytes_per_gpu_per_direction_max": int(mine.item()), "bytes_predicted_per_gpu_per_direction": int(pred),
+               "t_bound_ms_at_900GBs": round(float(mine.item()) / 900e9 * 1e3, 4),
+               "note": "rank-0 row counts; bytes = max over ranks of (forward + reverse rows) x k x s + head blocks"}
     oned = None
     if world > 1 and not args.no_lib_baseline:
         oned = one_d_baseline(g, X, k, dtype, world, rank, dev, flop)
@@ -441,6 +476,7 @@ def main():
             "cpu_baseline": cpu,
             "library_baseline": lib if world == 1 else oned,
             "iterate": it,
+            "nvlink": nvl,
             "create_seconds": round(info["create_seconds"], 2),
         }
         print(json.dumps(line), flush=True)
