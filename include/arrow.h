@@ -76,7 +76,7 @@ typedef struct {
     int32_t order;              /* ARROW_ORDER_*; default ORIGINAL.  Distributed mode forces PERMUTED. */
     int32_t residual;           /* ARROW_RESIDUAL_*; default ERROR */
     int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (16384) */
-    int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (128) */
+    int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32) */
     int32_t batch_segments;     /* segments per work batch of the segment-stream kernel; 0 = default */
     int32_t reserved[6];
 } arrow_options;
