@@ -263,6 +263,8 @@ def main():
                     help="X/Y row order: original vertex ids, or pi_0 order (R18; forced when distributed)")
     ap.add_argument("--iterate", type=int, default=10, help="iterations of the fused-ReLU iterate timing (0: skip)")
     ap.add_argument("--no-lib-baseline", action="store_true", help="skip the cuSPARSE (torch.sparse) comparator")
+    ap.add_argument("--band", default="block", choices=["block", "strict"],
+                    help="LA-Decompose step 3 band: block-diagonal tiles (R3) or strict |p-q| <= b (NEXT-2, 1 GPU)")
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
     ap.add_argument("--batch-segments", type=int, default=0)
@@ -312,7 +314,8 @@ def main():
             os.remove(path[0])
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
-                   window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments)
+                   window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
+                   band=args.band)
     info = plan.info()
     lo, hi = plan.local_begin, plan.local_end
     if comm is not None or args.order == "permuted":
@@ -450,7 +453,7 @@ def main():
         lib = cusparse_baseline(g, Xd, k, flop, stream)
 
     if rank == 0:
-        traffic = load_traffic(args.config, k, dtype)
+        traffic = load_traffic(args.config, k, dtype) if args.band == "block" else None
         line = {
             "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
@@ -458,6 +461,7 @@ def main():
             "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}",
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
+                       "band": args.band if world == 1 else "block",
                        "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",
                        "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},
             "hbm_roofline": {"bytes_alg_per_step": b_alg, "achieved_GBs": round(b_alg / (ms_per_step * 1e-3) / 1e9, 1),

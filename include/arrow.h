@@ -66,6 +66,12 @@ typedef struct arrow_comm_s *arrow_comm;
 
 enum { ARROW_ORDER_ORIGINAL = 0,   /* X, Y rows in A's vertex order (default; R18) */
        ARROW_ORDER_PERMUTED = 1 }; /* X, Y rows in pi_0 order: row p holds vertex perm_0[p] */
+/* Step 3 of LA-Decompose: which band around the diagonal a level captures besides the
+ * first b rows/columns.  BLOCK: the diagonal b x b tiles (the block-diagonal band Alg. 1 computes,
+ * §4.1; reading R3, default).  STRICT: every entry with |p - q| <= b -- the arrow-width
+ * definition itself and Fig. 3; fewer levels, body rows read X rows of the
+ * neighbouring tiles.  Single-GPU plans only (distributed: ARROW_E_UNSUPPORTED). */
+enum { ARROW_BAND_BLOCK = 0, ARROW_BAND_STRICT = 1 };
 enum { ARROW_RESIDUAL_ERROR = 0,   /* levels cap hit with entries left -> ARROW_E_LEVELS */
        ARROW_RESIDUAL_CSR = 1 };   /* keep the leftover entries as one unstructured CSR level */
 
@@ -78,7 +84,8 @@ typedef struct {
     int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (16384) */
     int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32) */
     int32_t batch_segments;     /* segments per work batch of the segment-stream kernel; 0 = default */
-    int32_t reserved[6];
+    int32_t band;               /* ARROW_BAND_*: step 3's band; default BLOCK */
+    int32_t reserved[5];
 } arrow_options;
 
 /* Fill *opt with the defaults above (compute = ARROW_F32 until a CSR is seen: callers that
@@ -212,6 +219,10 @@ arrow_status arrow_plan_kernel_times(arrow_plan plan, arrow_kernel_times_t *out)
  * keeps entries left at the `levels` cap instead of failing with ARROW_E_LEVELS. */
 arrow_status arrow_decompose(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
                              arrow_decomposition *out);
+/* Same with step 3's band chosen (ARROW_BAND_BLOCK = arrow_decompose, ARROW_BAND_STRICT: |p-q| <= b,
+ * P:253 / Fig. 3); any other value -> ARROW_E_INVALID_ARG.  Saved files record the band. */
+arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                                int32_t band, arrow_decomposition *out);
 /* n, b, order (number of arrow matrices), residual entries; any pointer may be NULL. */
 arrow_status arrow_decomposition_info(arrow_decomposition d, int64_t *n, int64_t *b, int32_t *levels,
                                       int64_t *residual_nnz);

@@ -23,6 +23,7 @@ listed in DESIGN.md §3:
       tree layout: root = min id, preorder, children by (size asc, id asc) (R12)   -- P:900
       order_i := H_i ++ layouts; pos_i(order_i[p]) := p
       (u,v,a) -> B_i at (pos u, pos v) iff p < b or q < b or p//b == q//b (R3)     -- step 3, P:811/P:473
+                 (band="strict": p < b or q < b or |p - q| <= b, P:253 / Fig. 3; NEXT-2)
       otherwise (u,v,a) -> E_{i+1}                                                  -- step 4
     level 0 is presented with n rows: positions n_0..n-1 hold A-isolated vertices in id order.
 """
@@ -78,6 +79,7 @@ class Decomposition:
     b: int
     levels: list = field(default_factory=list)
     residual: tuple | None = None    # (u, v, a) original-id triples left when the level cap is hit
+    band: str = "block"              # step 3's band (captured())
 
     @property
     def order(self) -> int:
@@ -167,13 +169,24 @@ def prune_head(eu: np.ndarray, n: int, b: int) -> np.ndarray:
     return V[np.lexsort((V, -deg[V]))][:min(b, len(V))]
 
 
-def captured(p: np.ndarray, q: np.ndarray, b: int) -> np.ndarray:
-    """Step 3 (P:811 with the block-diagonal band of §4.1; R3): entry at positions
-    (p, q) belongs to B_i iff it lies in the first b rows or columns or in a diagonal b x b tile."""
-    return (p < b) | (q < b) | (p // b == q // b)
+BANDS = ("block", "strict")
 
 
-def extract(eu, ev, ea, order, b: int):
+def captured(p: np.ndarray, q: np.ndarray, b: int, band: str = "block") -> np.ndarray:
+    """Step 3: entry at positions (p, q) belongs to B_i iff it lies in the first b rows
+    or columns, or in the band around the diagonal:
+      band="block"  -- a diagonal b x b tile (the block-diagonal band of §4.1, P:473; R3);
+      band="strict" -- |p - q| <= b, the arrow-width definition itself ("for all i>b and
+                       j>b ... if A_ij != 0 then |i-j| <= b", 1-based) and Fig. 3 (P:595-790);
+                       NEXT-2 of SURVEY §8(f)."""
+    if band == "block":
+        return (p < b) | (q < b) | (p // b == q // b)
+    if band == "strict":
+        return (p < b) | (q < b) | (np.abs(p - q) <= b)
+    raise ValueError(f"unknown band {band!r}")
+
+
+def extract(eu, ev, ea, order, b: int, band: str = "block"):
     """Apply step 3 for a given arrangement `order` (order[p] = vertex at position p).
     Returns ((p, q, a) captured, (u, v, a) remainder)."""
     eu, ev, ea = np.asarray(eu, np.int64), np.asarray(ev, np.int64), np.asarray(ea, np.float64)
@@ -183,12 +196,15 @@ def extract(eu, ev, ea, order, b: int):
     p, q = pos[eu], pos[ev]
     if ((p < 0) | (q < 0)).any():
         raise ValueError("arrangement does not cover every endpoint")
-    cap = captured(p, q, b)
+    cap = captured(p, q, b, band)
     return (p[cap], q[cap], ea[cap]), (eu[~cap], ev[~cap], ea[~cap])
 
 
 # ---------------------------------------------------------------------------- LA-Decompose
-def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4) -> Decomposition:
+def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4,
+                 band: str = "block") -> Decomposition:
+    if band not in BANDS:
+        raise ValueError(f"unknown band {band!r}")
     if b < 2:
         raise ValueError("arrow width b must be >= 2 (P:807)")
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
@@ -197,7 +213,7 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
     ea = np.asarray(val, dtype=np.float64)
     deg_a = np.diff(row_ptr)
     isolated_a = np.flatnonzero(deg_a == 0)
-    dec = Decomposition(n=n, b=b)
+    dec = Decomposition(n=n, b=b, band=band)
     i = 0
     while True:
         if len(eu) == 0:
@@ -223,9 +239,10 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
         assert len(order_i) == n_i
         pos = np.full(n, -1, dtype=np.int64)
         pos[order_i] = np.arange(n_i, dtype=np.int64)
-        # step 3: head rows/columns plus block-diagonal b x b tiles (R3)
+        # step 3: head rows/columns plus the band: block-diagonal b x b tiles (R3)
+        # or, band="strict", |p - q| <= b
         p, q = pos[eu], pos[ev]
-        cap = captured(p, q, b)
+        cap = captured(p, q, b, band)
         perm = order_i if i > 0 else np.concatenate([order_i, isolated_a])
         rows = len(perm)
         bp, bq, ba = p[cap], q[cap], ea[cap]

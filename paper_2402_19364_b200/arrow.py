@@ -21,6 +21,7 @@ _LIB: Optional[ctypes.CDLL] = None
 ARROW_F32, ARROW_F64 = 0, 1
 ORDER = {"original": 0, "permuted": 1}
 RESIDUAL = {"error": 0, "csr": 1}
+BAND = {"block": 0, "strict": 1}    # ARROW_BAND_* (step 3 of LA-Decompose; strict = P:253 / Fig. 3)
 STATUS = ["ARROW_OK", "ARROW_E_INVALID_ARG", "ARROW_E_BAD_CSR", "ARROW_E_NOT_SYMMETRIC", "ARROW_E_LEVELS",
           "ARROW_E_CUDA", "ARROW_E_NCCL", "ARROW_E_NOMEM", "ARROW_E_STATE", "ARROW_E_UNSUPPORTED"]
 KERNELS = ["head_stage", "segments", "head_epilogue", "comm"]
@@ -34,7 +35,7 @@ SYMBOLS = [
     "arrow_decomposition_export_level", "arrow_decomposition_export_residual", "arrow_decomposition_save",
     "arrow_decomposition_load", "arrow_decomposition_destroy", "arrow_plan_create_from", "arrow_comm_unique_id",
     "arrow_comm_create", "arrow_comm_destroy", "arrow_status_string", "arrow_last_error", "arrow_abi_version",
-    "arrow_dist_schedule", "arrow_spmm_iterate",
+    "arrow_dist_schedule", "arrow_spmm_iterate", "arrow_decompose_ex",
 ]
 
 
@@ -53,7 +54,7 @@ class CSR(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("compute", ctypes.c_int), ("seed", ctypes.c_uint64), ("order", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("window_rows", ctypes.c_int64), ("head_chunk", ctypes.c_int32),
-                ("batch_segments", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+                ("batch_segments", ctypes.c_int32), ("band", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -107,6 +108,7 @@ def lib() -> ctypes.CDLL:
             "arrow_plan_set_profiling": [p, i32],
             "arrow_plan_kernel_times": [p, p],
             "arrow_decompose": [p, i64, i32, u64, i32, p],
+            "arrow_decompose_ex": [p, i64, i32, u64, i32, i32, p],
             "arrow_decomposition_info": [p, p, p, p, p],
             "arrow_decomposition_level_info": [p, i32, p],
             "arrow_decomposition_export_level": [p, i32, p, p, p, p],
@@ -160,7 +162,7 @@ def _dtype_code(dtype) -> int:
 
 
 def options(dtype=None, seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
-            head_chunk: int = 0, batch_segments: int = 0) -> Options:
+            head_chunk: int = 0, batch_segments: int = 0, band: str = "block") -> Options:
     o = Options()
     _check(lib().arrow_options_default(ctypes.byref(o)), "arrow_options_default")
     o.compute = _dtype_code(dtype)
@@ -170,6 +172,7 @@ def options(dtype=None, seed: int = 4, order: str = "original", residual: str = 
     o.window_rows = window_rows
     o.head_chunk = head_chunk
     o.batch_segments = batch_segments
+    o.band = BAND[band]
     return o
 
 
@@ -190,15 +193,15 @@ class Decomposition:
     """Host LA-Decompose result (arrow_decompose); no GPU needed."""
 
     def __init__(self, n, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4, keep_residual: bool = False,
-                 _handle=None):
+                 band: str = "block", _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
             return
         keep: list = []
         A = _csr(n, row_ptr, col, val, keep)
-        _check(lib().arrow_decompose(ctypes.byref(A), b, levels, seed, int(keep_residual), ctypes.byref(self._h)),
-               "arrow_decompose")
+        _check(lib().arrow_decompose_ex(ctypes.byref(A), b, levels, seed, int(keep_residual), BAND[band],
+                                        ctypes.byref(self._h)), "arrow_decompose_ex")
 
     @classmethod
     def load(cls, path: str) -> "Decomposition":
@@ -287,9 +290,9 @@ class Plan:
     def __init__(self, n=None, row_ptr=None, col=None, val=None, b: int = 2, levels: int = 0, dtype=None,
                  seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
                  head_chunk: int = 0, batch_segments: int = 0, comm=None,
-                 decomposition: Optional[Decomposition] = None):
+                 decomposition: Optional[Decomposition] = None, band: str = "block"):
         self._h = ctypes.c_void_p()
-        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments)
+        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments, band)
         comm_h = comm.handle if comm is not None else None
         if decomposition is not None:
             _check(lib().arrow_plan_create_from(decomposition._h, ctypes.byref(opt), comm_h, ctypes.byref(self._h)),

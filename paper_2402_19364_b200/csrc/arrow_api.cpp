@@ -356,10 +356,11 @@ arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, ar
 }
 
 static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, bool keep_residual,
-                                   std::unique_ptr<arrow_decomposition_s> &D) {
+                                   int32_t band, std::unique_ptr<arrow_decomposition_s> &D) {
     const auto t0 = std::chrono::steady_clock::now();
     arrow_status st = validate_args(A, b, levels);
     if (st != ARROW_OK) return st;
+    if (band != ARROW_BAND_BLOCK && band != ARROW_BAND_STRICT) return fail(ARROW_E_INVALID_ARG, "bad band");
     std::string err;
     const int64_t n = A->n;
     if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
@@ -369,8 +370,9 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         D->n = n;
         D->b = b;
         D->seed = seed;
+        D->band = band;
         HostDecomposition H;
-        if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, H, err)) return fail(ARROW_E_INVALID_ARG, err);
+        if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, H, err)) return fail(ARROW_E_INVALID_ARG, err);
         if (!H.residual.empty() && !keep_residual)
             return fail(ARROW_E_LEVELS, "levels cap " + std::to_string(levels) + " reached with " +
                                             std::to_string(H.residual.size()) + " entries left");
@@ -633,6 +635,10 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     P->local_begin = 0;
     P->local_end = n;
     if (comm) {
+        // the distributed routes assume a level-0 row reads only X rows of its own tile (R3); the
+        // strict band reaches into the neighbouring tiles, i.e. across rank boundaries
+        if (D.band != ARROW_BAND_BLOCK)
+            return fail(ARROW_E_UNSUPPORTED, "distributed plans need ARROW_BAND_BLOCK (strict band: single GPU only)");
         P->comm = comm;
         arrow_status cs = dist_build(P.get(), D, comm, window_rows, head_chunk);
         if (cs != ARROW_OK) return cs;
@@ -653,7 +659,7 @@ arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels,
     if (opt.residual != ARROW_RESIDUAL_ERROR && opt.residual != ARROW_RESIDUAL_CSR)
         return fail(ARROW_E_INVALID_ARG, "bad options.residual");
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, D);
+    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, D);
     if (st != ARROW_OK) return st;
     st = plan_from(*D, &opt, A->dtype, comm, out);
     if (st == ARROW_OK) (*out)->create_seconds += D->seconds;
@@ -670,11 +676,16 @@ arrow_status arrow_plan_create_from(arrow_decomposition d, const arrow_options *
 
 arrow_status arrow_decompose(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
                              arrow_decomposition *out) {
+    return arrow_decompose_ex(A, b, levels, seed, keep_residual, ARROW_BAND_BLOCK, out);
+}
+
+arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                                int32_t band, arrow_decomposition *out) {
     g_err.clear();
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
     return ARROW_OK;
@@ -737,7 +748,8 @@ struct Fnv {
         for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
     }
 };
-const char kMagic[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '1'};
+const char kMagic[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '2'};   // 02: header + band
+const char kMagic1[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '1'};  // 01: block band only
 }  // namespace
 
 arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path) {
@@ -752,7 +764,8 @@ arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path) {
         ok = ok && std::fwrite(p, 1, n, f) == n;
     };
     w(kMagic, 8);
-    const int64_t hdr[6] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated};
+    const int64_t hdr[7] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated,
+                            (int64_t)d->band};
     w(hdr, sizeof(hdr));
     for (const HostLevel &L : d->levels) {
         const int64_t lh[4] = {L.rows, L.n_i, L.head, L.row_ptr[L.rows]};
@@ -788,11 +801,12 @@ arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out
         D.reset(new arrow_decomposition_s());
         char magic[8];
         r(magic, 8);
-        if (!ok || std::memcmp(magic, kMagic, 8) != 0) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "not an arrow decomposition file"); }
-        int64_t hdr[6];
-        r(hdr, sizeof(hdr));
-        if (!ok || hdr[0] < 0 || hdr[1] < 2 || hdr[3] < 0 || hdr[4] < 0) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
-        D->n = hdr[0]; D->b = hdr[1]; D->seed = (uint64_t)hdr[2]; D->isolated = hdr[5];
+        const bool v1 = ok && std::memcmp(magic, kMagic1, 8) == 0;
+        if (!ok || (!v1 && std::memcmp(magic, kMagic, 8) != 0)) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "not an arrow decomposition file"); }
+        int64_t hdr[7] = {0, 0, 0, 0, 0, 0, 0};
+        r(hdr, (v1 ? 6 : 7) * sizeof(int64_t));
+        if (!ok || hdr[0] < 0 || hdr[1] < 2 || hdr[3] < 0 || hdr[4] < 0 || hdr[6] < 0 || hdr[6] > 1) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
+        D->n = hdr[0]; D->b = hdr[1]; D->seed = (uint64_t)hdr[2]; D->isolated = hdr[5]; D->band = (int32_t)hdr[6];
         D->levels.resize(hdr[3]);
         for (HostLevel &L : D->levels) {
             int64_t lh[4];
@@ -922,6 +936,8 @@ static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("tail add: ") + cudaGetErrorString((cudaError_t)e)); }
         return ARROW_OK;
     }
+    const int32_t *zfold_rows = nullptr;
+    int64_t zfold_n = 0;
     for (size_t i = 0; i < P->levels.size(); ++i) {
         const DeviceLevel &L = P->levels[i];
         cudaEvent_t a = nullptr;
@@ -932,11 +948,19 @@ static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t
             // them; the rest on a side stream next to level 0, joined before level 1 (measured slower on
             // config R: 4.0 vs 3.1 ms -- a small side grid cannot keep enough stores in flight)
             static const bool overlap = std::getenv("ARROW_KZ_OVERLAP") && std::getenv("ARROW_KZ_OVERLAP")[0] == '1';  // measured slower
-            const int64_t nh = (overlap && i == 0 && L.nzero > L.head) ? L.head : L.nzero;
+            // default: only the head rows here (level 0 adds into them); the entry-less rows are
+            // zeroed inside K-A level 0, a share per batch grab (ARROW_KZ_FOLD=0: all here)
+            static const bool fold = !(std::getenv("ARROW_KZ_FOLD") && std::getenv("ARROW_KZ_FOLD")[0] == '0');
+            const bool folding = fold && !overlap && i == 0 && !P->seg.empty() && L.nzero > L.head;
+            const int64_t nh = ((overlap || folding) && i == 0 && L.nzero > L.head) ? L.head : L.nzero;
+            if (folding) {
+                zfold_rows = L.zero_rows + nh;
+                zfold_n = L.nzero - nh;
+            }
             prof_begin(P, st, a);
-            e = launch_zero_rows(dt, L.zero_rows, nh, k, Y, st);
+            if (nh > 0) e = launch_zero_rows(dt, L.zero_rows, nh, k, Y, st);
             prof_end(P, st, ARROW_K_HEAD_STAGE, a);
-            if (!e && nh < L.nzero) {
+            if (!e && nh < L.nzero && !folding) {
                 if (!P->side) {
                     CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
                     CUDA_TRY(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
@@ -953,9 +977,11 @@ static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t
         prof_begin(P, st, a);
         if (!P->seg.empty())
             e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->seg_bseg, st,
-                           nullptr, act);
+                           nullptr, act, zfold_rows, zfold_n);
         else
             e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
+        zfold_rows = nullptr;
+        zfold_n = 0;
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (!joined) CUDA_TRY(cudaStreamWaitEvent(st, P->join_ev, 0));
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }

@@ -24,13 +24,14 @@ struct HostLevel {
 
 struct HostDecomposition {
     int64_t n = 0, b = 0;
+    int band = 0;                    // step 3's band: 0 block-diagonal tiles (R3), 1 strict |p-q| <= b
     std::vector<HostLevel> levels;
     std::vector<uint32_t> residual;  // entry indices of A left when the level cap is reached
 };
 
 // LA-Decompose (decompose.cpp).  Returns 0 on success, else sets `err`.
 int la_decompose(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
-                 uint64_t seed, HostDecomposition &out, std::string &err);
+                 uint64_t seed, int band, HostDecomposition &out, std::string &err);
 
 // Validation helpers (decompose.cpp): 0 ok, 1 bad CSR, 2 not symmetric.
 int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, std::string &err);
@@ -82,6 +83,10 @@ constexpr uint32_t kLocalRmwBit = 0x40000000u;  // K-A (dist 2): out row is a lo
 struct PeerPtrs {
     void *p[kMaxPeers];
     int act = 0;  // K-A only: activation applied when a row's final segment is flushed (iterate mode)
+    // K-A level 0, single GPU: Y rows to zero (entry-less and A-isolated rows), shared out over the
+    // warps' batch grabs so that their stores overlap the gathers instead of a separate K-Z pass
+    const int32_t *zrows = nullptr;
+    int64_t nzero = 0;
 };
 // single GPU: a body segment whose row receives no later contribution (arrow_spmm_iterate's
 // activation is applied when it is flushed); activations: 0 identity, 1 ReLU
@@ -91,7 +96,8 @@ constexpr uint32_t kRowMask30 = 0x3fffffffu;
 // body rows stored through `outs` (encoded rows, levels >= 1 of the P2P transport) or, with
 // kLocalRmwBit, added into Y (rows whose home is this rank)
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs = nullptr, int act = 0);
+               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs = nullptr, int act = 0,
+               const int32_t *zrows = nullptr, int64_t nzero = 0);
 // Y[rows[i]] = act(Y[rows[i]]) (rows whose last contribution is a head-row partial)
 int launch_act_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, int act, void *Y, void *stream);
 // dst row enc(didx[i]) of bases = src[sidx[i]] (sidx < 0: zero); grid of `blocks` (0: sized to n)

@@ -10,7 +10,9 @@
 //   min(b,|V_i|) of V_i by (deg desc, id asc); forest F_i = Kruskal over G'_i = G_i[V_i \ H_i]
 //   with edge order (splitmix64(splitmix64(seed+i) ^ (u<<32|v)), u, v); trees by (size desc,
 //   min id asc), each rooted at its min id, preorder with children by (subtree size asc, id asc);
-//   order_i = H_i ++ trees; entry (u,v) captured iff p<b or q<b or p/b == q/b (p,q positions).
+//   order_i = H_i ++ trees; entry (u,v) captured iff p<b or q<b or p/b == q/b (p,q positions);
+//   band = 1 (strict, NEXT-2): p<b or q<b or |p-q| <= b -- the arrow-width definition of
+//   and Fig. 3.
 //
 // Parallel where the work is bulk (degree histograms, edge keys, the edge sort, extraction,
 // CSR assembly); union-find and the tree layouts are sequential.
@@ -122,10 +124,11 @@ void stable_partition_par(const std::vector<uint32_t> &in, Pred pred, std::vecto
 }  // namespace
 
 int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, int32_t max_levels,
-                 uint64_t seed, HostDecomposition &out, std::string &err) {
+                 uint64_t seed, int band, HostDecomposition &out, std::string &err) {
     out = HostDecomposition{};
     out.n = n;
     out.b = b;
+    out.band = band;
     const int64_t nnz = rp[n];
     if (nnz == 0) return 0;
 
@@ -290,12 +293,14 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
         std::fill(pos.begin(), pos.end(), -1);
         for (int64_t p = 0; p < n_i; ++p) pos[L.perm[p]] = (int32_t)p;
 
-        // ---- step 3: capture head rows/columns and diagonal b x b tiles (R3)
+        // ---- step 3: capture head rows/columns and diagonal b x b tiles (R3), or the
+        // strict band |p - q| <= b (band = 1; Fig. 3)
         stable_partition_par(
             ent,
             [&](uint32_t e) {
                 const int64_t p = pos[erow[e]], q = pos[col[e]];
-                return p < b || q < b || (p / b) == (q / b);
+                if (p < b || q < b) return true;
+                return band ? (p > q ? p - q : q - p) <= b : (p / b) == (q / b);
             },
             captured, rest_ent);
         // canonical CSR of B_i in positions

@@ -118,6 +118,7 @@ struct arrow_plan_s {
 struct arrow_decomposition_s {
     int64_t n = 0, b = 0;
     uint64_t seed = 4;
+    int32_t band = 0;                    // ARROW_BAND_* of step 3
     int64_t isolated = 0;
     std::vector<HostLevel> levels;
     std::vector<int32_t> res_u, res_v;  // residual entries, original ids, CSR order

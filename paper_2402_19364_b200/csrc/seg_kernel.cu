@@ -85,6 +85,26 @@ __device__ __forceinline__ void apply_act(Frag<T, VEC> &f, int act) {
     }
 }
 
+// Folded K-Z: grab g of ngrab zeroes its share of outs.zrows (streaming stores of zero rows, no
+// dependence on anything the warp computes, so they drain while the warp gathers).  Lanes fetch
+// up to 32 row ids at once; the whole warp then stores row by row (lanes with col < k).
+template <typename T, int VEC>
+__device__ __forceinline__ void zero_share(const PeerPtrs &outs, int64_t g, int64_t ngrab, T *Y, int64_t k, int lane) {
+    if (outs.nzero == 0) return;
+    const int64_t per = (outs.nzero + ngrab - 1) / ngrab;
+    const int64_t z0 = g * per, z1 = (z0 + per < outs.nzero) ? z0 + per : outs.nzero;
+    Frag<T, VEC> z;
+    z.zero();
+    for (int64_t r0 = z0; r0 < z1; r0 += 32) {
+        const int cnt = (z1 - r0 < 32) ? (int)(z1 - r0) : 32;
+        const int32_t myrow = lane < cnt ? __ldg(outs.zrows + r0 + lane) : 0;
+        for (int t = 0; t < cnt; ++t) {
+            const int64_t row = __shfl_sync(0xffffffffu, myrow, t);
+            for (int64_t c = (int64_t)lane * VEC; c < k; c += 32 * VEC) st_stream<T, VEC>(Y + row * k + c, z);
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------ K-A
 // Segment stream.  A sub-warp of LPE lanes owns a row slab of LPE*VEC elements.  Work is a list
 // of non-empty segments in tile-window order, cut into batches of LPE consecutive segments.
@@ -127,6 +147,7 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
         wb = __shfl_sync(0xffffffffu, wb, 0);
         const int64_t bt = (int64_t)wb * SUBS + sub;
         if ((int64_t)wb * SUBS >= nbatch) break;       // warp-uniform exit
+        if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, (nbatch + SUBS - 1) / SUBS, Y, k, lane);
         if (bt >= nbatch) continue;                    // sub-warp idle this round
         const int64_t s0 = bt * bseg;
         const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
@@ -365,6 +386,7 @@ __global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ se
         const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
         const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
         const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+        if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
 
         for (int64_t c0 = 0; c0 < k; c0 += 32 * VEC) {
             const int64_t col0 = c0 + (int64_t)lane * VEC;
@@ -481,6 +503,7 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
         const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
         const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
         const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+        if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
 
         Frag<T, VEC> acc;
         acc.zero();
@@ -672,13 +695,19 @@ static bool narrow_k32() {
 }
 
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs, int act) {
+               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs, int act,
+               const int32_t *zrows, int64_t nzero) {
     using namespace kseg;
-    if (L.nseg == 0 || k == 0) return 0;
+    if (k == 0) return 0;
+    if (L.nseg == 0) return nzero > 0 ? launch_zero_rows(dtype, zrows, nzero, k, Y, stream) : 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     PeerPtrs po{};
     if (outs) po = *outs;
     po.act = act;
+    if (!dist && nzero > 0) {
+        po.zrows = zrows;
+        po.nzero = nzero;
+    }
     if (dist == 2 && !outs) return (int)cudaErrorInvalidValue;
     int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
     if (dist == 2)

@@ -276,3 +276,27 @@ def test_iterate_relu(order):
     out = plan.spmm_iterate(Xd, 1, "none")
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle.spmm(g.n, S.indptr, S.indices, S.data, X0)[perm0])
+
+
+@pytest.mark.parametrize("spec,b,k", [("RMAT(12,4,1)", 256, 16), ("GRID(256,1)", 256, 8), ("RMAT(16,8,1)", 256, 128),
+                                      ("PATH(1000,1)", 4, 3), ("WEB(12,2)", 64, 32), ("RMAT(14,8,3)", 1000, 33)])
+@pytest.mark.parametrize("order", ["original", "permuted"])
+def test_strict_band_parity(spec, b, k, order):
+    """NEXT-2: plans built with the strict band (|p-q| <= b, P:253 / Fig. 3).  Structure bit-exact
+    against the oracle's strict decomposition; fp64 Y bitwise equal to O1 on dyadic data; fp32
+    within the north-star tolerance."""
+    g = datagen.make_graph(spec)
+    ref = oracle.la_decompose(g.n, g.row_ptr, g.col, g.val, b, band="strict")
+    p64 = ab.Plan(g.n, g.row_ptr, g.col, g.val, b, dtype="f64", band="strict", order=order)
+    assert p64.sha256() == oracle.decomposition_sha256(ref)
+    X = datagen.make_x(g.n, k)
+    perm0 = ref.levels[0].perm if order == "permuted" else np.arange(g.n)
+    Y = run(p64, X[perm0])
+    Yo = oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+    assert np.array_equal(Y, Yo[perm0])
+    p32 = ab.Plan(g.n, g.row_ptr, g.col, g.val, b, dtype="f32", band="strict", order=order)
+    X32 = X.astype(np.float32)
+    Y32 = run(p32, X32[perm0])
+    out = np.empty_like(Y32)
+    out[perm0] = Y32
+    check_fp32(g, out, X32)
