@@ -87,6 +87,7 @@ struct PeerPtrs {
     // warps' batch grabs so that their stores overlap the gathers instead of a separate K-Z pass
     const int32_t *zrows = nullptr;
     int64_t nzero = 0;
+    int ypf = 0;  // K-A levels >= 1, single GPU: prefetch the batch's Y rows into L2 at batch start
 };
 // single GPU: a body segment whose row receives no later contribution (arrow_spmm_iterate's
 // activation is applied when it is flushed); activations: 0 identity, 1 ReLU

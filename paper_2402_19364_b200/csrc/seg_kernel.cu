@@ -105,6 +105,15 @@ __device__ __forceinline__ void zero_share(const PeerPtrs &outs, int64_t g, int6
     }
 }
 
+// Levels >= 1 (read-modify-write): every lane holding one of the batch's segments asks L2 for that
+// segment's Y row at batch start, so the flush's load hits L2 instead of waiting on DRAM.
+template <typename T>
+__device__ __forceinline__ void prefetch_y_rows(int ypf, int32_t my_out, bool valid, const T *Y, int64_t k) {
+    if (!ypf || !valid || my_out < 0) return;
+    const char *row = reinterpret_cast<const char *>(Y) + (uint64_t)(uint32_t)(my_out & kRowMask30) * (uint64_t)(k * sizeof(T));
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(row));  // first 128-byte line (k <= 32 fp32: the row)
+}
+
 // ------------------------------------------------------------------------------------ K-A
 // Segment stream.  A sub-warp of LPE lanes owns a row slab of LPE*VEC elements.  Work is a list
 // of non-empty segments in tile-window order, cut into batches of LPE consecutive segments.
@@ -361,7 +370,7 @@ __device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int 
     }
 }
 
-template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool DEFER>
+template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool DEFER, bool PF>
 __global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ seg_out,
                                                   const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                   const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
@@ -395,11 +404,25 @@ __global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ se
             acc.zero();
             int cur = 0;
             PendingRmw<T, VEC> pend;
+            // PF: the next chunk's (col, val) are requested one chunk ahead
+            int32_t pcol = 0;
+            T pval = T(0);
+            if (PF && e_begin + lane < e_end) {
+                pcol = __ldcs(ent_col + e_begin + lane);
+                pval = __ldcs(ent_val + e_begin + lane);
+            }
             for (uint32_t cb = e_begin; cb < e_end; cb += 32) {
                 const int cnt = (e_end - cb < 32u) ? (int)(e_end - cb) : 32;
                 int32_t mycol = 0;
                 T myval = T(0);
-                if (lane < cnt) {
+                if (PF) {
+                    mycol = pcol;
+                    myval = pval;
+                    if (cb + 32 + lane < e_end) {
+                        pcol = __ldcs(ent_col + cb + 32 + lane);
+                        pval = __ldcs(ent_val + cb + 32 + lane);
+                    }
+                } else if (lane < cnt) {
                     mycol = __ldcs(ent_col + cb + lane);
                     myval = __ldcs(ent_val + cb + lane);
                 }
@@ -425,11 +448,15 @@ int run_seg32(const SegLevel &L, const void *X, const void *D0, void *Y, void *C
     // deferred row RMW for the single-GPU levels >= 1
     // (measured: no gain on config R, 2.84 vs 2.82 ms K-A -- off unless ARROW_SEG_DEFER=1)
     static const bool defer_env = std::getenv("ARROW_SEG_DEFER") && std::getenv("ARROW_SEG_DEFER")[0] == '1';
+    // entry prefetch one chunk ahead (ARROW_SEG32_PF=1; measured neutral-to-worse at k = 128 -- the
+    // full-warp kernel's chunk has four 8-row gather groups, so the entry load was 1 of 5 latencies)
+    static const bool pf = std::getenv("ARROW_SEG32_PF") && std::getenv("ARROW_SEG32_PF")[0] == '1';
     constexpr bool kDefer = MODE == 1 && DIST == 0;
-    auto kern = (kDefer && defer_env) ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, kDefer> : k_seg32<T, VEC, MODE, DIST, false, kDefer>)
-                                      : (off32 ? k_seg32<T, VEC, MODE, DIST, true, false> : k_seg32<T, VEC, MODE, DIST, false, false>);
-    static int bps[4] = {0, 0, 0, 0};
-    int &b = bps[(off32 ? 1 : 0) + (kDefer && defer_env ? 2 : 0)];
+    auto kern = (kDefer && defer_env) ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, kDefer, false> : k_seg32<T, VEC, MODE, DIST, false, kDefer, false>)
+              : pf ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, false, true> : k_seg32<T, VEC, MODE, DIST, false, false, true>)
+                   : (off32 ? k_seg32<T, VEC, MODE, DIST, true, false, false> : k_seg32<T, VEC, MODE, DIST, false, false, false>);
+    static int bps[6] = {0, 0, 0, 0, 0, 0};
+    int &b = bps[(off32 ? 1 : 0) + (kDefer && defer_env ? 2 : (pf ? 4 : 0))];
     if (b == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
         if (b <= 0) b = 1;
@@ -472,7 +499,7 @@ __device__ __forceinline__ Frag<T, VEC> shfl_frag(const Frag<T, VEC> &f, int src
     return r;
 }
 
-template <typename T, int VEC, int LPE, int MODE, int DIST, bool OFF32>
+template <typename T, int VEC, int LPE, int MODE, int DIST, bool OFF32, bool PF>
 __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__ seg_out,
                                                      const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                      const int32_t *__restrict__ ent_col,
@@ -481,7 +508,9 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
                                                      int64_t k, unsigned *__restrict__ counter, int bseg,
                                                      const PeerPtrs outs) {
     constexpr int G = 32 / LPE;
-    constexpr int U = (32 / G) < 4 ? (32 / G) : 4;  // steps whose rows are loaded together
+    // steps whose rows are loaded together (PF: a whole 32-entry chunk when it fits in 8 steps)
+    constexpr int UMAX = PF ? 8 : 4;
+    constexpr int U = (32 / G) < UMAX ? (32 / G) : UMAX;
     const int lane = threadIdx.x & 31;
     const int q = lane / LPE;   // sub-warp: entry slot within a step
     const int sl = lane % LPE;  // 16-byte slice of the row
@@ -504,15 +533,31 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
         const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
         const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
         if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
+        if (MODE == 1 && DIST == 0) prefetch_y_rows<T>(outs.ypf, my_out, lane < nb, Y, k);
 
         Frag<T, VEC> acc;
         acc.zero();
         int cur = 0;  // segments of the batch closed so far
+        // PF: the next chunk's (col, val) are requested before this chunk's rows are gathered, so a
+        // chunk costs one memory latency (its gathers) instead of two
+        int32_t pcol = 0;
+        T pval = T(0);
+        if (PF && e_begin + lane < e_end) {
+            pcol = __ldcs(ent_col + e_begin + lane);
+            pval = __ldcs(ent_val + e_begin + lane);
+        }
         for (uint32_t cb = e_begin; cb < e_end; cb += 32) {
             const int cnt = (e_end - cb < 32u) ? (int)(e_end - cb) : 32;
             int32_t mycol = 0;
             T myval = T(0);
-            if (lane < cnt) {
+            if (PF) {
+                mycol = pcol;
+                myval = pval;
+                if (cb + 32 + lane < e_end) {
+                    pcol = __ldcs(ent_col + cb + 32 + lane);
+                    pval = __ldcs(ent_val + cb + 32 + lane);
+                }
+            } else if (lane < cnt) {
                 mycol = __ldcs(ent_col + cb + lane);
                 myval = __ldcs(ent_val + cb + lane);
             }
@@ -612,9 +657,12 @@ template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segsmall(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
                  unsigned *counter, const PeerPtrs &outs, bool off32, cudaStream_t st) {
     const int bseg = 32;
-    auto kern = off32 ? k_segsmall<T, VEC, LPE, MODE, DIST, true> : k_segsmall<T, VEC, LPE, MODE, DIST, false>;
-    static int bps[2] = {0, 0};
-    int &b = bps[off32 ? 1 : 0];
+    // entry prefetch + whole-chunk row loads (ARROW_SEG_PF=0: the earlier 4-step groups)
+    static const bool pf = !(std::getenv("ARROW_SEG_PF") && std::getenv("ARROW_SEG_PF")[0] == '0');
+    auto kern = pf ? (off32 ? k_segsmall<T, VEC, LPE, MODE, DIST, true, true> : k_segsmall<T, VEC, LPE, MODE, DIST, false, true>)
+                   : (off32 ? k_segsmall<T, VEC, LPE, MODE, DIST, true, false> : k_segsmall<T, VEC, LPE, MODE, DIST, false, false>);
+    static int bps[4] = {0, 0, 0, 0};
+    int &b = bps[(off32 ? 1 : 0) + (pf ? 2 : 0)];
     if (b == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
         if (b <= 0) b = 1;
@@ -708,6 +756,9 @@ int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void
         po.zrows = zrows;
         po.nzero = nzero;
     }
+    // ARROW_SEG_YPF=1: L2 prefetch of the batch's Y rows in the levels >= 1 (off by default)
+    static const bool ypf = std::getenv("ARROW_SEG_YPF") && std::getenv("ARROW_SEG_YPF")[0] == '1';
+    po.ypf = (!dist && ypf) ? 1 : 0;
     if (dist == 2 && !outs) return (int)cudaErrorInvalidValue;
     int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
     if (dist == 2)
