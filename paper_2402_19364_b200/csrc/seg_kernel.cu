@@ -93,14 +93,29 @@ __device__ __forceinline__ void zero_share(const PeerPtrs &outs, int64_t g, int6
     if (outs.nzero == 0) return;
     const int64_t per = (outs.nzero + ngrab - 1) / ngrab;
     const int64_t z0 = g * per, z1 = (z0 + per < outs.nzero) ? z0 + per : outs.nzero;
+    if (z0 >= z1) return;
     Frag<T, VEC> z;
     z.zero();
+    const uint32_t kv = (uint32_t)(k / VEC);           // VEC-wide chunks per row (pick_vec: k % VEC == 0)
+    if (kv <= 32u && (32u % kv) == 0u) {
+        // rows of <= 32 chunks: RP = 32 / kv rows per warp store, lane -> (row lane / kv, chunk lane % kv)
+        const uint32_t rp = 32u / kv, sub = (uint32_t)lane / kv, ch = (uint32_t)lane % kv;
+        for (int64_t r0 = z0; r0 < z1; r0 += 32) {
+            const int cnt = (z1 - r0 < 32) ? (int)(z1 - r0) : 32;
+            const int32_t myrow = lane < cnt ? __ldg(outs.zrows + r0 + lane) : 0;
+            for (uint32_t t = 0; t < (uint32_t)cnt; t += rp) {
+                const int32_t row = __shfl_sync(0xffffffffu, myrow, (int)((t + sub) & 31u));
+                if (t + sub < (uint32_t)cnt) st_stream<T, VEC>(Y + (int64_t)row * k + ch * VEC, z);
+            }
+        }
+        return;
+    }
     for (int64_t r0 = z0; r0 < z1; r0 += 32) {
         const int cnt = (z1 - r0 < 32) ? (int)(z1 - r0) : 32;
         const int32_t myrow = lane < cnt ? __ldg(outs.zrows + r0 + lane) : 0;
         for (int t = 0; t < cnt; ++t) {
-            const int64_t row = __shfl_sync(0xffffffffu, myrow, t);
-            for (int64_t c = (int64_t)lane * VEC; c < k; c += 32 * VEC) st_stream<T, VEC>(Y + row * k + c, z);
+            T *row = Y + (int64_t)__shfl_sync(0xffffffffu, myrow, t) * k;
+            for (uint32_t c = (uint32_t)lane; c < kv; c += 32u) st_stream<T, VEC>(row + c * VEC, z);
         }
     }
 }
@@ -584,15 +599,15 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
                 for (int t = 0; t < U; ++t) {
                     const int u0 = g0 + t * G;
                     if (u0 >= cnt) break;  // warp-uniform
-                    Frag<T, VEC> v;
-#pragma unroll
-                    for (int i = 0; i < VEC; ++i) v.v[i] = vals[t] * xs[t].v[i];
                     const unsigned ends = (endmask >> u0) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
                     if (ends == 0u) {  // warp-uniform: every entry of the step continues the open segment
 #pragma unroll
-                        for (int i = 0; i < VEC; ++i) acc.v[i] += v.v[i];
+                        for (int i = 0; i < VEC; ++i) acc.v[i] = fma(vals[t], xs[t].v[i], acc.v[i]);
                         continue;
                     }
+                    Frag<T, VEC> v;
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) v.v[i] = vals[t] * xs[t].v[i];
                     if (__popc(ends) == 1) {  // warp-uniform, the common case: one segment closes at slot e
                         const int e = __ffs(ends) - 1;
                         // total = every partial + the products of slots <= e; slots > e open the next one
