@@ -496,6 +496,143 @@ int run_seg32_mode(int dist, const SegLevel &L, const void *X, const void *D0, v
                        : run_seg32<T, VEC, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, off32, st);
 }
 
+// ------------------------------------------------------------------------------------ K-A (levels >= 1)
+// Levels >= 1 of a single-GPU plan read-modify-write scattered Y rows.  In k_seg32 the read of a
+// row is issued when its segment closes and the warp waits for it before going on (one DRAM
+// latency per segment, ~6 entries).  Here a warp takes STAGE segments at a time and, before
+// gathering their entries, starts asynchronous copies (cp.async, 16 B per lane) of all their Y
+// slabs into a warp-private shared-memory stage; the flush then reads the row from shared memory.
+// The Y reads overlap the gathers as in a plain RMW stream (profiles/rmw_bw.cu: 6.2 TB/s).
+template <typename T, int VEC, bool OFF32, int STAGE>
+__global__ void __launch_bounds__(256, 4) k_tail32(const int32_t *__restrict__ seg_out,
+                                                   const uint32_t *__restrict__ seg_end, int64_t nseg,
+                                                   const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
+                                                   const T *__restrict__ X, T *__restrict__ Y, int64_t k,
+                                                   unsigned *__restrict__ counter, const PeerPtrs outs) {
+    constexpr int UNROLL = Seg32Unroll<T>::value;
+    using V = typename VecT<T, VEC>::type;
+    __shared__ V stage[8][STAGE][32];  // 8 warps x STAGE rows x 512 B
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int64_t nbatch = (nseg + STAGE - 1) / STAGE;
+    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
+    const char *Xc = reinterpret_cast<const char *>(X);
+    for (;;) {
+        unsigned wb = 0;
+        if (lane == 0) wb = atomicAdd(counter, 1u);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if ((int64_t)wb >= nbatch) break;
+        const int64_t s0 = (int64_t)wb * STAGE;
+        const int nb = (nseg - s0 < STAGE) ? (int)(nseg - s0) : STAGE;
+        const int32_t my_out = (lane < nb) ? __ldg(seg_out + s0 + lane) : 0;
+        const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+        for (int64_t c0 = 0; c0 < k; c0 += 32 * VEC) {
+            const int64_t col0 = c0 + (int64_t)lane * VEC;
+            const uint32_t lane_off = (uint32_t)(col0 * (int64_t)sizeof(T));
+            // stage the Y slabs of the body segments (head partials are L2 atomics, not staged)
+#pragma unroll
+            for (int s = 0; s < STAGE; ++s) {
+                const int32_t o = __shfl_sync(0xffffffffu, my_out, s);
+                if (s < nb && o >= 0) {
+                    const T *src = Y + (int64_t)(o & kRowMask30) * k + col0;
+                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&stage[wid][s][lane]);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            Frag<T, VEC> acc;
+            acc.zero();
+            int cur = 0;
+            bool waited = false;
+            for (uint32_t cb = e_begin; cb < e_end; cb += 32) {
+                const int cnt = (e_end - cb < 32u) ? (int)(e_end - cb) : 32;
+                int32_t mycol = 0;
+                T myval = T(0);
+                if (lane < cnt) {
+                    mycol = __ldcs(ent_col + cb + lane);
+                    myval = __ldcs(ent_val + cb + lane);
+                }
+                const uint32_t rel = my_end - 1u - cb;
+                const unsigned endmask = __reduce_or_sync(0xffffffffu, (rel < 32u) ? (1u << rel) : 0u);
+#pragma unroll 1
+                for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
+                    const int n = min(cnt - u0, UNROLL);
+                    const unsigned grp = (endmask >> u0) & ((1u << UNROLL) - 1u);
+                    Frag<T, VEC> xv[UNROLL];
+                    T av[UNROLL];
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+                        const int32_t col = __shfl_sync(0xffffffffu, mycol, (u0 + t) & 31);
+                        av[t] = __shfl_sync(0xffffffffu, myval, (u0 + t) & 31);
+                        const char *p;
+                        if (OFF32) p = Xc + (uint32_t)((uint32_t)col * rowbytes + lane_off);
+                        else p = Xc + (uint64_t)(uint32_t)col * rowbytes + lane_off;
+                        if (t < n) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
+                    }
+                    if (n == UNROLL && grp == 0u) {
+#pragma unroll
+                        for (int t = 0; t < UNROLL; ++t)
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        continue;
+                    }
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+                        if (t < n) {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        }
+                        if ((grp >> t) & 1u) {
+                            const int32_t o = __shfl_sync(0xffffffffu, my_out, cur);
+                            if (o < 0) {
+                                atomic_add_frag<T, VEC>(Y + (int64_t)(o & 0x7fffffff) * k + col0, acc);
+                            } else {
+                                if (!waited) {
+                                    asm volatile("cp.async.wait_all;" ::: "memory");
+                                    waited = true;
+                                }
+                                Frag<T, VEC> y;
+                                const V sv = stage[wid][cur][lane];
+                                memcpy(&y, &sv, sizeof(V));
+#pragma unroll
+                                for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                if ((o & kFinalBit) && outs.act) apply_act<T, VEC>(y, outs.act);
+                                st_plain<T, VEC>(Y + (int64_t)(o & kRowMask30) * k + col0, y);
+                            }
+                            acc.zero();
+                            ++cur;
+                        }
+                    }
+                }
+            }
+            if (!waited) asm volatile("cp.async.wait_all;" ::: "memory");  // never leave copies in flight
+            __syncwarp();
+        }
+    }
+}
+
+template <typename T, int VEC>
+int run_tail32(const SegLevel &L, const void *X, void *Y, int64_t k, int num_sms, unsigned *counter,
+               const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    constexpr int STAGE = 8;
+    auto kern = off32 ? k_tail32<T, VEC, true, STAGE> : k_tail32<T, VEC, false, STAGE>;
+    static int bps[2] = {0, 0};
+    int &b = bps[off32 ? 1 : 0];
+    if (b == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
+        if (b <= 0) b = 1;
+    }
+    const int64_t nbatch = (L.nseg + STAGE - 1) / STAGE;
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (nbatch + 7) / 8);
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
+                                           reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                           reinterpret_cast<T *>(Y), k, counter, outs);
+    return (int)cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------ K-A (short rows)
 // Rows of LPE < 32 lanes (k = 8/16/32 fp32 with 16-byte lanes): the warp still works on ONE batch,
 // and each step hands G = 32/LPE consecutive entries to its G sub-warps (one entry each), so a
@@ -784,6 +921,13 @@ int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void
     static const bool seg32 = !(std::getenv("ARROW_SEG32") && std::getenv("ARROW_SEG32")[0] == '0');
     // 32-bit X offsets when every X row offset (and D0's) fits
     const bool off32 = (uint64_t)L.max_x_row * (uint64_t)k * (dtype == 1 ? 8u : 4u) < (1ull << 32) - (1ull << 20);
+    // levels >= 1, single GPU, full-warp rows: Y slabs staged by cp.async (ARROW_TAIL_STAGE=1; measured
+    // slower on config R, 3.58 vs 2.86 ms: level 1 757 vs 506 us at 2.4 TB/s -- off by default)
+    static const bool tail_stage = std::getenv("ARROW_TAIL_STAGE") && std::getenv("ARROW_TAIL_STAGE")[0] == '1';
+    if (seg32 && tail_stage && dist == 0 && L.mode == 1 && lpe == 32 && k % (32 * vec) == 0) {
+        if (dtype == 0 && vec == 4) return run_tail32<float, 4>(L, X, Y, k, num_sms, counter, po, off32, st);
+        if (dtype == 1 && vec == 2) return run_tail32<double, 2>(L, X, Y, k, num_sms, counter, po, off32, st);
+    }
     if (seg32 && lpe == 32 && k % (32 * vec) == 0) {
         if (dtype == 0 && vec == 4)
             return run_seg32_mode<float, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, off32, st);
