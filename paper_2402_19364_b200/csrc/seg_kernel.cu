@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -621,7 +622,10 @@ int run_tail32(const SegLevel &L, const void *X, void *Y, int64_t k, int num_sms
     static int bps[2] = {0, 0};
     int &b = bps[off32 ? 1 : 0];
     if (b == 0) {
+        // 4 blocks x 32 KB of stage per SM: ask for the shared-memory carveout that holds them
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
+        if (std::getenv("ARROW_TAIL_STAGE_VERBOSE")) fprintf(stderr, "k_tail32: %d blocks/SM\n", b);
         if (b <= 0) b = 1;
     }
     const int64_t nbatch = (L.nseg + STAGE - 1) / STAGE;
