@@ -322,28 +322,11 @@ __device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T 
 
 template <typename T> struct Seg32Unroll { static constexpr int value = sizeof(T) == 4 ? 8 : 4; };
 
-// Deferred read-modify-write of a level >= 1 row (single GPU): the Y row is loaded when the segment
-// closes and added/stored at the next close (or at the batch end), so the load latency overlaps
-// the next segment's gathers instead of stalling the warp.  Rows are unique within a level.
-template <typename T, int VEC> struct PendingRmw {
-    T *p = nullptr;
-    Frag<T, VEC> y, a;
-};
-template <typename T, int VEC>
-__device__ __forceinline__ void complete_rmw(PendingRmw<T, VEC> &q) {
-    if (q.p) {
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) q.y.v[i] += q.a.v[i];
-        st_plain<T, VEC>(q.p, q.y);
-        q.p = nullptr;
-    }
-}
-
-template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool DEFER>
+template <typename T, int VEC, int MODE, int DIST, bool OFF32>
 __device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int n, unsigned grp, const char *Xc,
                                             const char *Dc, uint32_t rowbytes, uint32_t lane_off, Frag<T, VEC> &acc,
                                             int &cur, int32_t my_out, T *Y, T *C0, int64_t k, int64_t col0,
-                                            const PeerPtrs &outs, PendingRmw<T, VEC> &pend) {
+                                            const PeerPtrs &outs) {
     constexpr int UNROLL = Seg32Unroll<T>::value;
     Frag<T, VEC> xv[UNROLL];
     T av[UNROLL];
@@ -372,21 +355,14 @@ __device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int 
         }
         if ((grp >> t) & 1u) {  // (only set for t < n)
             const int32_t o = __shfl_sync(0xffffffffu, my_out, cur);
-            if (DEFER && o >= 0) {
-                complete_rmw<T, VEC>(pend);
-                pend.p = Y + (int64_t)o * k + col0;
-                pend.y = ld_plain<T, VEC>(pend.p);
-                pend.a = acc;
-            } else {
-                flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
-            }
+            flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
             acc.zero();
             ++cur;
         }
     }
 }
 
-template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool DEFER, bool PF>
+template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool PF>
 __global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ seg_out,
                                                   const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                   const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
@@ -419,7 +395,6 @@ __global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ se
             Frag<T, VEC> acc;
             acc.zero();
             int cur = 0;
-            PendingRmw<T, VEC> pend;
             // PF: the next chunk's (col, val) are requested one chunk ahead
             int32_t pcol = 0;
             T pval = T(0);
@@ -447,12 +422,11 @@ __global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ se
 #pragma unroll 1
                 for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
                     const unsigned grp = (endmask >> u0) & ((1u << UNROLL) - 1u);
-                    seg32_group<T, VEC, MODE, DIST, OFF32, DEFER>(mycol, myval, u0, min(cnt - u0, UNROLL), grp, Xc,
+                    seg32_group<T, VEC, MODE, DIST, OFF32>(mycol, myval, u0, min(cnt - u0, UNROLL), grp, Xc,
                                                                   Dc, rowbytes, lane_off, acc, cur, my_out, Y, C0, k,
-                                                                  col0, outs, pend);
+                                                                  col0, outs);
                 }
             }
-            if (DEFER) complete_rmw<T, VEC>(pend);
         }
     }
 }
@@ -461,18 +435,15 @@ template <typename T, int VEC, int MODE, int DIST>
 int run_seg32(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
               unsigned *counter, int bseg, const PeerPtrs &outs, bool off32, cudaStream_t st) {
     if (bseg <= 0 || bseg > 32) bseg = 32;
-    // deferred row RMW for the single-GPU levels >= 1
-    // (measured: no gain on config R, 2.84 vs 2.82 ms K-A -- off unless ARROW_SEG_DEFER=1)
-    static const bool defer_env = std::getenv("ARROW_SEG_DEFER") && std::getenv("ARROW_SEG_DEFER")[0] == '1';
+    // (a deferred read-modify-write of level >= 1 rows -- the Y load issued when a segment closes and
+    // completed at the next close -- measured no gain on config R, 2.84 vs 2.82 ms K-A; removed)
     // entry prefetch one chunk ahead (ARROW_SEG32_PF=1; measured neutral-to-worse at k = 128 -- the
     // full-warp kernel's chunk has four 8-row gather groups, so the entry load was 1 of 5 latencies)
     static const bool pf = std::getenv("ARROW_SEG32_PF") && std::getenv("ARROW_SEG32_PF")[0] == '1';
-    constexpr bool kDefer = MODE == 1 && DIST == 0;
-    auto kern = (kDefer && defer_env) ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, kDefer, false> : k_seg32<T, VEC, MODE, DIST, false, kDefer, false>)
-              : pf ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, false, true> : k_seg32<T, VEC, MODE, DIST, false, false, true>)
-                   : (off32 ? k_seg32<T, VEC, MODE, DIST, true, false, false> : k_seg32<T, VEC, MODE, DIST, false, false, false>);
-    static int bps[6] = {0, 0, 0, 0, 0, 0};
-    int &b = bps[(off32 ? 1 : 0) + (kDefer && defer_env ? 2 : (pf ? 4 : 0))];
+    auto kern = pf ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, true> : k_seg32<T, VEC, MODE, DIST, false, true>)
+                   : (off32 ? k_seg32<T, VEC, MODE, DIST, true, false> : k_seg32<T, VEC, MODE, DIST, false, false>);
+    static int bps[4] = {0, 0, 0, 0};
+    int &b = bps[(off32 ? 1 : 0) + (pf ? 2 : 0)];
     if (b == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
         if (b <= 0) b = 1;
