@@ -556,6 +556,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     if (!comm) {
         if (use_seg) {
             if (const char *b2 = std::getenv("ARROW_SEG_BS")) P->seg_bseg = std::atoi(b2);
+            if (const char *b3 = std::getenv("ARROW_SEG_BS_TAIL")) P->seg_bseg_tail = std::atoi(b3);
             const size_t es = P->esize();
             // last launch that writes each Y row: 2*launch + (1 if as a head-row partial); a body
             // segment in its row's last launch is marked final (kFinalBit, arrow_spmm_iterate
@@ -976,7 +977,8 @@ static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t
         }
         prof_begin(P, st, a);
         if (!P->seg.empty())
-            e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, P->seg_bseg, st,
+            e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i,
+                           (i > 0 && P->seg_bseg_tail > 0) ? P->seg_bseg_tail : P->seg_bseg, st,
                            nullptr, act, zfold_rows, zfold_n);
         else
             e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);

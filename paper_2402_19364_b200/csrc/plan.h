@@ -67,6 +67,7 @@ struct arrow_plan_s {
     int64_t stage_k = 0;
     std::vector<void *> seg_allocs;
     int seg_bseg = 16;
+    int seg_bseg_tail = 0;  // segments per batch in levels >= 1 (0: seg_bseg)
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
     void *ws = nullptr;          // D0 | C0
     int64_t ws_k = 0;
