@@ -216,6 +216,44 @@ def one_d_baseline(g, X, k, dtype, world, rank, dev, flop, steps=10):
         return {"impl": "1D-row baseline", "unavailable": str(e)[:200]}
 
 
+def one_five_d_baseline(g, X, k, dtype, world, rank, dev, flop, steps=10):
+    """NEXT-4 comparator: the paper's 1.5D A-stationary SpMM with c = floor(sqrt(p))
+     -- NCCL broadcasts along grid columns, cuSPARSE local products, an all-reduce of the
+    Y tile (comparators/one_five_d.py).  Device-timed like our step (barrier + CUDA events, max over
+    ranks); the ledger is the bytes a rank receives per step vs P:322's beta term."""
+    import torch
+    import torch.distributed as dist
+    try:
+        from comparators.one_five_d import OneFiveD
+        tdt = torch.float64 if dtype == "f64" else torch.float32
+        op = OneFiveD(g.n, g.row_ptr, g.col, g.val, k, tdt, rank, world, dev)
+        r0, r1 = op.row_range
+        Xt = torch.from_numpy(np.ascontiguousarray(X[r0:r1])).to(dev)
+        for _ in range(3):
+            op.step(Xt)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            op.step(Xt)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        led = op.ledger(8 if dtype == "f64" else 4)
+        mx = torch.tensor([led["bcast_recv_bytes"] + led["allreduce_bytes"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        del op, Xt
+        torch.cuda.empty_cache()
+        return {"impl": f"1.5D A-stationary (c={led['c']}, {led['rounds']} round(s)): NCCL broadcast + cuSPARSE + all-reduce",
+                "ms_per_step": round(ms, 4), "value": round(flop / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                "recv_bytes_per_gpu_max": int(mx.item()), "predicted_beta_bytes": led["predicted_beta_bytes"]}
+    except Exception as e:
+        return {"impl": "1.5D A-stationary baseline", "unavailable": str(e)[:200]}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the oracle as it stands, on this arm's config and metric (rank 0 only)."""
     if rank != 0:
@@ -445,9 +483,10 @@ def main():
                "bytes_per_gpu_per_direction_max": int(mine.item()), "bytes_predicted_per_gpu_per_direction": int(pred),
                "t_bound_ms_at_900GBs": round(float(mine.item()) / 900e9 * 1e3, 4),
                "note": "rank-0 row counts; bytes = max over ranks of (forward + reverse rows) x k x s + head blocks"}
-    oned = None
+    oned = oned15 = None
     if world > 1 and not args.no_lib_baseline:
         oned = one_d_baseline(g, X, k, dtype, world, rank, dev, flop)
+        oned15 = one_five_d_baseline(g, X, k, dtype, world, rank, dev, flop)
     lib = None
     if rank == 0 and world == 1 and not args.no_lib_baseline:
         lib = cusparse_baseline(g, Xd, k, flop, stream)
@@ -479,6 +518,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "library_baseline": lib if world == 1 else oned,
+            "baseline_1_5d": oned15,
             "iterate": it,
             "nvlink": nvl,
             "create_seconds": round(info["create_seconds"], 2),
