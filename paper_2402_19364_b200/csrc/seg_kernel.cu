@@ -322,7 +322,7 @@ __device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T 
 
 template <typename T> struct Seg32Unroll { static constexpr int value = sizeof(T) == 4 ? 8 : 4; };
 
-template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool YP>
+template <typename T, int VEC, int MODE, int DIST, bool OFF32>
 __device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int n, unsigned grp, const char *Xc,
                                             const char *Dc, uint32_t rowbytes, uint32_t lane_off, Frag<T, VEC> &acc,
                                             int &cur, int32_t my_out, T *Y, T *C0, int64_t k, int64_t col0,
@@ -347,22 +347,6 @@ __device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int 
             for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
         return;
     }
-    // YP (levels >= 1, read-modify-write): the Y rows of every body segment that ends in this group
-    // are requested right after the gathers, so the group's flushes wait on one overlapped latency
-    // instead of one DRAM round trip each (a body row has exactly one segment per launch, so no
-    // flush of this group can write a row another preloaded one reads)
-    Frag<T, VEC> yv[YP ? UNROLL : 1];
-    if constexpr (YP) {
-        int c2 = cur;
-#pragma unroll
-        for (int t = 0; t < UNROLL; ++t) {
-            if ((grp >> t) & 1u) {  // warp-uniform
-                const int32_t o = __shfl_sync(0xffffffffu, my_out, c2 & 31);
-                ++c2;
-                if (o >= 0) yv[t] = ld_plain<T, VEC>(Y + (int64_t)(DIST == 0 ? (o & kRowMask30) : o) * k + col0);
-            }
-        }
-    }
 #pragma unroll
     for (int t = 0; t < UNROLL; ++t) {
         if (t < n) {
@@ -371,23 +355,15 @@ __device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int 
         }
         if ((grp >> t) & 1u) {  // (only set for t < n)
             const int32_t o = __shfl_sync(0xffffffffu, my_out, cur);
-            if (YP && o >= 0) {
-                Frag<T, VEC> y = yv[YP ? t : 0];
-#pragma unroll
-                for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
-                if (DIST == 0 && (o & kFinalBit) && outs.act) apply_act<T, VEC>(y, outs.act);
-                st_plain<T, VEC>(Y + (int64_t)(DIST == 0 ? (o & kRowMask30) : o) * k + col0, y);
-            } else {
-                flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
-            }
+            flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
             acc.zero();
             ++cur;
         }
     }
 }
 
-template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool PF, bool YP = false>
-__global__ void __launch_bounds__(256, YP ? 3 : 4) k_seg32(const int32_t *__restrict__ seg_out,
+template <typename T, int VEC, int MODE, int DIST, bool OFF32, bool PF>
+__global__ void __launch_bounds__(256, 4) k_seg32(const int32_t *__restrict__ seg_out,
                                                   const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                   const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
                                                   const T *__restrict__ X, const T *__restrict__ D0,
@@ -446,7 +422,7 @@ __global__ void __launch_bounds__(256, YP ? 3 : 4) k_seg32(const int32_t *__rest
 #pragma unroll 1
                 for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
                     const unsigned grp = (endmask >> u0) & ((1u << UNROLL) - 1u);
-                    seg32_group<T, VEC, MODE, DIST, OFF32, YP>(mycol, myval, u0, min(cnt - u0, UNROLL), grp, Xc,
+                    seg32_group<T, VEC, MODE, DIST, OFF32>(mycol, myval, u0, min(cnt - u0, UNROLL), grp, Xc,
                                                                   Dc, rowbytes, lane_off, acc, cur, my_out, Y, C0, k,
                                                                   col0, outs);
                 }
@@ -460,19 +436,17 @@ int run_seg32(const SegLevel &L, const void *X, const void *D0, void *Y, void *C
               unsigned *counter, int bseg, const PeerPtrs &outs, bool off32, cudaStream_t st) {
     if (bseg <= 0 || bseg > 32) bseg = 32;
     // (a deferred read-modify-write of level >= 1 rows -- the Y load issued when a segment closes and
-    // completed at the next close -- measured no gain on config R, 2.84 vs 2.82 ms K-A; removed)
+    // completed at the next close -- measured no gain on config R, 2.84 vs 2.82 ms K-A; removed.
+    // Preloading the Y rows of every segment ending in an 8-entry group together with its gathers
+    // needs 80 registers (3 blocks/SM): level 1 0.66 vs 0.50 ms, step 3.17 vs 2.88 ms; removed,
+    // profiles/r01/ab_yp/)
     // entry prefetch one chunk ahead (ARROW_SEG32_PF=1; measured neutral-to-worse at k = 128 -- the
     // full-warp kernel's chunk has four 8-row gather groups, so the entry load was 1 of 5 latencies)
     static const bool pf = std::getenv("ARROW_SEG32_PF") && std::getenv("ARROW_SEG32_PF")[0] == '1';
-    // Y-row preload for levels >= 1 (ARROW_SEG32_YP=1; see seg32_group)
-    static const bool yp_env = std::getenv("ARROW_SEG32_YP") && std::getenv("ARROW_SEG32_YP")[0] == '1';
-    constexpr bool kYP = MODE != 0 && DIST != 2;
-    const bool yp = kYP && yp_env;
     auto kern = pf ? (off32 ? k_seg32<T, VEC, MODE, DIST, true, true> : k_seg32<T, VEC, MODE, DIST, false, true>)
                    : (off32 ? k_seg32<T, VEC, MODE, DIST, true, false> : k_seg32<T, VEC, MODE, DIST, false, false>);
-    if (yp) kern = off32 ? k_seg32<T, VEC, MODE, DIST, true, false, kYP> : k_seg32<T, VEC, MODE, DIST, false, false, kYP>;
-    static int bps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int &b = bps[(off32 ? 1 : 0) + (pf ? 2 : 0) + (yp ? 4 : 0)];
+    static int bps[4] = {0, 0, 0, 0};
+    int &b = bps[(off32 ? 1 : 0) + (pf ? 2 : 0)];
     if (b == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
         if (b <= 0) b = 1;
