@@ -133,6 +133,16 @@ arrow_status arrow_spmm_ex(arrow_plan plan, const void *X, void *Y, int64_t k, v
  * Device staging buffers are owned by the plan and reused. */
 arrow_status arrow_spmm_host(arrow_plan plan, const void *X_host, void *Y_host, int64_t k, void *stream);
 
+/* Batched end-to-end call: Y_host[c] = A X_host[c] for c = 0..count-1, each an n x k HOST buffer
+ * of the plan's dtype (pinned memory needed for the overlap), e.g. several feature matrices
+ * multiplied by the same A (preprocessing amortised over many products).  Single-GPU plans
+ * pipeline the copies with the kernels through two device slots owned by the plan: the H2D copy
+ * of X[c+1] and the D2H copy of Y[c-1] run on two copy streams while the kernels of c run on
+ * `stream` (PCIe is full duplex).  Distributed plans run the items one by one (arrow_spmm_host).
+ * Synchronises `stream` before returning.  count < 0 or a NULL pointer: ARROW_E_INVALID_ARG. */
+arrow_status arrow_spmm_host_batch(arrow_plan plan, const void *const *X_host, void *const *Y_host,
+                                   int64_t count, int64_t k, void *stream);
+
 /* Iterated SpMM with a fused activation (the paper's use case of repeated
  * products with the rows left in pi_0 order):  X_{t+1} = act(A X_t), t = 0..iters-1.
  * X and Y are both n x k device buffers of the plan's dtype (row order of the plan: original,

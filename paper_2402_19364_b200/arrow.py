@@ -35,7 +35,7 @@ SYMBOLS = [
     "arrow_decomposition_export_level", "arrow_decomposition_export_residual", "arrow_decomposition_save",
     "arrow_decomposition_load", "arrow_decomposition_destroy", "arrow_plan_create_from", "arrow_comm_unique_id",
     "arrow_comm_create", "arrow_comm_destroy", "arrow_status_string", "arrow_last_error", "arrow_abi_version",
-    "arrow_dist_schedule", "arrow_spmm_iterate", "arrow_decompose_ex",
+    "arrow_dist_schedule", "arrow_spmm_iterate", "arrow_decompose_ex", "arrow_spmm_host_batch",
 ]
 
 
@@ -98,6 +98,7 @@ def lib() -> ctypes.CDLL:
             "arrow_spmm": [p, p, p, i64],
             "arrow_spmm_ex": [p, p, p, i64, p],
             "arrow_spmm_host": [p, p, p, i64, p],
+            "arrow_spmm_host_batch": [p, p, p, i64, i64, p],
             "arrow_plan_destroy": [p],
             "arrow_plan_set_stream": [p, p],
             "arrow_plan_reserve": [p, i64],
@@ -404,6 +405,27 @@ class Plan:
             Y = np.empty((rows, k), self.np_dtype)
         _check(lib().arrow_spmm_host(self._h, X.ctypes.data, Y.ctypes.data, k, stream_ptr), "arrow_spmm_host")
         return Y
+
+    def spmm_host_batch(self, Xs, Ys=None, stream_ptr: int = 0):
+        """Y_c = A X_c for a list of host buffers, copies pipelined with the kernels
+        (arrow_spmm_host_batch; pinned buffers give the overlap)."""
+        rows = self.local_end - self.local_begin
+        Xs = [np.ascontiguousarray(X, dtype=self.np_dtype) for X in Xs]
+        if not Xs:
+            return []
+        k = Xs[0].shape[1]
+        for X in Xs:
+            if X.shape != (rows, k):
+                raise ValueError(f"every X must be {rows} x {k}")
+        if Ys is None:
+            Ys = [np.empty((rows, k), self.np_dtype) for _ in Xs]
+        if len(Ys) != len(Xs) or any(Y.shape != (rows, k) or Y.dtype != self.np_dtype or not Y.flags.c_contiguous
+                                     for Y in Ys):
+            raise ValueError("Ys must match Xs (shape, dtype, C-contiguous)")
+        xp = (ctypes.c_void_p * len(Xs))(*[X.ctypes.data for X in Xs])
+        yp = (ctypes.c_void_p * len(Ys))(*[Y.ctypes.data for Y in Ys])
+        _check(lib().arrow_spmm_host_batch(self._h, xp, yp, len(Xs), k, stream_ptr), "arrow_spmm_host_batch")
+        return Ys
 
     def set_profiling(self, on: bool):
         _check(lib().arrow_plan_set_profiling(self._h, int(on)), "arrow_plan_set_profiling")

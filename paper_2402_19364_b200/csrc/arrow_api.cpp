@@ -1030,7 +1030,7 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
         P->stage_k = k;
     }
     static const bool graphs = !(std::getenv("ARROW_GRAPHS") && std::getenv("ARROW_GRAPHS")[0] == '0');
-    if (graphs && !P->profiling && st != nullptr) {
+    if (graphs && !P->profiling && !P->no_graph && st != nullptr) {
         if (P->gexec && P->g_x == X && P->g_y == Y && P->g_k == k && P->g_stream == st) {
             CUDA_TRY(cudaGraphLaunch(P->gexec, st));
             return ARROW_OK;
@@ -1125,6 +1125,77 @@ arrow_status arrow_spmm_host(arrow_plan P, const void *Xh, void *Yh, int64_t k, 
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
     return ARROW_OK;
+}
+
+arrow_status arrow_spmm_host_batch(arrow_plan P, const void *const *Xh, void *const *Yh, int64_t count, int64_t k,
+                                   void *stream) {
+    if (!P) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
+    if (count < 0) return fail(ARROW_E_INVALID_ARG, "count < 0");
+    if (k < 0) return fail(ARROW_E_INVALID_ARG, "k < 0");
+    if (count == 0 || k == 0 || P->n == 0) return ARROW_OK;
+    if (!Xh || !Yh) return fail(ARROW_E_INVALID_ARG, "X or Y list is NULL");
+    for (int64_t c = 0; c < count; ++c)
+        if (!Xh[c] || !Yh[c]) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
+    if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
+    if (P->dist || count == 1) {
+        for (int64_t c = 0; c < count; ++c) {
+            const arrow_status s = arrow_spmm_host(P, Xh[c], Yh[c], k, stream);
+            if (s != ARROW_OK) return s;
+        }
+        return ARROW_OK;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t rows = P->local_end - P->local_begin;
+    const size_t bytes = (size_t)(rows * k * (int64_t)P->esize());
+    if (k > P->hb_k) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        for (int i = 0; i < 2; ++i) {
+            if (P->hb_x[i]) { cudaFree(P->hb_x[i]); P->hb_x[i] = nullptr; }
+            if (P->hb_y[i]) { cudaFree(P->hb_y[i]); P->hb_y[i] = nullptr; }
+        }
+        P->hb_k = 0;
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaMalloc(&P->hb_x[i], std::max<size_t>(bytes, 1)));
+            CUDA_TRY(cudaMalloc(&P->hb_y[i], std::max<size_t>(bytes, 1)));
+        }
+        P->hb_k = k;
+    }
+    if (!P->hb_h2d) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&P->hb_h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&P->hb_d2h, cudaStreamNonBlocking));
+        for (cudaEvent_t &e : P->hb_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaEvent_t *ex = P->hb_ev, *ec = P->hb_ev + 2, *ey = P->hb_ev + 4, e_start = P->hb_ev[6];
+    // everything already queued on `stream` comes first
+    CUDA_TRY(cudaEventRecord(e_start, st));
+    CUDA_TRY(cudaStreamWaitEvent(P->hb_h2d, e_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(P->hb_d2h, e_start, 0));
+    // the slots alternate; a graph keyed by (X, Y) would be re-captured every item
+    struct NoGraph { arrow_plan p; ~NoGraph() { p->no_graph = false; } } guard{P};
+    P->no_graph = true;
+    arrow_status status = ARROW_OK;
+    for (int64_t c = 0; c < count && status == ARROW_OK; ++c) {
+        const int s = (int)(c & 1);
+        if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(P->hb_h2d, ec[s], 0));  // kernels of c-2 done reading slot s
+        CUDA_TRY(cudaMemcpyAsync(P->hb_x[s], Xh[c], bytes, cudaMemcpyHostToDevice, P->hb_h2d));
+        CUDA_TRY(cudaEventRecord(ex[s], P->hb_h2d));
+        CUDA_TRY(cudaStreamWaitEvent(st, ex[s], 0));
+        if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(st, ey[s], 0));          // Y of c-2 copied out of slot s
+        status = arrow_spmm_ex(P, P->hb_x[s], P->hb_y[s], k, stream);
+        if (status != ARROW_OK) break;
+        CUDA_TRY(cudaEventRecord(ec[s], st));
+        CUDA_TRY(cudaStreamWaitEvent(P->hb_d2h, ec[s], 0));
+        CUDA_TRY(cudaMemcpyAsync(Yh[c], P->hb_y[s], bytes, cudaMemcpyDeviceToHost, P->hb_d2h));
+        CUDA_TRY(cudaEventRecord(ey[s], P->hb_d2h));
+    }
+    // join both copy streams back into `stream`, then wait for everything
+    CUDA_TRY(cudaEventRecord(e_start, P->hb_d2h));
+    CUDA_TRY(cudaStreamWaitEvent(st, e_start, 0));
+    CUDA_TRY(cudaEventRecord(e_start, P->hb_h2d));
+    CUDA_TRY(cudaStreamWaitEvent(st, e_start, 0));
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
+    return status;
 }
 
 arrow_status arrow_plan_info(arrow_plan P, arrow_plan_info_t *info) {

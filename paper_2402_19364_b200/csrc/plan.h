@@ -73,6 +73,12 @@ struct arrow_plan_s {
     int64_t ws_k = 0;
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
+    // arrow_spmm_host_batch: two device slots, two copy streams, per-slot events
+    void *hb_x[2] = {nullptr, nullptr}, *hb_y[2] = {nullptr, nullptr};
+    int64_t hb_k = 0;
+    cudaStream_t hb_h2d = nullptr, hb_d2h = nullptr;
+    cudaEvent_t hb_ev[7] = {};  // x[2], c[2], y[2], start/done
+    bool no_graph = false;
     cudaStream_t stream = nullptr;
     // single GPU: the level-0 zero rows that K-A does not touch (entry-less / A-isolated rows) are
     // written on a side stream next to level 0 (HBM writes under an L2-bound kernel)
@@ -105,6 +111,10 @@ struct arrow_plan_s {
         if (ws) cudaFree(ws);
         if (host_x) cudaFree(host_x);
         if (host_y) cudaFree(host_y);
+        for (int i = 0; i < 2; ++i) { if (hb_x[i]) cudaFree(hb_x[i]); if (hb_y[i]) cudaFree(hb_y[i]); }
+        for (cudaEvent_t e : hb_ev) if (e) cudaEventDestroy(e);
+        if (hb_h2d) cudaStreamDestroy(hb_h2d);
+        if (hb_d2h) cudaStreamDestroy(hb_d2h);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (post_rows) cudaFree(post_rows);
         if (stage) cudaFree(stage);

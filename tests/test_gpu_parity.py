@@ -155,6 +155,30 @@ def test_host_entry_point_and_repeat():
         assert np.array_equal(run(p64, X), oracle.spmm(g.n, g.row_ptr, g.col, g.val, X))
 
 
+def test_host_batch_pipelined():
+    """arrow_spmm_host_batch: every item equals O1 bitwise (fp64, dyadic), with pinned and pageable
+    host buffers, an odd count (both slots reused), then k changing; fp32 within 1e-4."""
+    g = datagen.rmat(12, 8, 5)
+    p64 = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f64")
+    for k, pinned in ((16, True), (16, False), (40, True)):
+        Xs = [datagen.make_x(g.n, k, s_x=100 + c) for c in range(5)]
+        if pinned:
+            Xs = [torch.from_numpy(X).pin_memory().numpy() for X in Xs]
+            Ys = [torch.empty((g.n, k), dtype=torch.float64).pin_memory().numpy() for _ in Xs]
+        else:
+            Ys = None
+        Ys = p64.spmm_host_batch(Xs, Ys)
+        for X, Y in zip(Xs, Ys):
+            assert np.array_equal(Y, oracle.spmm(g.n, g.row_ptr, g.col, g.val, X))
+    p32 = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f32")
+    Xs = [datagen.make_x(g.n, 128, s_x=7 + c, dtype=np.float32) for c in range(3)]
+    for X, Y in zip(Xs, p32.spmm_host_batch(Xs)):
+        check_fp32(g, Y, X)
+    assert p32.spmm_host_batch([]) == []
+    with pytest.raises(ValueError):
+        p32.spmm_host_batch([Xs[0], Xs[0][:, :64]])
+
+
 def test_profiling_counters():
     g = datagen.rmat(12, 8, 5)
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f32")
