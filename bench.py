@@ -126,13 +126,13 @@ def cpu_oracle_baseline(g, X, k, budget_s=12.0, max_reps=10):
     """O1 (oracle/spmm_ref.c, fp64, OpenMP over rows) on the host cores: full SpMMs repeated
     until ~budget_s of CPU work (bounded sample of the same workload)."""
     import oracle
-    threads = oracle.num_threads()
-    oracle.spmm(g.n, g.row_ptr, g.col, g.val, X[: min(g.n, 1024)] if False else X)  # warm-up (page-in)
+    threads = len(os.sched_getaffinity(0))
+    oracle.spmm(g.n, g.row_ptr, g.col, g.val, X, nthreads=threads)  # warm-up (page-in)
     times = []
     t_all = time.perf_counter()
     while len(times) < max_reps and (time.perf_counter() - t_all) < budget_s:
         t0 = time.perf_counter()
-        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X, nthreads=threads)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
     gflops = 2.0 * g.nnz * k / t / 1e9
@@ -274,14 +274,16 @@ def run_reference(args, cfg, rank, world):
     k, dtype = args.k or cfg["k"], args.dtype or cfg["dtype"]
     g, X = make_inputs(cfg, k, dtype)
     import oracle
-    threads = oracle.num_threads()
-    oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)  # page-in
+    # every host core this process may use: torchrun sets OMP_NUM_THREADS=1 for each rank, which
+    # would time the oracle on one core when the driver launches the reference arm with N > 1
+    threads = len(os.sched_getaffinity(0))
+    oracle.spmm(g.n, g.row_ptr, g.col, g.val, X, nthreads=threads)  # page-in
     times = []
     for _ in range(args.warmup):
-        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X, nthreads=threads)
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)
+        oracle.spmm(g.n, g.row_ptr, g.col, g.val, X, nthreads=threads)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     flop = 2.0 * g.nnz * k
