@@ -310,7 +310,7 @@ def main():
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--dtype", default="", choices=["", "f32", "f64"])
     ap.add_argument("--impl", default="arrow", choices=["arrow", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order", default="original", choices=["original", "permuted"],
                     help="X/Y row order: original vertex ids, or pi_0 order (R18; forced when distributed)")
