@@ -439,7 +439,8 @@ int run_seg32(const SegLevel &L, const void *X, const void *D0, void *Y, void *C
     // completed at the next close -- measured no gain on config R, 2.84 vs 2.82 ms K-A; removed.
     // Preloading the Y rows of every segment ending in an 8-entry group together with its gathers
     // needs 80 registers (3 blocks/SM): level 1 0.66 vs 0.50 ms, step 3.17 vs 2.88 ms; removed,
-    // profiles/r01/ab_yp/)
+    // profiles/r01/ab_yp/.  An L2 evict-first policy (createpolicy + .L2::cache_hint) on those Y
+    // loads/stores: 2.85/2.85/2.92 vs 2.86/2.87/2.87 ms, neutral; removed, profiles/r01/yef/)
     // entry prefetch one chunk ahead (ARROW_SEG32_PF=1; measured neutral-to-worse at k = 128 -- the
     // full-warp kernel's chunk has four 8-row gather groups, so the entry load was 1 of 5 latencies)
     static const bool pf = std::getenv("ARROW_SEG32_PF") && std::getenv("ARROW_SEG32_PF")[0] == '1';
