@@ -321,6 +321,8 @@ def main():
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
     ap.add_argument("--batch-segments", type=int, default=0)
+    ap.add_argument("--flags", type=int, default=0, help="arrow_options.flags (ARROW_FLAG_*)")
+    ap.add_argument("--prefetch-batches", type=int, default=0, help="K-A L2 prefetch distance (0 auto, <0 off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -354,7 +356,7 @@ def main():
         # one host decomposition for the node: rank 0 computes and checkpoints it, the others load it
         # (arrow_decomposition_save/load), instead of G processes decomposing the same A at once
         import tempfile
-        path = [os.path.join(tempfile.gettempdir(), f"arrow_bench_{os.getpid()}.dec") if rank == 0 else None]
+        path = [os.path.join(tempfile.mkdtemp(prefix="arrow_bench_"), "A.dec") if rank == 0 else None]
         dist.broadcast_object_list(path, src=0)
         if rank == 0:
             dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"])
@@ -365,10 +367,11 @@ def main():
         dist.barrier()
         if rank == 0:
             os.remove(path[0])
+            os.rmdir(os.path.dirname(path[0]))
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
                    window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
-                   band=args.band)
+                   band=args.band, prefetch_batches=args.prefetch_batches, flags=args.flags)
     info = plan.info()
     lo, hi = plan.local_begin, plan.local_end
     if comm is not None or args.order == "permuted":
@@ -543,6 +546,7 @@ def main():
                          "peak_source": peak_src},
             "kernel_ms_per_step": {kname: round(kt[kname]["ms"] / max(1, kt["calls"]), 4)
                                    for kname in ("head_stage", "segments", "head_epilogue", "comm")},
+            "per_launch_ms": kt["launch_ms"],
             "gpu_launches": int(sum(kt[kname]["launches"] for kname in ("head_stage", "segments", "head_epilogue"))),
             "clocks": clk,
             "e2e": e2e,

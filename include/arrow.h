@@ -46,7 +46,8 @@ typedef enum {
     ARROW_E_UNSUPPORTED = 9     /* size beyond the implementation's index widths, feature not built */
 } arrow_status;
 
-typedef enum { ARROW_F32 = 0, ARROW_F64 = 1 } arrow_dtype;
+typedef enum { ARROW_DTYPE_DEFAULT = -1,  /* options.compute only: same as A's dtype */
+               ARROW_F32 = 0, ARROW_F64 = 1 } arrow_dtype;
 
 /* Canonical CSR of A, host memory, borrowed.  row_ptr[0] = 0, nondecreasing,
  * row_ptr[n] = nnz; col_idx in [0, n), strictly increasing within each row (no
@@ -83,10 +84,27 @@ typedef struct {
     int32_t residual;           /* ARROW_RESIDUAL_*; default ERROR */
     int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (16384) */
     int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32) */
-    int32_t batch_segments;     /* segments per work batch of the segment-stream kernel; 0 = default */
+    int32_t batch_segments;     /* segments per K-A work batch: 0 = default (16) or a power of two <= 32 */
     int32_t band;               /* ARROW_BAND_*: step 3's band; default BLOCK */
-    int32_t reserved[5];
+    int32_t flags;              /* ARROW_FLAG_* bits; default 0 */
+    int32_t transport;          /* ARROW_TRANSPORT_* (distributed plans); default AUTO */
+    int32_t prefetch_batches;   /* staged single-GPU schedule: L2 prefetch distance of K-A in work batches
+                                   (> 0: batch b prefetches the rows first gathered in batch b + distance);
+                                   0 = off (default; measured slower on B200) */
+    int32_t reserved[2];
 } arrow_options;
+
+/* options.flags */
+enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each call directly instead of
+                                          replaying one CUDA graph per (X, Y, k, stream) */
+       ARROW_FLAG_STAGED = 2,          /* single GPU schedule: levels >= 1 in one launch into staging rows
+                                          that level 0 adds (instead of one read-modify-write launch per level) */
+       ARROW_FLAG_KA_BROADCAST = 4,    /* full-warp rows: entries read by broadcast 16-byte loads (k_ka)
+                                          instead of coalesced loads + shuffles (k_seg32) */
+       ARROW_FLAGS_ALL = 7 };
+/* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
+ * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
+enum { ARROW_TRANSPORT_AUTO = 0, ARROW_TRANSPORT_P2P = 1, ARROW_TRANSPORT_NCCL = 2 };
 
 /* Fill *opt with the defaults above (compute = ARROW_F32 until a CSR is seen: callers that
  * want "same as A" leave compute = -1 after this call, which is what the default sets). */
@@ -112,7 +130,9 @@ arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, ar
  * Workspaces are sized for the largest k seen; call arrow_plan_reserve before graph capture. */
 arrow_status arrow_spmm(arrow_plan plan, const void *X, void *Y, int64_t k);
 
-/* Synchronises the plan's device work, frees everything.  NULL is a no-op. */
+/* Synchronises the plan's device work, frees everything.  NULL is a no-op.  For a distributed plan
+ * of the P2P transport the call is COLLECTIVE (every rank must call it, before arrow_comm_destroy):
+ * peers read each other's workspaces, so no rank frees its own until all have drained. */
 arrow_status arrow_plan_destroy(arrow_plan plan);
 
 /* ---------------------------------------------------------------- extended */

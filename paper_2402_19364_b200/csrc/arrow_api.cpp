@@ -44,11 +44,11 @@ arrow_status arrow::set_error(arrow_status s, const std::string &msg) { return f
 namespace {
 
 struct BuiltLevel {
-    std::vector<uint32_t> keys;
+    std::vector<uint32_t> keys;    // record stream (arrow_internal.h)
     std::vector<uint8_t> vals;     // plan dtype
-    std::vector<uint32_t> bstart;  // batch boundaries (record offsets)
-    std::vector<int32_t> head_rows;
     std::vector<int32_t> zero_rows;
+    std::vector<int64_t> wseg;     // [NW + 1] first segment of each tile window (stream order)
+    std::vector<int64_t> wpos;     // [NW + 1] first position of each window's rows (>= head)
     int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0, nseg = 0;
     int mode = 0;
 };
@@ -62,30 +62,12 @@ inline void put_val(std::vector<uint8_t> &dst, int64_t at, arrow_dtype pdt, doub
     }
 }
 
-// Cut the record stream into batches of >= target records, at pseudo records.  Small levels get
-// smaller batches (down to 32 records) so that every resident warp has a few batches to take.
-void cut_batches(BuiltLevel &B, int32_t target) {
-    const int64_t warps = 148 * 32;
-    target = (int32_t)std::max<int64_t>(32, std::min<int64_t>(target, (int64_t)B.keys.size() / (warps * 4)));
-    B.bstart.clear();
-    B.bstart.push_back(0);
-    const int64_t m = (int64_t)B.keys.size();
-    int64_t start = 0;
-    for (int64_t r = 0; r < m; ++r) {
-        if ((B.keys[r] & kPseudoRec) && (r + 1 - start >= target || r + 1 == m)) {
-            B.bstart.push_back((uint32_t)(r + 1));
-            start = r + 1;
-        }
-    }
-}
-
 // Window-ordered record stream of one arrow level (encoding: arrow_internal.h).
 //   dist = 0: head columns read X directly, head-row partials add into Y[perm_i[j]];
 //             level 0 zeroes head rows and entry-less rows first (zero_rows).
 //   dist = 1: head columns read the staged head block D0, head partials add into C0[j].
 void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_rows, int32_t head_chunk,
-                 int32_t batch_records, const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, bool tail_atomic,
-                 BuiltLevel &B) {
+                 const std::vector<int32_t> *pos0, arrow_dtype pdt, int dist, BuiltLevel &B) {
     const int64_t n_i = L.n_i, h = L.head, rows = L.rows;
     B.rows = rows;
     B.n_i = n_i;
@@ -101,8 +83,6 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
     auto headkey = [&](int64_t j) -> uint32_t {
         return kPseudoRec | kAuxRec | (dist ? (uint32_t)j : rowid(L.perm[j]));
     };
-    B.head_rows.resize(h);
-    for (int64_t j = 0; j < h; ++j) B.head_rows[j] = (int32_t)rowid(L.perm[j]);
     if (level_idx == 0) {
         if (!dist)
             for (int64_t j = 0; j < h; ++j) B.zero_rows.push_back((int32_t)rowid(L.perm[j]));
@@ -135,6 +115,9 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
     for (int64_t w = 0; w < NW; ++w) { wrec[w + 1] += wrec[w]; wseg[w + 1] += wseg[w]; }
     const int64_t nrec = wrec[NW];
     B.nseg = wseg[NW];
+    B.wseg = wseg;
+    B.wpos.resize(NW + 1);
+    for (int64_t w = 0; w <= NW; ++w) B.wpos[w] = std::min(n_i, std::max(h, w * W));
     B.keys.resize(nrec);
     B.vals.assign(nrec * (pdt == ARROW_F64 ? 8 : 4), 0);
 #pragma omp parallel for schedule(dynamic, 1)
@@ -149,9 +132,8 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
         for (int64_t p = std::max(h, lo); p < hi; ++p) {
             if (L.row_ptr[p + 1] == L.row_ptr[p]) continue;
             for (int64_t x = L.row_ptr[p]; x < L.row_ptr[p + 1]; ++x) entry(x);
-            // levels >= 1 add into Y rows written by earlier levels: a fire-and-forget L2 reduction
-            // (tail_atomic) or a read-modify-write
-            B.keys[r++] = kPseudoRec | ((tail_atomic && level_idx > 0) ? kAuxRec : 0u) | rowid(L.perm[p]);
+            // level 0 stores the row; levels >= 1 read-modify-write it (S5)
+            B.keys[r++] = kPseudoRec | rowid(L.perm[p]);
         }
         for (int64_t j = 0; j < h; ++j) {
             const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
@@ -165,12 +147,11 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
             }
         }
     }
-    cut_batches(B, batch_records);
 }
 
 // Residual CSR level (ARROW_RESIDUAL_CSR): every row with leftover entries is one RMW segment.
 void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *pos0, arrow_dtype pdt,
-                    int32_t batch_records, bool tail_atomic, BuiltLevel &B) {
+                    BuiltLevel &B) {
     auto rowid = [&](int32_t v) -> uint32_t { return (uint32_t)(pos0 ? (*pos0)[v] : v); };
     const size_t m = D.res_u.size();
     B.mode = 1;
@@ -182,36 +163,13 @@ void build_residual(const arrow_decomposition_s &D, const std::vector<int32_t> *
         B.vals.resize(B.keys.size() * es);
         put_val(B.vals, (int64_t)B.keys.size() - 1, pdt, D.res_a[t]);
         if (t + 1 == m || D.res_u[t + 1] != D.res_u[t]) {
-            B.keys.push_back(kPseudoRec | (tail_atomic ? kAuxRec : 0u) | rowid(D.res_u[t]));
+            B.keys.push_back(kPseudoRec | rowid(D.res_u[t]));
             B.vals.resize(B.keys.size() * es, 0);
             ++B.nseg;
         }
     }
     B.rows = B.nseg;
     B.n_i = B.nseg;
-    cut_batches(B, batch_records);
-}
-
-// Concatenate the record streams of levels 1.. (all flushes are L2 reductions, so their order does
-// not matter) into one launch; batch boundaries are rebased.
-BuiltLevel merge_tail(std::vector<BuiltLevel> &built) {
-    BuiltLevel M;
-    M.mode = 1;
-    M.bstart.push_back(0);
-    for (size_t i = 1; i < built.size(); ++i) {
-        BuiltLevel &B = built[i];
-        const uint32_t base = (uint32_t)M.keys.size();
-        M.keys.insert(M.keys.end(), B.keys.begin(), B.keys.end());
-        M.vals.insert(M.vals.end(), B.vals.begin(), B.vals.end());
-        for (size_t j = 1; j < B.bstart.size(); ++j) M.bstart.push_back(base + B.bstart[j]);
-        M.nseg += B.nseg;
-        M.nnz += B.nnz;
-        M.rows += B.rows;
-        M.n_i += B.n_i;
-        std::vector<uint32_t>().swap(B.keys);
-        std::vector<uint8_t>().swap(B.vals);
-    }
-    return M;
 }
 
 arrow_status validate_args(const arrow_csr *A, int64_t b, int32_t levels) {
@@ -230,93 +188,6 @@ arrow_status validate_args(const arrow_csr *A, int64_t b, int32_t levels) {
 }  // namespace
 
 // ------------------------------------------------------------------------------------ ABI
-
-// Single GPU, "staged tail": the levels >= 1 run as ONE launch, concurrently with level 0 (which
-// is bound by the L1/TEX data pipe while the tail is latency-bound), writing each body row into
-// its own staging row (plain stores, no read-modify-write) and each head-row partial into a
-// per-(level, head) staging row (atomics); one CSR gather-add then adds every staged row into
-// Y in level order.  Segment lists are concatenated level by level (window order inside each).
-static arrow_status build_stage_tail(arrow_plan P, const std::vector<std::vector<int32_t>> &so,
-                                     const std::vector<std::vector<uint32_t>> &se,
-                                     const std::vector<std::vector<int32_t>> &ec,
-                                     const std::vector<std::vector<uint8_t>> &ev) {
-    const int nl = (int)so.size();
-    // staging rows: one per (level, head row) for the head partials (zeroed every call), then one
-    // per (level, body row)
-    std::vector<int32_t> stamp((size_t)P->n, -1), hidx((size_t)P->n, -1), hrow;
-    for (int i = 0; i < nl; ++i)
-        for (int32_t o : so[i])
-            if (o < 0) {
-                const int32_t r = o & 0x7fffffff;
-                if (stamp[r] != i) { stamp[r] = i; hrow.push_back(r); }
-            }
-    const int64_t nhead = (int64_t)hrow.size();
-    std::fill(stamp.begin(), stamp.end(), -1);
-    std::vector<int32_t> mso, mec;
-    std::vector<uint32_t> mse;
-    std::vector<uint8_t> mev;
-    std::vector<std::pair<int32_t, int32_t>> contrib;  // (Y row, staging row), level order
-    int64_t nbody = 0, ebase = 0, nh = 0;
-    for (int i = 0; i < nl; ++i) {
-        for (size_t t = 0; t < so[i].size(); ++t) {
-            const int32_t o = so[i][t];
-            if (o < 0) {  // head-row partial of one window: atomically into its (level, row) staging row
-                const int32_t r = o & 0x7fffffff;
-                if (stamp[r] != i) { stamp[r] = i; hidx[r] = (int32_t)nh++; }
-                mso.push_back((int32_t)(kFlag | (uint32_t)hidx[r]));
-            } else {  // body row: stored into its own staging row
-                const int32_t sr = (int32_t)(nhead + nbody++);
-                mso.push_back(sr);
-                contrib.emplace_back((int32_t)(o & (int32_t)kRowMask30), sr);
-            }
-            mse.push_back((uint32_t)(ebase + se[i][t]));
-        }
-        mec.insert(mec.end(), ec[i].begin(), ec[i].end());
-        mev.insert(mev.end(), ev[i].begin(), ev[i].end());
-        ebase += (int64_t)ec[i].size();
-    }
-    for (int64_t h = 0; h < nhead; ++h) contrib.emplace_back(hrow[h], (int32_t)h);
-    if (ebase >= ((int64_t)1 << 32)) return fail(ARROW_E_UNSUPPORTED, "staged tail exceeds 2^32 entries");
-    if (nhead + nbody >= ((int64_t)1 << 30)) return fail(ARROW_E_UNSUPPORTED, "staged tail exceeds 2^30 rows");
-    // CSR of contributions by Y row; within a row: body rows in level order, then head partials
-    std::stable_sort(contrib.begin(), contrib.end(),
-                     [](const std::pair<int32_t, int32_t> &a, const std::pair<int32_t, int32_t> &b) { return a.first < b.first; });
-    std::vector<int32_t> ptr(1, 0), src, dst;
-    for (const auto &c : contrib) {
-        if (dst.empty() || dst.back() != c.first) {
-            if (!dst.empty()) ptr.push_back((int32_t)src.size());
-            dst.push_back(c.first);
-        }
-        src.push_back(c.second);
-    }
-    if (!dst.empty()) ptr.push_back((int32_t)src.size());
-    auto up = [&](const void *data, size_t bytes) -> void * {
-        void *d = nullptr;
-        if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
-        P->seg_allocs.push_back(d);
-        if (bytes) cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice);
-        return d;
-    };
-    SegLevel T;
-    T.nseg = (int64_t)mso.size();
-    T.mode = 0;
-    T.max_x_row = P->n;
-    T.seg_out = (int32_t *)up(mso.data(), mso.size() * 4);
-    T.seg_end = (uint32_t *)up(mse.data(), mse.size() * 4);
-    T.ent_col = (int32_t *)up(mec.data(), mec.size() * 4);
-    T.ent_val = up(mev.data(), mev.size());
-    P->tail_ptr = (int32_t *)up(ptr.data(), ptr.size() * 4);
-    P->tail_src = (int32_t *)up(src.data(), src.size() * 4);
-    P->tail_dst = (int32_t *)up(dst.data(), dst.size() * 4);
-    if (!T.seg_out || !T.seg_end || !T.ent_col || !T.ent_val || !P->tail_ptr || !P->tail_src || !P->tail_dst)
-        return fail(ARROW_E_CUDA, "cudaMalloc(staged tail)");
-    P->tail = T;
-    P->tail_on = true;
-    P->tail_nhead = nhead;
-    P->tail_rows = nhead + nbody;
-    P->tail_ndst = (int64_t)dst.size();
-    return ARROW_OK;
-}
 
 extern "C" {
 
@@ -342,7 +213,7 @@ int32_t arrow_abi_version(void) { return ARROW_ABI_VERSION; }
 arrow_status arrow_options_default(arrow_options *opt) {
     if (!opt) return fail(ARROW_E_INVALID_ARG, "opt is NULL");
     std::memset(opt, 0, sizeof(*opt));
-    opt->compute = (arrow_dtype)-1;
+    opt->compute = ARROW_DTYPE_DEFAULT;
     opt->seed = 4;
     opt->order = ARROW_ORDER_ORIGINAL;
     opt->residual = ARROW_RESIDUAL_ERROR;
@@ -405,6 +276,311 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
     return ARROW_OK;
 }
 
+// Structural checks of a decomposition before a plan is built from it (a loaded file is only
+// checksummed): every perm_i injective into [0, n), sizes ordered n_i <= rows_i <= n and
+// head_i <= n_i, CSR offsets from 0 nondecreasing to nnz_i, positions in [0, rows_i), residual
+// entries in [0, n).  Returns 0 if valid, else 1 with `err` set.
+static int validate_decomposition(const arrow_decomposition_s &D, std::string &err) {
+    const int64_t n = D.n;
+    std::vector<int32_t> seen((size_t)std::max<int64_t>(n, 0), -1);
+    for (size_t i = 0; i < D.levels.size(); ++i) {
+        const HostLevel &L = D.levels[i];
+        const std::string at = "level " + std::to_string(i) + ": ";
+        if (L.rows < 0 || L.rows > n || L.n_i < 0 || L.n_i > L.rows || L.head < 0 || L.head > L.n_i) {
+            err = at + "sizes out of range";
+            return 1;
+        }
+        if ((int64_t)L.perm.size() != L.rows || (int64_t)L.row_ptr.size() != L.rows + 1 || L.row_ptr[0] != 0) {
+            err = at + "array sizes";
+            return 1;
+        }
+        for (int64_t p = 0; p < L.rows; ++p) {
+            const int32_t v = L.perm[p];
+            if (v < 0 || v >= n || seen[v] == (int32_t)i) {
+                err = at + "perm is not injective into [0, n)";
+                return 1;
+            }
+            seen[v] = (int32_t)i;
+            if (L.row_ptr[p + 1] < L.row_ptr[p]) {
+                err = at + "row_ptr decreases";
+                return 1;
+            }
+        }
+        if (L.row_ptr[L.rows] != (int64_t)L.col.size() || L.col.size() != L.val.size()) {
+            err = at + "row_ptr[rows] != nnz";
+            return 1;
+        }
+        for (int32_t q : L.col)
+            if (q < 0 || q >= L.rows) {
+                err = at + "column position out of range";
+                return 1;
+            }
+    }
+    if (D.res_u.size() != D.res_v.size() || D.res_u.size() != D.res_a.size()) {
+        err = "residual array sizes";
+        return 1;
+    }
+    for (size_t t = 0; t < D.res_u.size(); ++t)
+        if (D.res_u[t] < 0 || D.res_u[t] >= n || D.res_v[t] < 0 || D.res_v[t] >= n) {
+            err = "residual entry out of range";
+            return 1;
+        }
+    return 0;
+}
+
+// Single-GPU schedule, level by level (default): K-A level 0 stores every Y row it owns, then one
+// K-A launch per level >= 1 adds its rows into Y (read-modify-write, in level order) -- Alg. 2's
+// reverse aggregation with the permutations folded into the output rows (S4, S5).
+static arrow_status build_single_gpu_rmw(arrow_plan P, std::vector<BuiltLevel> &built, int bs) {
+    const size_t es = P->esize();
+    const size_t nlv = built.size();
+    {
+        const BuiltLevel &B = built[0];
+        const int64_t zb = align_up(std::max<int64_t>((int64_t)B.zero_rows.size() * 4, 1), 256);
+        const int64_t total = zb + align_up((int64_t)(nlv + 1) * 4, 256);
+        cudaError_t e = cudaMalloc(&P->arena, (size_t)total);
+        if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(plan arena): ") + cudaGetErrorString(e));
+        P->arena_bytes = total;
+        for (size_t li = 0; li < nlv; ++li) {
+            DeviceLevel L = P->meta[li];
+            L.zero_rows = reinterpret_cast<int32_t *>(P->arena);
+            L.nzero = li == 0 ? (int64_t)B.zero_rows.size() : 0;
+            P->levels.push_back(L);
+        }
+        CUDA_TRY(cudaMemcpy(P->arena, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
+        P->counters = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(P->arena) + zb);
+    }
+    // the last launch writing each Y row: 2 * level + (1 if as a head-row partial); a body segment in
+    // its row's last launch is final (kFinalBit: arrow_spmm_iterate applies the activation when it is
+    // flushed); rows last written by head partials get a post pass
+    std::vector<int32_t> last((size_t)P->n, -1);
+    for (size_t li = 0; li < nlv; ++li)
+        for (const uint32_t key : built[li].keys)
+            if (key & kPseudoRec) last[key & (kAuxRec - 1)] = (int32_t)(2 * li + ((key & kAuxRec) ? 1 : 0));
+    std::vector<int32_t> post_rows;
+    for (int64_t r = 0; r < P->n; ++r)
+        if (last[r] >= 0 && (last[r] & 1)) post_rows.push_back((int32_t)r);
+    for (size_t li = 0; li < nlv; ++li) {
+        BuiltLevel &B = built[li];
+        HostSegs hs;
+        hs.ent_val.reserve(B.vals.size());
+        for (size_t r = 0; r < B.keys.size(); ++r) {
+            const uint32_t key = B.keys[r];
+            if (key & kPseudoRec) {
+                const uint32_t row = key & (kAuxRec - 1);
+                const bool fin = !(key & kAuxRec) && last[row] == (int32_t)(2 * li);
+                hs.seg_out.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (fin ? kFinalBit : 0u) | row));
+                hs.seg_end.push_back((uint32_t)hs.ent_col.size());
+            } else {
+                hs.ent_col.push_back((int32_t)(key & (kAuxRec - 1)));
+                hs.ent_val.insert(hs.ent_val.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
+            }
+        }
+        std::vector<uint32_t>().swap(B.keys);
+        std::vector<uint8_t>().swap(B.vals);
+        SegLevel S;
+        std::string err;
+        const int e = upload_seg_level(hs, (int)es, bs, li == 0 ? 0 : 1, P->seg_allocs, S, err);
+        if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
+        P->seg.push_back(S);
+    }
+    P->n_post = (int64_t)post_rows.size();
+    if (P->n_post) {
+        CUDA_TRY(cudaMalloc(&P->post_rows, post_rows.size() * 4));
+        CUDA_TRY(cudaMemcpy(P->post_rows, post_rows.data(), post_rows.size() * 4, cudaMemcpyHostToDevice));
+    }
+    return ARROW_OK;
+}
+
+// Single-GPU schedule: levels >= 1 first, ONE K-A launch over all of them, writing
+// every body row into its own staging row and every head-row partial (atomically) into a per-(level,
+// head row) staging row; then K-A level 0, whose body row r ends with one pseudo-entry (staging row,
+// value 1) per level >= 1 that contributes to r, so that Y[r] is written exactly once, as
+//     Y[r] = sum_{level 0 entries} a X[c]  +  sum_{i >= 1} (P_{pi_i} Y_i)[r]        (Eq. (1))
+// -- Alg. 2's reverse aggregation of the level results done in registers instead of a
+// read-modify-write of Y per level.  Body staging rows are numbered in level 0's consumption order,
+// so level 0 reads them front to back.  Rows with contributions but no level-0 entries get a
+// level-0 segment of pseudo-entries only (appended after the windows).
+static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &built, int bs,
+                                     const arrow_decomposition_s &D, const std::vector<int32_t> *pos0) {
+    (void)D;
+    (void)pos0;
+    // L2 prefetch distance in batches (layout.cpp); off by default (measured slower)
+    const int64_t ahead = P->prefetch_batches > 0 ? P->prefetch_batches : 0;
+    const size_t es = P->esize();
+    const int64_t n = P->n;
+    const size_t nlv = built.size();
+    // zero-row list and the work counters (level 0 and the merged levels >= 1)
+    // contributions of levels >= 1 per output row, in level order: head slot (>= 0) or ~(body sequence)
+    std::vector<int64_t> cptr((size_t)n + 1, 0);
+    std::vector<int32_t> stamp((size_t)n, -1);  // level that last gave the row a head slot
+    std::vector<int64_t> hslot((size_t)n, -1);  // that head slot
+    for (size_t li = 1; li < nlv; ++li)
+        for (const uint32_t key : built[li].keys)
+            if (key & kPseudoRec) {
+                const uint32_t row = key & (kAuxRec - 1);
+                if (key & kAuxRec) {  // one contribution per (level, head row), however many chunks
+                    if (stamp[row] == (int32_t)li) continue;
+                    stamp[row] = (int32_t)li;
+                }
+                cptr[row + 1] += 1;
+            }
+    for (int64_t r = 0; r < n; ++r) cptr[r + 1] += cptr[r];
+    const int64_t ncontrib = cptr[n];
+    std::vector<int64_t> citem((size_t)ncontrib);
+    std::vector<int64_t> cfill(cptr.begin(), cptr.end() - 1);
+    int64_t nhead_slots = 0, nbody = 0;
+    std::fill(stamp.begin(), stamp.end(), -1);
+    for (size_t li = 1; li < nlv; ++li)
+        for (const uint32_t key : built[li].keys)
+            if (key & kPseudoRec) {
+                const uint32_t row = key & (kAuxRec - 1);
+                if (key & kAuxRec) {
+                    if (stamp[row] == (int32_t)li) continue;
+                    stamp[row] = (int32_t)li;
+                    hslot[row] = nhead_slots;
+                    citem[cfill[row]++] = nhead_slots++;
+                } else {
+                    citem[cfill[row]++] = ~nbody++;
+                }
+            }
+    // staging rows: [0, nhead_slots) head partials (zeroed every call), then body rows in level-0 order
+    std::vector<int64_t> body_slot((size_t)nbody, -1);
+    int64_t next_slot = nhead_slots;
+    std::vector<uint8_t> one(es);
+    put_val(one, 0, P->dtype, 1.0);
+    HostSegs h0;
+    std::vector<uint8_t> has_seg((size_t)n, 0);
+    auto append_staging = [&](uint32_t row) {
+        for (int64_t c = cptr[row]; c < cptr[row + 1]; ++c) {
+            int64_t slot = citem[c];
+            if (slot < 0) {
+                int64_t &bsl = body_slot[(size_t)~slot];
+                bsl = next_slot++;
+                slot = bsl;
+            }
+            h0.ent_col.push_back((int32_t)(kFlag | (uint32_t)slot));
+            h0.ent_val.insert(h0.ent_val.end(), one.begin(), one.end());
+        }
+    };
+    {
+        BuiltLevel &B = built[0];
+        h0.ent_val.reserve(B.vals.size() + (size_t)ncontrib * es);
+        for (size_t r = 0; r < B.keys.size(); ++r) {
+            const uint32_t key = B.keys[r];
+            if (key & kPseudoRec) {
+                const uint32_t row = key & (kAuxRec - 1);
+                // level 0 is every row's last write: body rows are final (iterate's activation)
+                if (!(key & kAuxRec)) {
+                    append_staging(row);
+                    has_seg[row] = 1;
+                }
+                h0.seg_out.push_back((int32_t)(((key & kAuxRec) ? kFlag : kFinalBit) | row));
+                h0.seg_end.push_back((uint32_t)h0.ent_col.size());
+            } else {
+                h0.ent_col.push_back((int32_t)(key & (kAuxRec - 1)));
+                h0.ent_val.insert(h0.ent_val.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
+            }
+        }
+        // rows with level >= 1 contributions but no level-0 entries: segments of pseudo-entries only.
+        // (A level-0 head row never has any: its entries are all captured at level 0.)
+        for (int64_t t = 0; t < std::min<int64_t>(B.head, (int64_t)B.zero_rows.size()); ++t)
+            if (cptr[B.zero_rows[t] + 1] > cptr[B.zero_rows[t]]) return fail(ARROW_E_STATE, "internal: level-0 head row with later contributions");
+        for (int64_t row = 0; row < n; ++row)
+            if (!has_seg[row] && cptr[row + 1] > cptr[row]) {
+                append_staging((uint32_t)row);
+                h0.seg_out.push_back((int32_t)(kFinalBit | (uint32_t)row));
+                h0.seg_end.push_back((uint32_t)h0.ent_col.size());
+                has_seg[row] = 2;
+            }
+        for (const int64_t v : body_slot)
+            if (v < 0) return fail(ARROW_E_STATE, "internal: a level >= 1 row without a level-0 reader");
+        // level-0 zero rows: its head rows first (they receive the head-row partials atomically), then
+        // the rows nothing writes
+        std::vector<int32_t> z(B.zero_rows.begin(), B.zero_rows.begin() + std::min<int64_t>(B.head, (int64_t)B.zero_rows.size()));
+        for (size_t t = z.size(); t < B.zero_rows.size(); ++t)
+            if (has_seg[B.zero_rows[t]] != 2) z.push_back(B.zero_rows[t]);
+        B.zero_rows.swap(z);
+        std::vector<uint32_t>().swap(B.keys);
+        std::vector<uint8_t>().swap(B.vals);
+    }
+    P->stage_rows = next_slot;
+    P->stage_head_rows = nhead_slots;
+    h0.pf_ahead = ahead;
+    // levels >= 1 (+ residual), concatenated in level order: body rows -> their staging rows (stores),
+    // head-row chunks -> their level's head staging rows (L2 reductions)
+    HostSegs ht;
+    {
+        int64_t seq = 0, hbase = 0;
+        for (size_t li = 1; li < nlv; ++li) {
+            BuiltLevel &B = built[li];
+            if (li > 1) ht.level_seg.push_back((int64_t)ht.seg_out.size());
+            int64_t nh = 0;
+            for (size_t r = 0; r < B.keys.size(); ++r) {
+                const uint32_t key = B.keys[r];
+                if (key & kPseudoRec) {
+                    const uint32_t row = key & (kAuxRec - 1);
+                    int64_t slot = -1;
+                    if (key & kAuxRec) {  // head slots of a level are numbered in first-chunk order
+                        if (stamp[row] != (int32_t)(nlv + li)) {
+                            stamp[row] = (int32_t)(nlv + li);
+                            hslot[row] = hbase + nh++;
+                        }
+                        slot = hslot[row];
+                        ht.seg_out.push_back((int32_t)(kFlag | (uint32_t)slot));
+                    } else {
+                        slot = body_slot[(size_t)seq++];
+                        ht.seg_out.push_back((int32_t)slot);
+                    }
+                    ht.seg_end.push_back((uint32_t)ht.ent_col.size());
+                } else {
+                    ht.ent_col.push_back((int32_t)(key & (kAuxRec - 1)));
+                    ht.ent_val.insert(ht.ent_val.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
+                }
+            }
+            hbase += nh;
+            std::vector<uint32_t>().swap(B.keys);
+            std::vector<uint8_t>().swap(B.vals);
+        }
+    }
+    ht.pf_ahead = ahead;
+    if (P->stage_rows >= (int64_t)kRowMask30) return fail(ARROW_E_UNSUPPORTED, "staging rows exceed 2^30");
+    // device: zero rows + counters (arena), then the two segment layouts
+    {
+        const BuiltLevel &B = built[0];
+        const int64_t zb = align_up(std::max<int64_t>((int64_t)B.zero_rows.size() * 4, 1), 256);
+        const int64_t total = zb + 256;
+        cudaError_t e = cudaMalloc(&P->arena, (size_t)total);
+        if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(plan arena): ") + cudaGetErrorString(e));
+        P->arena_bytes = total;
+        DeviceLevel L0 = P->meta[0];
+        L0.zero_rows = reinterpret_cast<int32_t *>(P->arena);
+        L0.nzero = (int64_t)B.zero_rows.size();
+        CUDA_TRY(cudaMemcpy(L0.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
+        P->levels.push_back(L0);
+        P->counters = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(P->arena) + zb);
+    }
+    std::string err;
+    SegLevel S0, ST;
+    int e = upload_seg_level(h0, (int)es, bs, 0, P->seg_allocs, S0, err);
+    if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
+    P->seg.push_back(S0);
+    if (!ht.seg_out.empty()) {
+        e = upload_seg_level(ht, (int)es, bs, 0, P->seg_allocs, ST, err);
+        if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
+        P->seg.push_back(ST);
+    }
+    // iterate mode: rows last written by head-row partials (level 0's head rows) get a post pass
+    std::vector<int32_t> post_rows(built[0].zero_rows.begin(),
+                                   built[0].zero_rows.begin() + std::min<int64_t>(built[0].head, (int64_t)built[0].zero_rows.size()));
+    P->n_post = (int64_t)post_rows.size();
+    if (P->n_post) {
+        CUDA_TRY(cudaMalloc(&P->post_rows, post_rows.size() * 4));
+        CUDA_TRY(cudaMemcpy(P->post_rows, post_rows.data(), post_rows.size() * 4, cudaMemcpyHostToDevice));
+    }
+    return ARROW_OK;
+}
+
 static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_options *opt_in, arrow_dtype default_dt,
                               arrow_comm comm, arrow_plan *out) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -418,25 +594,25 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         return fail(ARROW_E_INVALID_ARG, "bad options.order");
     if (opt.window_rows < 0 || opt.head_chunk < 0 || opt.batch_segments < 0)
         return fail(ARROW_E_INVALID_ARG, "negative window/chunk/batch");
+    if (opt.batch_segments > 32 || (opt.batch_segments & (opt.batch_segments - 1)) != 0)
+        return fail(ARROW_E_INVALID_ARG, "options.batch_segments must be 0 or a power of two <= 32");
+    if ((opt.flags & ~ARROW_FLAGS_ALL) != 0) return fail(ARROW_E_INVALID_ARG, "unknown options.flags bits");
+    if (opt.transport < ARROW_TRANSPORT_AUTO || opt.transport > ARROW_TRANSPORT_NCCL)
+        return fail(ARROW_E_INVALID_ARG, "bad options.transport");
     const int64_t window_rows = opt.window_rows > 0 ? opt.window_rows : kDefaultWindowRows;
     const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : kDefaultHeadChunk;
-    const int32_t batch_records = opt.batch_segments > 0 ? opt.batch_segments : kDefaultBatchRecords;
+    const int bs = opt.batch_segments > 0 ? opt.batch_segments : kDefaultBatchSegs;
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
     const int64_t n = D.n, b = D.b;
-    // levels >= 1: L2 reductions instead of read-modify-write, all of them in one launch
-    // (measured worse on B200: L2 atomic throughput on 3M body rows > the RMW it saves; off by default)
-    bool tail_atomic = false;
-    if (const char *e = std::getenv("ARROW_TAIL_ATOMIC")) tail_atomic = !comm && std::atoi(e) != 0;
-    // kernel family: "seg" (default, descriptor layout) or "rec"/"stream"/"tma" (record-stream layout)
-    std::string ka = "seg";
-    if (const char *e = std::getenv("ARROW_KA")) ka = e;
-    const bool use_seg = (ka == "seg");
     if (n >= kMaxRows) return fail(ARROW_E_UNSUPPORTED, "n must be < 2^30 (30-bit row keys)");
+    if (std::string e; validate_decomposition(D, e)) return fail(ARROW_E_INVALID_ARG, "invalid decomposition: " + e);
 
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     std::unique_ptr<arrow_plan_s> P;
     std::vector<BuiltLevel> built;
+    std::vector<int32_t> pos0;
+    const std::vector<int32_t> *pos0p = nullptr;
     try {
         P.reset(new arrow_plan_s());
         P->device = dev;
@@ -446,10 +622,13 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         P->n = n;
         P->b = b;
         P->isolated = D.isolated;
+        P->use_graphs = (opt.flags & ARROW_FLAG_NO_GRAPHS) == 0;
+        P->staged = (opt.flags & ARROW_FLAG_STAGED) != 0 && !comm;
+        P->launch.kernel = (opt.flags & ARROW_FLAG_KA_BROADCAST) ? 1 : 0;
+        P->transport = opt.transport;
+        P->prefetch_batches = opt.prefetch_batches;
         P->nnz = (int64_t)D.res_u.size();
         for (auto &L : D.levels) P->nnz += L.row_ptr[L.rows];
-        std::vector<int32_t> pos0;
-        const std::vector<int32_t> *pos0p = nullptr;
         if (order == ARROW_ORDER_PERMUTED && !D.levels.empty()) {
             pos0.assign(n, 0);
             for (int64_t p = 0; p < n; ++p) pos0[D.levels[0].perm[p]] = (int32_t)p;
@@ -457,9 +636,8 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         }
         built.resize(D.levels.size() + (D.res_u.empty() ? 0 : 1));
         for (size_t i = 0; i < D.levels.size(); ++i)
-            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, batch_records, pos0p, pdt, comm ? 1 : 0, tail_atomic,
-                        built[i]);
-        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, batch_records, tail_atomic, built.back());
+            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, pos0p, pdt, comm ? 1 : 0, built[i]);
+        if (!D.res_u.empty()) build_residual(D, pos0p, pdt, built.back());
         P->residual_nnz = (int64_t)D.res_u.size();
         P->arrow_levels = (int32_t)D.levels.size();
         P->host_levels.resize(D.levels.size());
@@ -490,148 +668,18 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         P->bytes_alg_rows += n;  // level-0 store of every Y row
     }
 
-    // per-level metadata for introspection; device launch list (levels >= 1 merged when atomic)
+    // per-level metadata (introspection; single GPU: also the launch list)
     for (const BuiltLevel &B : built) {
         DeviceLevel L;
         L.rows = B.rows; L.n_i = B.n_i; L.head = B.head; L.nnz = B.nnz; L.head_nnz = B.head_nnz;
         L.tiles = B.tiles; L.nseg = B.nseg; L.mode = B.mode;
-        L.nrec = (int64_t)B.keys.size();
-        L.nbatch = (int64_t)B.bstart.size() - 1;
         L.nzero = (int64_t)B.zero_rows.size();
         P->meta.push_back(L);
     }
-    if (tail_atomic && built.size() > 2) {
-        BuiltLevel M = merge_tail(built);
-        built.resize(1);
-        built.push_back(std::move(M));
-    }
 
-    if (!comm) {
-    // upload: one arena for all launch levels
-    {
-        const size_t es = P->esize();
-        int64_t total = 0;
-        auto reserve = [&](int64_t bytes) { int64_t at = total; total += align_up(std::max<int64_t>(bytes, 1), 256); return at; };
-        std::vector<std::array<int64_t, 5>> offs(built.size());
-        for (size_t i = 0; i < built.size(); ++i) {
-            const BuiltLevel &B = built[i];
-            offs[i][0] = reserve(use_seg ? 0 : (int64_t)B.keys.size() * 4);
-            offs[i][1] = reserve(use_seg ? 0 : (int64_t)B.vals.size());
-            offs[i][2] = reserve(use_seg ? 0 : (int64_t)B.bstart.size() * 4);
-            offs[i][3] = reserve((int64_t)B.head_rows.size() * 4);
-            offs[i][4] = reserve((int64_t)B.zero_rows.size() * 4);
-        }
-        const int64_t off_counters = reserve((int64_t)(built.size() + 1) * 4);
-        if (total > 0) {
-            cudaError_t e = cudaMalloc(&P->arena, (size_t)total);
-            if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(plan arena): ") + cudaGetErrorString(e));
-        }
-        P->arena_bytes = total;
-        char *base = reinterpret_cast<char *>(P->arena);
-        for (size_t i = 0; i < built.size(); ++i) {
-            const BuiltLevel &B = built[i];
-            DeviceLevel L;
-            L.rows = B.rows; L.n_i = B.n_i; L.head = B.head; L.nnz = B.nnz; L.head_nnz = B.head_nnz;
-            L.tiles = B.tiles; L.nseg = B.nseg; L.mode = B.mode;
-            L.nrec = (int64_t)B.keys.size();
-            L.nbatch = (int64_t)B.bstart.size() - 1;
-            L.nzero = (int64_t)B.zero_rows.size();
-            L.keys = reinterpret_cast<uint32_t *>(base + offs[i][0]);
-            L.vals = base + offs[i][1];
-            L.bstart = reinterpret_cast<uint32_t *>(base + offs[i][2]);
-            L.head_rows = reinterpret_cast<int32_t *>(base + offs[i][3]);
-            L.zero_rows = reinterpret_cast<int32_t *>(base + offs[i][4]);
-            if (!use_seg) {
-                CUDA_TRY(cudaMemcpy(L.keys, B.keys.data(), B.keys.size() * 4, cudaMemcpyHostToDevice));
-                CUDA_TRY(cudaMemcpy(L.vals, B.vals.data(), B.vals.size(), cudaMemcpyHostToDevice));
-                CUDA_TRY(cudaMemcpy(L.bstart, B.bstart.data(), B.bstart.size() * 4, cudaMemcpyHostToDevice));
-            }
-            CUDA_TRY(cudaMemcpy(L.head_rows, B.head_rows.data(), B.head_rows.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(L.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
-            P->levels.push_back(L);
-        }
-        P->counters = reinterpret_cast<unsigned *>(base + off_counters);
-    }
-    }
-    if (!comm) {
-        if (use_seg) {
-            if (const char *b2 = std::getenv("ARROW_SEG_BS")) P->seg_bseg = std::atoi(b2);
-            if (const char *b3 = std::getenv("ARROW_SEG_BS_TAIL")) P->seg_bseg_tail = std::atoi(b3);
-            const size_t es = P->esize();
-            // last launch that writes each Y row: 2*launch + (1 if as a head-row partial); a body
-            // segment in its row's last launch is marked final (kFinalBit, arrow_spmm_iterate
-            // applies the activation when it is flushed); rows last written by head partials are
-            // listed for a post pass
-            std::vector<int32_t> last((size_t)P->n, -1);
-            for (size_t li = 0; li < built.size(); ++li)
-                for (const uint32_t key : built[li].keys)
-                    if (key & kPseudoRec) last[key & (kAuxRec - 1)] = (int32_t)(2 * li + ((key & kAuxRec) ? 1 : 0));
-            // levels >= 1 as one staged launch next to level 0 (ARROW_TAIL=stage; see build_stage_tail).
-            // Measured at config R: level 0 + tail 2.70 ms together (vs 2.84 ms in sequence) but the
-            // final gather-add costs 0.47 ms -- off by default.
-            const char *tenv = std::getenv("ARROW_TAIL");
-            const bool stage_tail = built.size() > 2 && tenv && std::string(tenv) == "stage";
-            std::vector<std::vector<int32_t>> tail_so, tail_ec;
-            std::vector<std::vector<uint32_t>> tail_se;
-            std::vector<std::vector<uint8_t>> tail_ev;
-            std::vector<int32_t> post_rows;
-            for (int64_t r = 0; r < P->n; ++r)
-                if (last[r] >= 0 && (last[r] & 1)) post_rows.push_back((int32_t)r);
-            size_t li = 0;
-            for (const BuiltLevel &B : built) {
-                std::vector<int32_t> so, ec;
-                std::vector<uint32_t> se;
-                std::vector<uint8_t> ev;
-                ev.reserve(B.vals.size());
-                for (size_t r = 0; r < B.keys.size(); ++r) {
-                    const uint32_t key = B.keys[r];
-                    if (key & kPseudoRec) {
-                        const uint32_t row = key & (kAuxRec - 1);
-                        const bool fin = !(key & kAuxRec) && last[row] == (int32_t)(2 * li);
-                        so.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (fin ? kFinalBit : 0u) | row));
-                        se.push_back((uint32_t)ec.size());
-                    } else {
-                        ec.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (key & (kAuxRec - 1))));
-                        ev.insert(ev.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
-                    }
-                }
-                SegLevel S;
-                S.nseg = (int64_t)so.size();
-                S.mode = B.mode;
-                S.max_x_row = P->n;  // entries reference rows of X [n, k]
-                auto up = [&](const void *src, size_t bytes) -> void * {
-                    void *d = nullptr;
-                    if (cudaMalloc(&d, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
-                    P->seg_allocs.push_back(d);
-                    cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice);
-                    return d;
-                };
-                S.seg_out = (int32_t *)up(so.data(), so.size() * 4);
-                S.seg_end = (uint32_t *)up(se.data(), se.size() * 4);
-                S.ent_col = (int32_t *)up(ec.data(), ec.size() * 4);
-                S.ent_val = up(ev.data(), ev.size());
-                if (!S.seg_out || !S.seg_end || !S.ent_col || !S.ent_val)
-                    return fail(ARROW_E_CUDA, "cudaMalloc(seg layout)");
-                P->seg.push_back(S);
-                if (stage_tail && li > 0) {
-                    tail_so.push_back(std::move(so));
-                    tail_se.push_back(std::move(se));
-                    tail_ec.push_back(std::move(ec));
-                    tail_ev.push_back(std::move(ev));
-                }
-                ++li;
-            }
-            if (stage_tail) {
-                arrow_status st2 = build_stage_tail(P.get(), tail_so, tail_se, tail_ec, tail_ev);
-                if (st2 != ARROW_OK) return st2;
-            }
-            P->n_post = (int64_t)post_rows.size();
-            if (P->n_post) {
-                if (cudaMalloc(&P->post_rows, post_rows.size() * 4) != cudaSuccess)
-                    return fail(ARROW_E_CUDA, "cudaMalloc(post rows)");
-                cudaMemcpy(P->post_rows, post_rows.data(), post_rows.size() * 4, cudaMemcpyHostToDevice);
-            }
-        }
+    if (!comm && !built.empty()) {
+        arrow_status st = P->staged ? build_single_gpu(P.get(), built, bs, D, pos0p) : build_single_gpu_rmw(P.get(), built, bs);
+        if (st != ARROW_OK) return st;
     }
     P->local_begin = 0;
     P->local_end = n;
@@ -641,7 +689,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         if (D.band != ARROW_BAND_BLOCK)
             return fail(ARROW_E_UNSUPPORTED, "distributed plans need ARROW_BAND_BLOCK (strict band: single GPU only)");
         P->comm = comm;
-        arrow_status cs = dist_build(P.get(), D, comm, window_rows, head_chunk);
+        arrow_status cs = dist_build(P.get(), D, comm, window_rows, head_chunk, bs);
         if (cs != ARROW_OK) return cs;
     }
     P->create_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -856,18 +904,19 @@ arrow_status arrow_plan_set_stream(arrow_plan plan, void *stream) {
     return ARROW_OK;
 }
 
+// single GPU: the staging rows of levels >= 1 (stage_rows x k), sized for the largest k seen
 static arrow_status ensure_ws(arrow_plan P, int64_t k) {
-    if (k <= P->ws_k) return ARROW_OK;
-    const int64_t bytes = 2 * align_up(std::max<int64_t>(P->max_head, 1) * k * (int64_t)P->esize(), 256);
+    if (k <= P->ws_k || P->dist || P->stage_rows == 0) return ARROW_OK;
+    const int64_t bytes = P->stage_rows * k * (int64_t)P->esize();
     if (P->ws) {
-        cudaError_t e = cudaStreamSynchronize(P->stream);
+        cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
         cudaFree(P->ws);
         P->ws = nullptr;
         P->ws_k = 0;
     }
     cudaError_t e = cudaMalloc(&P->ws, (size_t)bytes);
-    if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(workspace): ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(staging rows): ") + cudaGetErrorString(e));
     P->ws_k = k;
     return ARROW_OK;
 }
@@ -896,100 +945,72 @@ inline void prof_end(arrow_plan P, cudaStream_t st, int kid, cudaEvent_t a) {
 }
 }  // namespace
 
-static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st, int act = 0) {
+static arrow_status enqueue_rmw(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st, int act) {
     const int dt = P->dtype == ARROW_F64 ? 1 : 0;
-    if (P->profiling) P->prof_acc.calls += 1;
-    P->prof_pos = 0;
     CUDA_TRY(cudaMemsetAsync(P->counters, 0, P->levels.size() * sizeof(unsigned), st));
-    if (P->tail_on && act == 0 && P->stage && P->stage_k >= k) {
-        // K-Z, then level 0 (main stream) next to the staged tail (side stream), then the gather-add
-        const DeviceLevel &L0 = P->levels[0];
-        const size_t es = P->esize();
-        cudaEvent_t a = nullptr, a2 = nullptr;
-        int e = 0;
-        if (L0.nzero > 0) {
-            prof_begin(P, st, a);
-            e = launch_zero_rows(dt, L0.zero_rows, L0.nzero, k, Y, st);
-            prof_end(P, st, ARROW_K_HEAD_STAGE, a);
-            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
-        }
-        if (!P->side) {
-            CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
-            CUDA_TRY(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
-            CUDA_TRY(cudaEventCreateWithFlags(&P->join_ev, cudaEventDisableTiming));
-        }
-        static const int tail_sms_env = std::getenv("ARROW_TAIL_SMS") ? std::atoi(std::getenv("ARROW_TAIL_SMS")) : 0;
-        const int tail_sms = tail_sms_env > 0 ? tail_sms_env : std::max(1, P->num_sms / 4);
-        prof_begin(P, st, a2);  // K-A: from the fork to the join (level 0 and the tail run together)
-        CUDA_TRY(cudaEventRecord(P->fork_ev, st));
-        CUDA_TRY(cudaStreamWaitEvent(P->side, P->fork_ev, 0));
-        CUDA_TRY(cudaMemsetAsync(P->stage, 0, (size_t)P->tail_nhead * k * es, P->side));
-        e = launch_seg(dt, 0, P->tail, X, nullptr, P->stage, nullptr, k, tail_sms, P->counters + 1, P->seg_bseg, P->side);
-        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A tail: ") + cudaGetErrorString((cudaError_t)e)); }
-        CUDA_TRY(cudaEventRecord(P->join_ev, P->side));
-        e = launch_seg(dt, 0, P->seg[0], X, nullptr, Y, nullptr, k, P->num_sms, P->counters, P->seg_bseg, st);
-        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
-        CUDA_TRY(cudaStreamWaitEvent(st, P->join_ev, 0));
-        prof_end(P, st, ARROW_K_SEGMENTS, a2);
-        prof_begin(P, st, a);
-        e = launch_gather_add(dt, P->stage, P->tail_ptr, P->tail_src, P->tail_dst, P->tail_ndst, k, Y, st);
-        prof_end(P, st, ARROW_K_HEAD_EPI, a);
-        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("tail add: ") + cudaGetErrorString((cudaError_t)e)); }
-        return ARROW_OK;
-    }
-    const int32_t *zfold_rows = nullptr;
-    int64_t zfold_n = 0;
     for (size_t i = 0; i < P->levels.size(); ++i) {
         const DeviceLevel &L = P->levels[i];
         cudaEvent_t a = nullptr;
         int e = 0;
-        bool joined = true;
-        if (L.nzero > 0) {  // S0/S3 single GPU: head rows and entry-less rows of level 0 start at zero
-            // ARROW_KZ_OVERLAP=1: head rows (the first L.head zero rows) before level 0, which adds into
-            // them; the rest on a side stream next to level 0, joined before level 1 (measured slower on
-            // config R: 4.0 vs 3.1 ms -- a small side grid cannot keep enough stores in flight)
-            static const bool overlap = std::getenv("ARROW_KZ_OVERLAP") && std::getenv("ARROW_KZ_OVERLAP")[0] == '1';  // measured slower
-            // default: only the head rows here (level 0 adds into them); the entry-less rows are
-            // zeroed inside K-A level 0, a share per batch grab (ARROW_KZ_FOLD=0: all here)
-            static const bool fold = !(std::getenv("ARROW_KZ_FOLD") && std::getenv("ARROW_KZ_FOLD")[0] == '0');
-            const bool folding = fold && !overlap && i == 0 && !P->seg.empty() && L.nzero > L.head;
-            const int64_t nh = ((overlap || folding) && i == 0 && L.nzero > L.head) ? L.head : L.nzero;
-            if (folding) {
-                zfold_rows = L.zero_rows + nh;
-                zfold_n = L.nzero - nh;
-            }
+        // level 0's head rows start at zero (its head-row slices add into them); its entry-less rows
+        // are zeroed inside K-A level 0, a share per batch grab
+        const int64_t nh = i == 0 ? std::min<int64_t>(L.head, L.nzero) : 0;
+        if (nh > 0) {
             prof_begin(P, st, a);
-            if (nh > 0) e = launch_zero_rows(dt, L.zero_rows, nh, k, Y, st);
+            e = launch_zero_rows(dt, L.zero_rows, nh, k, Y, st);
             prof_end(P, st, ARROW_K_HEAD_STAGE, a);
-            if (!e && nh < L.nzero && !folding) {
-                if (!P->side) {
-                    CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
-                    CUDA_TRY(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
-                    CUDA_TRY(cudaEventCreateWithFlags(&P->join_ev, cudaEventDisableTiming));
-                }
-                CUDA_TRY(cudaEventRecord(P->fork_ev, st));
-                CUDA_TRY(cudaStreamWaitEvent(P->side, P->fork_ev, 0));
-                e = launch_zero_rows(dt, L.zero_rows + nh, L.nzero - nh, k, Y, P->side, P->num_sms);
-                CUDA_TRY(cudaEventRecord(P->join_ev, P->side));
-                joined = false;
-            }
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
-        if (!P->seg.empty())
-            e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i,
-                           (i > 0 && P->seg_bseg_tail > 0) ? P->seg_bseg_tail : P->seg_bseg, st,
-                           nullptr, act, zfold_rows, zfold_n);
-        else
-            e = launch_stream(dt, 0, L, X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st);
-        zfold_rows = nullptr;
-        zfold_n = 0;
+        e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st, P->launch, nullptr,
+                       act, i == 0 ? L.zero_rows + nh : nullptr, i == 0 ? L.nzero - nh : 0);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
-        if (!joined) CUDA_TRY(cudaStreamWaitEvent(st, P->join_ev, 0));
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
     }
     if (act && P->n_post) {  // iterate mode: rows last written by head-row partials
         const int e = launch_act_rows(dt, P->post_rows, P->n_post, k, act, Y, st);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("activation pass: ") + cudaGetErrorString((cudaError_t)e)); }
+    }
+    return ARROW_OK;
+}
+
+static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st, int act = 0) {
+    const int dt = P->dtype == ARROW_F64 ? 1 : 0;
+    if (P->profiling) P->prof_acc.calls += 1;
+    P->prof_pos = 0;
+    if (!P->staged) return enqueue_rmw(P, X, Y, k, st, act);
+    const DeviceLevel &L0 = P->levels[0];
+    const bool staged = P->seg.size() > 1;
+    cudaEvent_t a = nullptr;
+    int e = 0;
+    CUDA_TRY(cudaMemsetAsync(P->counters, 0, 2 * sizeof(unsigned), st));
+    if (staged) {
+        // levels >= 1 in one launch: body rows -> staging rows, head-row partials -> the zeroed
+        // head staging rows (L2 reductions)
+        prof_begin(P, st, a);
+        if (P->stage_head_rows > 0)
+            CUDA_TRY(cudaMemsetAsync(P->ws, 0, (size_t)(P->stage_head_rows * k * (int64_t)P->esize()), st));
+        e = launch_seg(dt, 0, P->seg[1], X, nullptr, P->ws, nullptr, k, P->num_sms, P->counters + 1, st, P->launch);
+        prof_end(P, st, ARROW_K_SEGMENTS, a);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A levels >= 1: ") + cudaGetErrorString((cudaError_t)e)); }
+    }
+    // S0/S3 on one GPU: level 0's head rows start at zero (its head-row slices add into them); the
+    // rows nothing writes are zeroed inside K-A level 0, a share per batch grab
+    const int64_t nh = std::min<int64_t>(L0.head, L0.nzero);
+    if (nh > 0) {
+        prof_begin(P, st, a);
+        e = launch_zero_rows(dt, L0.zero_rows, nh, k, Y, st);
+        prof_end(P, st, ARROW_K_HEAD_STAGE, a);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
+    }
+    // level 0 (the last write of every Y row): its own entries + the staged rows of levels >= 1
+    prof_begin(P, st, a);
+    e = launch_seg(dt, staged ? 3 : 0, P->seg[0], X, staged ? P->ws : nullptr, Y, nullptr, k, P->num_sms, P->counters,
+                   st, P->launch, nullptr, act, L0.zero_rows + nh, L0.nzero - nh);
+    prof_end(P, st, ARROW_K_SEGMENTS, a);
+    if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A level 0: ") + cudaGetErrorString((cudaError_t)e)); }
+    if (act && P->n_post) {  // iterate mode: rows last written by head-row partials
+        e = launch_act_rows(dt, P->post_rows, P->n_post, k, act, Y, st);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("activation pass: ") + cudaGetErrorString((cudaError_t)e)); }
     }
     return ARROW_OK;
@@ -1012,25 +1033,24 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     if (rows > 0 && xa < ya + bytes && ya < xa + bytes) return fail(ARROW_E_INVALID_ARG, "X and Y overlap");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (P->dist) return dist_spmm(P, X, Y, k, st);
-    const int dt = P->dtype == ARROW_F64 ? 1 : 0;
     if (P->levels.empty()) {
         int e = launch_zero(Y, bytes, st);
         if (e) return fail(ARROW_E_CUDA, cudaGetErrorString((cudaError_t)e));
         return ARROW_OK;
     }
-    // Single GPU: the whole call (memset + K-Z + one K-A launch per level) is captured once into a
-    // CUDA graph per (X, Y, k, stream) and replayed -- one launch instead of ~10 for the
-    // launch-bound small configs.  Off while profiling (per-kernel events) or on the legacy stream.
-    if (P->tail_on && P->stage_k < k) {  // staging rows of the staged tail (allocated outside any capture)
-        CUDA_TRY(cudaStreamSynchronize(st));
-        if (P->stage) cudaFree(P->stage);
-        P->stage = nullptr;
-        P->stage_k = 0;
-        CUDA_TRY(cudaMalloc(&P->stage, (size_t)std::max<int64_t>(P->tail_rows, 1) * k * P->esize()));
-        P->stage_k = k;
+    // Single GPU: the whole call (memsets, K-Z, the two K-A launches) is captured once into a CUDA
+    // graph per (X, Y, k, stream) and replayed.  Not while profiling (per-kernel events), on the
+    // legacy stream, or when the caller is itself capturing `st` (its graph then receives the
+    // kernels directly; the staging rows must then exist already: arrow_plan_reserve).
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (st != nullptr) CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    if (P->ws_k < k && P->stage_rows > 0) {
+        if (cap != cudaStreamCaptureStatusNone)
+            return fail(ARROW_E_STATE, "staging rows for this k not reserved before stream capture (arrow_plan_reserve)");
+        arrow_status ws = ensure_ws(P, k);
+        if (ws != ARROW_OK) return ws;
     }
-    static const bool graphs = !(std::getenv("ARROW_GRAPHS") && std::getenv("ARROW_GRAPHS")[0] == '0');
-    if (graphs && !P->profiling && !P->no_graph && st != nullptr) {
+    if (P->use_graphs && !P->profiling && !P->no_graph && st != nullptr && cap == cudaStreamCaptureStatusNone) {
         if (P->gexec && P->g_x == X && P->g_y == Y && P->g_k == k && P->g_stream == st) {
             CUDA_TRY(cudaGraphLaunch(P->gexec, st));
             return ARROW_OK;
@@ -1089,6 +1109,8 @@ arrow_status arrow_spmm_iterate(arrow_plan P, void *X, void *Y, int64_t k, int32
     CUDA_TRY(cudaGetDevice(&cur));
     if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    arrow_status ws = ensure_ws(P, k);
+    if (ws != ARROW_OK) return ws;
     for (int32_t t = 0; t < iters; ++t) {  // X_{t+1} = act(A X_t), ping-pong between X and Y
         const void *src = (t & 1) ? Y : X;
         void *dst = (t & 1) ? X : Y;
@@ -1230,8 +1252,6 @@ arrow_status arrow_plan_level_info(arrow_plan P, int32_t level, arrow_level_info
     info->head_nnz = L.head_nnz;
     info->tiles = L.tiles;
     info->segments = L.nseg;
-    info->reserved[0] = L.nrec;
-    info->reserved[1] = L.nbatch;
     return ARROW_OK;
 }
 

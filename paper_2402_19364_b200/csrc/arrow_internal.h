@@ -38,40 +38,70 @@ int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *
 int check_symmetric(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &err);
 
 // ------------------------------------------------------------------ device layout of one level
-// A level is a stream of records (key, val) in tile-window order (see stream_kernel.cuh):
+// Built on the host as a stream of records (key, val) in tile-window order:
 //   plain record  : key = X row (the folded permutation: P_pi^T X is never materialised, S4);
 //                   kAux set (distributed only) = row of the staged head block D0 = X[head_i]
 //   pseudo record : kPseudo | out row -- closes the current segment.  kAux set = head-row partial of
 //                   one tile window (Alg. 1 line 2, C^(0) = sum_t B^(0,t) D^(t)) added
 //                   atomically (single GPU: into Y[perm_i[j]]; distributed: into C0[j]); otherwise
 //                   body row p >= h_i stored (level 0) or read-modify-written (levels >= 1, S5).
-// Batches (bstart) are record ranges cut at pseudo records.
+// and converted into the segment layout below (layout.cpp).
 constexpr uint32_t kPseudoRec = 0x80000000u;
 constexpr uint32_t kFlag = 0x80000000u;
 constexpr uint32_t kAuxRec = 0x40000000u;
 constexpr int64_t kMaxRows = (int64_t)1 << 30;
+constexpr int kDefaultBatchSegs = 16;  // segments per K-A work batch (measured: 16-32 flat, 8 and 4 slower)
 
+// metadata of one level (introspection) and its level-0 zero-row list
 struct DeviceLevel {
     int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0;
-    int64_t nseg = 0, nrec = 0, nbatch = 0, nzero = 0;
+    int64_t nseg = 0, nzero = 0;
     int mode = 0;                  // 0: level 0 stores Y rows; 1: levels >= 1 read-modify-write (S5)
-    uint32_t *keys = nullptr;      // [nrec]
-    void *vals = nullptr;          // [nrec] of dtype
-    uint32_t *bstart = nullptr;    // [nbatch + 1]
-    int32_t *head_rows = nullptr;  // [head] X/Y row of head vertex j
-    int32_t *zero_rows = nullptr;  // [nzero] level 0: Y rows written as 0 before the level runs
+    int32_t *zero_rows = nullptr;  // [nzero] level 0: Y rows written as 0 (head rows first, then entry-less rows)
 };
 
-// descriptor layout of the earlier K-A ("v2", seg_kernel.cu): entries + per-segment (out, end)
+// Segment layout of one level (the K-A input).  Segments (an output row, or one window's chunk of a
+// head row; never empty) are cut into batches of `bs` consecutive segments; each batch's entries
+// are contiguous and start at a multiple of 8 entries (the gap before a batch is padding).
+//   seg_out[nseg]  output row (bit 31: head-row partial, added atomically; bit 30: final write, iterate)
+//   seg_end[nseg]  end offset of the segment's entries (absolute, in the padded entry arrays)
+//   ent_col[nent]  X row of each entry (bit 31, distributed: row of the head block D0)
+//   ent_val[nent]  value (plan dtype)
+//   gmask[nent/8]  bit t of byte g: entry 8g + t is the last entry of its segment
+//   bat[2*nbatch]  (first entry, end entry) of batch b
+//   pf_rng[2*nbatch], pf_rows: L2 prefetch plan -- batch b requests rows pf_rows[pf_rng[2b] ..
+//                  pf_rng[2b+1]) (X rows; bit 31: a row of the second source, e.g. staging): the rows
+//                  whose first gather of their level is in batch b + ahead (null: no prefetch)
 struct SegLevel {
-    int64_t nseg = 0;
+    int64_t nseg = 0, nent = 0, nbatch = 0;
+    int bs = kDefaultBatchSegs;
     int mode = 0;
-    int32_t *seg_out = nullptr;   // [nseg] out row (bit 31: atomic)
-    uint32_t *seg_end = nullptr;  // [nseg] end offset into the entries
-    int32_t *ent_col = nullptr;   // [nnz] X row (bit 31: D0 row)
-    void *ent_val = nullptr;      // [nnz]
-    int64_t max_x_row = (int64_t)1 << 40;  // bound on the X rows referenced (enables 32-bit offsets)
+    int32_t *seg_out = nullptr;
+    uint32_t *seg_end = nullptr;
+    int32_t *ent_col = nullptr;
+    void *ent_val = nullptr;
+    uint8_t *gmask = nullptr;
+    uint32_t *bat = nullptr;
+    int32_t *pf_rows = nullptr;
+    uint32_t *pf_rng = nullptr;
 };
+
+// host form of a level's segment list before padding (layout.cpp input): seg_end relative to ent_col
+struct HostSegs {
+    std::vector<int32_t> seg_out;
+    std::vector<uint32_t> seg_end;
+    std::vector<int32_t> ent_col;
+    std::vector<uint8_t> ent_val;  // plan dtype, element size es
+    // L2 prefetch plan (optional): ahead > 0 batches; level boundaries (first segment of each level
+    // after the first) restart the first-reference bookkeeping
+    int64_t pf_ahead = 0;
+    std::vector<int64_t> level_seg;
+};
+// Pad into the batch layout and upload (cudaMalloc'ed pointers appended to `allocs`, freed by the
+// owner).  Returns 0 or a cudaError_t; `err` gets a message for layout errors (offsets beyond 32 bits).
+int upload_seg_level(const HostSegs &h, int es, int bs, int mode, std::vector<void *> &allocs, SegLevel &out,
+                     std::string &err);
+
 // Peer (NVLink) addressing of the distributed P2P transport: an encoded row is
 // (rank << kPeerShift | row) into the per-rank base pointers of a PeerPtrs; kParityBit marks a row
 // of the double-buffered head partial C0 (shifted by the current call's parity offset).
@@ -87,18 +117,22 @@ struct PeerPtrs {
     // warps' batch grabs so that their stores overlap the gathers instead of a separate K-Z pass
     const int32_t *zrows = nullptr;
     int64_t nzero = 0;
-    int ypf = 0;  // K-A levels >= 1, single GPU: prefetch the batch's Y rows into L2 at batch start
 };
 // single GPU: a body segment whose row receives no later contribution (arrow_spmm_iterate's
 // activation is applied when it is flushed); activations: 0 identity, 1 ReLU
 constexpr uint32_t kFinalBit = 0x40000000u;
 constexpr uint32_t kRowMask30 = 0x3fffffffu;
+// per-call K-A options (from arrow_options.flags)
+struct SegLaunch {
+    int kernel = 0;  // full-warp rows: 0 shuffle-entry k_seg32, 1 broadcast-entry k_ka
+};
 // dist: 0 single GPU, 1 distributed (head columns from D0, head partials into C0), 2 as 1 with
 // body rows stored through `outs` (encoded rows, levels >= 1 of the P2P transport) or, with
-// kLocalRmwBit, added into Y (rows whose home is this rank)
+// kLocalRmwBit, added into Y (rows whose home is this rank), 3 single GPU level 0 of the staged
+// schedule (entries with bit 31 read the staging rows passed as D0; flushes as 0)
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-               int num_sms, unsigned *counter, int bseg, void *stream, const PeerPtrs *outs = nullptr, int act = 0,
-               const int32_t *zrows = nullptr, int64_t nzero = 0);
+               int num_sms, unsigned *counter, void *stream, const SegLaunch &opt, const PeerPtrs *outs = nullptr,
+               int act = 0, const int32_t *zrows = nullptr, int64_t nzero = 0);
 // Y[rows[i]] = act(Y[rows[i]]) (rows whose last contribution is a head-row partial)
 int launch_act_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, int act, void *Y, void *stream);
 // dst row enc(didx[i]) of bases = src[sidx[i]] (sidx < 0: zero); grid of `blocks` (0: sized to n)
@@ -112,32 +146,8 @@ int launch_gather_add_peers(int dtype, const PeerPtrs &bases, int64_t par_shift,
 // after ~60 s so a lost peer cannot hang the GPU)
 int launch_barrier(const PeerPtrs &flags, const unsigned *mine, int slot, unsigned epoch, int me, int G, void *stream);
 
-struct StreamArgs {
-    const uint32_t *keys;
-    const void *vals;
-    const uint32_t *bstart;
-    int64_t nbatch;
-    const void *X, *D0;
-    void *Y, *C0;
-    int64_t k;
-    unsigned *counter;
-    int num_sms, mode, dist;
-};
-struct StreamCfg {
-    int vb, lpe, nv, d;
-};
-
-StreamCfg pick_stream_cfg(int dtype, int64_t k, const void *X, const void *Y, const void *D0, const void *C0);
-int launch_stream_f32(const StreamArgs &a, const StreamCfg &c, cudaStream_t st);
-int launch_stream_f64(const StreamArgs &a, const StreamCfg &c, cudaStream_t st);
-
 // kernels.cu launchers (all on `stream`; return cudaError_t as int)
-int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                  int64_t k, int num_sms, unsigned *counter, void *stream);
-int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k,
-                      void *D0, void *C0, void *stream);
-int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k,
-                         int add, void *Y, void *stream);
+int device_sms();  // SM count of the current device (cudaDevAttrMultiProcessorCount, cached)
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream, int blocks = 0);
 int launch_zero(void *Y, int64_t bytes, void *stream);
 // dst[didx[i]] (= | +=) src[sidx[i]] (identity when an index list is NULL; sidx[i] < 0 writes zero)

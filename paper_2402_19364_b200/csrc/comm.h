@@ -15,6 +15,6 @@ namespace arrow {
 arrow_status comm_status(int nccl_result, const char *what);
 // Build this rank's part of a distributed plan (dist.cpp).
 arrow_status dist_build(arrow_plan plan, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
-                        int32_t head_chunk);
+                        int32_t head_chunk, int bs);
 arrow_status dist_spmm(arrow_plan plan, const void *X, void *Y, int64_t k, cudaStream_t st);
 }  // namespace arrow

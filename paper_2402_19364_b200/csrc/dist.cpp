@@ -47,9 +47,7 @@ struct DistHostLevel {
     int64_t h = 0;
     std::vector<int64_t> recv_cnt, send_cnt, out_cnt, in_cnt;  // per peer (levels >= 1)
     std::vector<int32_t> head_j, head_row, zero_rows;
-    std::vector<int32_t> seg_out, ent_col;
-    std::vector<uint32_t> seg_end;
-    std::vector<uint8_t> ent_val;
+    HostSegs segs;  // K-A work of this rank (layout.cpp pads and uploads it)
 };
 
 struct DistHost {
@@ -71,7 +69,6 @@ struct DistHost {
     int64_t zero_tail_lo = 0, zero_tail_n = 0;  // local Y rows of the A-isolated tail (written as 0)
     std::vector<int64_t> halo_all, stage_all;           // per rank
     std::vector<int32_t> d0push_src, d0push_dst;        // my heads -> every rank's D0
-    std::vector<int32_t> halopush_src, halopush_dst;    // my X rows -> every rank's halo (push kernel)
     std::vector<int32_t> pack_src, pack_dst;            // my X rows -> my send chunks / my own halo (DMA)
     std::vector<int64_t> send_row, halo_dst_row;        // per peer: my send chunk, its place in the peer's halo
     int64_t send_rows = 0;
@@ -95,12 +92,9 @@ struct DistState {
     int32_t *pre_src = nullptr, *pre_dst = nullptr;
     int64_t n_pre = 0;
     // P2P: pushes of my head rows into every D0 and of my X rows into every halo (encoded rows)
-    int32_t *d0push_src = nullptr, *d0push_dst = nullptr, *halopush_src = nullptr, *halopush_dst = nullptr;
-    int64_t n_d0push = 0, n_halopush = 0;
-    // P2P, DMA halo (default; ARROW_DIST_HALO=push uses the push kernel): pack, then one copy-engine
-    // transfer per peer into its halo
-    int halo_dma = 1;
-    int pack_on_comm = 0;  // ARROW_DIST_PACK=comm: pack on the communication stream, next to level 0
+    int32_t *d0push_src = nullptr, *d0push_dst = nullptr;
+    int64_t n_d0push = 0;
+    // P2P halo: X rows packed per peer, then one copy-engine transfer per peer into its halo
     int32_t *pack_src = nullptr, *pack_dst = nullptr;
     int64_t n_pack = 0;
     std::vector<int64_t> send_row, halo_dst_row;
@@ -125,8 +119,9 @@ struct DistState {
     // different copy engines concurrently
     std::vector<cudaStream_t> ds;
     std::vector<cudaEvent_t> ds_ev;
-    int bseg = 16, reserve_sms = 16, push_blocks = 0;
+    int reserve_sms = 16;  // NCCL transport: SMs' worth of K-A blocks left free for the NCCL kernels
     int64_t fwd_rows = 0, rev_rows = 0;  // rows exchanged with peers (trace)
+    bool ready = false;                  // dist_build completed on this rank (teardown is collective)
 };
 
 namespace {
@@ -136,21 +131,6 @@ void close_peers(DistState *d, PeerPtrs &pp) {
     pp = PeerPtrs{};
 }
 }  // namespace
-
-void dist_free(DistState *d) {
-    if (!d) return;
-    if (d->cs) cudaStreamSynchronize(d->cs);
-    close_peers(d, d->ws_peer);
-    close_peers(d, d->flags_peer);
-    for (void *p : d->allocs) cudaFree(p);
-    if (d->ws) cudaFree(d->ws);
-    for (auto e : d->ev)
-        if (e) cudaEventDestroy(e);
-    for (auto e : d->ds_ev) cudaEventDestroy(e);
-    for (auto s : d->ds) cudaStreamDestroy(s);
-    if (d->cs) cudaStreamDestroy(d->cs);
-    delete d;
-}
 
 namespace {
 
@@ -374,11 +354,6 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         for (int t = 0; t < G; ++t) {
             if (o_halo + H.halo_all[t] + H.stage_all[t] > (int64_t)kPeerRowMask)
                 return set_error(ARROW_E_UNSUPPORTED, "P2P workspace exceeds 2^27 rows");
-            for (int i = 1; i < nl; ++i)
-                for (size_t m = 0; m < sl[i][t].size(); ++m) {
-                    H.halopush_src.push_back(sl[i][t][m]);
-                    H.halopush_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)(o_halo + HBt[t][me][i] + (int64_t)m)));
-                }
         }
         const int64_t o_stage = o_halo + H.halo_all[me];
         // DMA variant: pack every peer's rows contiguously ([D0 | C0 x 2 | halo | stage | send]),
@@ -459,19 +434,19 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             return (i == 0) ? (int32_t)(q - lo) : halo_slot[q - ha];
         };
         auto push_val = [&](double v) {
-            const size_t at = DL.ent_val.size();
-            DL.ent_val.resize(at + es);
-            if (es == 8) std::memcpy(DL.ent_val.data() + at, &v, 8);
-            else { const float f = (float)v; std::memcpy(DL.ent_val.data() + at, &f, 4); }
+            const size_t at = DL.segs.ent_val.size();
+            DL.segs.ent_val.resize(at + es);
+            if (es == 8) std::memcpy(DL.segs.ent_val.data() + at, &v, 8);
+            else { const float f = (float)v; std::memcpy(DL.segs.ent_val.data() + at, &f, 4); }
         };
         const int64_t W = std::max<int64_t>(1, window_rows / b) * b;
         for (int64_t lo_w = qa; lo_w < qb; lo_w += W) {
             const int64_t hi_w = std::min(qb, lo_w + W);
             for (int64_t p = std::max(h, lo_w); p < hi_w; ++p) {
                 if (L.row_ptr[p + 1] == L.row_ptr[p]) continue;
-                for (int64_t e = L.row_ptr[p]; e < L.row_ptr[p + 1]; ++e) { DL.ent_col.push_back(colmap(L.col[e])); push_val(L.val[e]); }
-                DL.seg_out.push_back(i == 0 ? (int32_t)(p - lo) : out_slot[p - ha]);
-                DL.seg_end.push_back((uint32_t)DL.ent_col.size());
+                for (int64_t e = L.row_ptr[p]; e < L.row_ptr[p + 1]; ++e) { DL.segs.ent_col.push_back(colmap(L.col[e])); push_val(L.val[e]); }
+                DL.segs.seg_out.push_back(i == 0 ? (int32_t)(p - lo) : out_slot[p - ha]);
+                DL.segs.seg_end.push_back((uint32_t)DL.segs.ent_col.size());
             }
             for (int64_t j = 0; j < h; ++j) {
                 const int32_t *a = L.col.data() + L.row_ptr[j], *z = L.col.data() + L.row_ptr[j + 1];
@@ -479,9 +454,9 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                 const int64_t x1 = L.row_ptr[j] + (std::lower_bound(a, z, (int32_t)hi_w) - a);
                 while (x0 < x1) {
                     const int64_t x2 = std::min<int64_t>(x1, x0 + head_chunk);
-                    for (int64_t e = x0; e < x2; ++e) { DL.ent_col.push_back(colmap(L.col[e])); push_val(L.val[e]); }
-                    DL.seg_out.push_back((int32_t)(kFlag | (uint32_t)j));
-                    DL.seg_end.push_back((uint32_t)DL.ent_col.size());
+                    for (int64_t e = x0; e < x2; ++e) { DL.segs.ent_col.push_back(colmap(L.col[e])); push_val(L.val[e]); }
+                    DL.segs.seg_out.push_back((int32_t)(kFlag | (uint32_t)j));
+                    DL.segs.seg_end.push_back((uint32_t)DL.segs.ent_col.size());
                     x0 = x2;
                 }
             }
@@ -557,8 +532,33 @@ arrow_status all_true(DistState *S, bool &v) {
 
 }  // namespace
 
+// Collective for P2P plans: every rank's last gather-add still reads its peers' workspaces over
+// NVLink, so no rank unmaps or frees its workspace before all ranks have drained their streams
+// (one NCCL all-reduce after a device synchronise).  arrow_plan_destroy is therefore collective for
+// distributed plans (include/arrow.h).
+void dist_free(DistState *d) {
+    if (!d) return;
+    if (d->ready && d->p2p && d->comm) {
+        cudaDeviceSynchronize();
+        bool dummy = true;
+        all_true(d, dummy);
+    }
+    if (d->cs) cudaStreamSynchronize(d->cs);
+    close_peers(d, d->ws_peer);
+    close_peers(d, d->flags_peer);
+    for (void *p : d->allocs) cudaFree(p);
+    if (d->ws) cudaFree(d->ws);
+    for (auto e : d->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto e : d->ds_ev) cudaEventDestroy(e);
+    for (auto s : d->ds) cudaStreamDestroy(s);
+    if (d->cs) cudaStreamDestroy(d->cs);
+    delete d;
+}
+
+
 arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
-                        int32_t head_chunk) {
+                        int32_t head_chunk, int bs) {
     auto *S = new DistState();
     P->dist = S;
     S->comm = (ncclComm_t)comm->comm;
@@ -569,10 +569,9 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     for (auto &e : S->ev)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
             return set_error(ARROW_E_CUDA, "cudaEventCreate");
-    // transport: P2P (peer memory over NVLink, fused with the kernels) unless ARROW_DIST_TRANSPORT=nccl,
-    // a single rank, or some rank cannot map its peers' memory (decided collectively)
-    const char *tr = std::getenv("ARROW_DIST_TRANSPORT");
-    bool p2p = S->G > 1 && S->G <= kMaxPeers && !(tr && std::string(tr) == "nccl");
+    // transport: P2P (peer memory over NVLink, fused with the kernels) unless options.transport is
+    // NCCL, a single rank, or some rank cannot map its peers' memory (decided collectively)
+    bool p2p = S->G > 1 && S->G <= kMaxPeers && P->transport != ARROW_TRANSPORT_NCCL;
     if (p2p) {
         DCUDA(cudaMalloc(&S->flags, 3 * kMaxPeers * sizeof(unsigned)));
         DCUDA(cudaMemset(S->flags, 0, 3 * kMaxPeers * sizeof(unsigned)));
@@ -584,6 +583,8 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         if (st != ARROW_OK) return st;
         if (!ok) {
             close_peers(S, S->flags_peer);
+            if (P->transport == ARROW_TRANSPORT_P2P)
+                return set_error(ARROW_E_UNSUPPORTED, "P2P transport requested but a peer's memory cannot be mapped");
             p2p = false;
         }
         if (std::getenv("ARROW_DIST_TRACE"))
@@ -598,9 +599,6 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     S->lo = H.lo;
     S->hi = H.hi;
     S->nl = (int)H.L.size();
-    if (const char *e = std::getenv("ARROW_SEG_BS")) S->bseg = std::atoi(e);
-    if (const char *e = std::getenv("ARROW_DIST_RESERVE_SMS")) S->reserve_sms = std::atoi(e);
-    if (const char *e = std::getenv("ARROW_DIST_PUSH_BLOCKS")) S->push_blocks = std::atoi(e);
     const int nl = S->nl, G = S->G, me = S->me;
     for (int i = 0; i < nl; ++i) {
         S->h.push_back(H.L[i].h);
@@ -625,8 +623,6 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         S->ws_rows = S->o_out + H.stage_all[me] + H.send_rows;
         S->send_row = H.send_row;
         S->halo_dst_row = H.halo_dst_row;
-        if (const char *e = std::getenv("ARROW_DIST_HALO")) S->halo_dma = std::string(e) != "push";
-        if (const char *e = std::getenv("ARROW_DIST_PACK")) S->pack_on_comm = std::string(e) == "comm";
         for (int g = 0; g < G; ++g) {
             if (g == me) continue;
             cudaStream_t q;
@@ -677,16 +673,12 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
 
     bool ok = true;
     for (int i = 0; i < nl; ++i) {
-        DistHostLevel &HL = H.L[i];
+        // every output row is written once (mode 0): local Y (level 0) or a staging buffer
         SegLevel sg;
-        sg.nseg = (int64_t)HL.seg_out.size();
-        // level 0 reads the local X rows, levels >= 1 the halo inside the workspace
-        sg.max_x_row = (i == 0) ? std::max<int64_t>(S->hi - S->lo, S->d0_rows) : S->ws_rows;
-        sg.mode = 0;  // every output row is written once: local Y (level 0) or a staging buffer
-        sg.seg_out = upload(S, HL.seg_out, ok);
-        sg.seg_end = reinterpret_cast<uint32_t *>(upload(S, HL.seg_end, ok));
-        sg.ent_col = upload(S, HL.ent_col, ok);
-        sg.ent_val = upload(S, HL.ent_val.data(), HL.ent_val.size(), ok);
+        std::string err;
+        const int e = upload_seg_level(H.L[i].segs, (int)P->esize(), bs, 0, S->allocs, sg, err);
+        if (e) return set_error(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
+        H.L[i].segs = HostSegs();
         S->seg.push_back(sg);
     }
     S->n_pre = (int64_t)pre_src.size();
@@ -698,9 +690,6 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     S->n_pack = (int64_t)H.pack_src.size();
     S->pack_src = upload(S, H.pack_src, ok);
     S->pack_dst = upload(S, H.pack_dst, ok);
-    S->n_halopush = (int64_t)H.halopush_src.size();
-    S->halopush_src = upload(S, H.halopush_src, ok);
-    S->halopush_dst = upload(S, H.halopush_dst, ok);
     S->n_zero = (int64_t)zero.size();
     S->zero_rows = upload(S, zero, ok);
     S->zero_tail_lo = H.zero_tail_lo;
@@ -719,6 +708,7 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     S->allocs.push_back(S->counters);
     P->local_begin = S->lo;
     P->local_end = S->hi;
+    S->ready = true;
     return ARROW_OK;
 }
 
@@ -792,27 +782,26 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     const int par = (int)(S->calls & 1);
     S->calls++;
     const int64_t c0 = S->o_c0 + par * S->d0_rows;  // this call's C0
-    const int sms = std::max(1, P->num_sms - (S->halo_dma ? 0 : S->reserve_sms));
+    const int sms = P->num_sms;
     static const bool trace = std::getenv("ARROW_DIST_TRACE") != nullptr;
     Marks M;
     M.on = P->profiling || trace;
 
     // S: the previous call (and the caller's writes of X) precede everything.  My head rows go into
-    // every rank's D0 first (level 0 needs only them), then C0 = 0 and the zero rows; DMA halo: the
-    // rows for the peers are packed, and C moves one chunk per peer with the copy engines while
-    // the SMs run level 0.  Push halo: C pushes the rows with a kernel next to level 0.
+    // every rank's D0 first (level 0 needs only them), then C0 = 0 and the zero rows; the rows for
+    // the peers are packed, and C moves one chunk per peer with the copy engines while the SMs run
+    // level 0.
     const int m0 = M(st);
     DK(launch_push_rows(dt, X, S->d0push_src, S->d0push_dst, S->n_d0push, k, S->ws_peer, 0, st));
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(c0), 0, (size_t)S->d0_rows * k * es, st));
     DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, st));
-    if (S->halo_dma && !S->pack_on_comm) DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, st));
+    DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, st));
     const int m0p = M(st);
     DCUDA(cudaEventRecord(S->ev[0], st));
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
     const int m0c = M(S->cs);
-    if (S->halo_dma && S->pack_on_comm) DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, S->cs));
-    if (S->halo_dma) {
+    {
         DCUDA(cudaEventRecord(S->ev[5], S->cs));
         for (int g = 0, q = 0; g < G; ++g) {
             if (g == me) continue;
@@ -826,9 +815,6 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
             DCUDA(cudaStreamWaitEvent(S->cs, S->ds_ev[q], 0));
             ++q;
         }
-    } else {
-        DK(launch_push_rows(dt, X, S->halopush_src, S->halopush_dst, S->n_halopush, k, S->ws_peer,
-                            S->push_blocks > 0 ? S->push_blocks : 8 * S->reserve_sms, S->cs));
     }
     const int m1c = M(S->cs);
     DK(launch_barrier(S->flags_peer, S->flags, 1, ++S->epoch[1], me, G, S->cs));
@@ -837,14 +823,14 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     // S: every D0 complete -> level 0
     DK(launch_barrier(S->flags_peer, S->flags, 0, ++S->epoch[0], me, G, st));
     const int m1 = M(st), m1b = M(st);
-    DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(c0), k, sms, S->counters, S->bseg, st));
+    DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(c0), k, sms, S->counters, st, P->launch));
     const int m2 = M(st);
     // levels >= 1 once every halo is complete; body rows are stored into their home rank's stage
     DCUDA(cudaStreamWaitEvent(st, S->ev[1], 0));
     const int m3 = M(st);
     for (int i = 1; i < nl; ++i)
         DK(launch_seg(dt, 2, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), Y, row(c0 + S->d0_off[i]),
-                      k, sms, S->counters + i, S->bseg, st, &S->ws_peer));
+                      k, sms, S->counters + i, st, P->launch, &S->ws_peer));
     const int m4 = M(st), m4b = M(st);
     // the A-isolated tail of Y (no level writes it) is zeroed while the other ranks finish
     if (S->zero_tail_n)
@@ -858,7 +844,7 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     if (trace) {
         cudaEventSynchronize(M.ev[m6]);
         std::string line = "[arrow dist rank " + std::to_string(me) + " p2p] ms: halo " +
-                           std::string(S->halo_dma ? "D0+zero+pack " + M.el(m0, m0p) + " dma " : "push ") + M.el(m0c, m1c) +
+                           std::string("D0+zero+pack " + M.el(m0, m0p) + " dma ") + M.el(m0c, m1c) +
                            " + barrier " + M.el(m1c, m2c) + " (done at " + M.el(m0, m2c) + ") | barrier0 " +
                            M.el(m0p, m1) + " | K-A L0 " + M.el(m1, m2) + " | wait " + M.el(m2, m3) + " | K-A L>=1 " +
                            M.el(m3, m4) + " | barrier " + M.el(m4, m5) + " | gather-add " + M.el(m5, m6) +
@@ -933,13 +919,13 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     // 3. (S) level 0 overlaps the forward exchange; levels >= 1 after it
     DCUDA(cudaStreamWaitEvent(st, S->ev[1], 0));
     const int m4 = M(st);
-    DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(S->o_c0), k, sms, S->counters, S->bseg, st));
+    DK(launch_seg(dt, 1, S->seg[0], X, row(S->o_d0), Y, row(S->o_c0), k, sms, S->counters, st, P->launch));
     const int m5 = M(st);
     DCUDA(cudaStreamWaitEvent(st, S->ev[2], 0));
     const int m6 = M(st);
     for (int i = 1; i < nl; ++i)
         DK(launch_seg(dt, 1, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), row(S->o_out),
-                      row(S->o_c0 + S->d0_off[i]), k, sms, S->counters + i, S->bseg, st));
+                      row(S->o_c0 + S->d0_off[i]), k, sms, S->counters + i, st, P->launch));
     const int m7 = M(st), m7b = M(st);
     DCUDA(cudaEventRecord(S->ev[3], st));
     // 4. (C) staging rows go home, head partials are reduced
@@ -996,6 +982,10 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
 extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nranks, int32_t rank, int64_t window_rows,
                                             int32_t head_chunk, int64_t *lohi, int64_t *counts) {
     if (!d || !lohi) return arrow::set_error(ARROW_E_INVALID_ARG, "NULL argument");
+    if (nranks < 1 || nranks > arrow::kMaxPeers || rank < 0 || rank >= nranks)
+        return arrow::set_error(ARROW_E_INVALID_ARG, "nranks must be in [1, 8] and rank in [0, nranks)");
+    if (d->band != ARROW_BAND_BLOCK)
+        return arrow::set_error(ARROW_E_UNSUPPORTED, "distributed schedules need ARROW_BAND_BLOCK");
     arrow::DistHost H;
     arrow_status st = arrow::dist_schedule(*d, nranks, rank, window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
                                            head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, 0, H);
@@ -1011,8 +1001,8 @@ extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nrank
             for (int g = 0; g < G; ++g) c[G + g] = L.recv_cnt.empty() ? 0 : L.recv_cnt[g];
             for (int g = 0; g < G; ++g) c[2 * G + g] = L.out_cnt.empty() ? 0 : L.out_cnt[g];
             for (int g = 0; g < G; ++g) c[3 * G + g] = L.in_cnt.empty() ? 0 : L.in_cnt[g];
-            c[4 * G + 0] = (int64_t)L.ent_col.size();
-            c[4 * G + 1] = (int64_t)L.seg_out.size();
+            c[4 * G + 0] = (int64_t)L.segs.ent_col.size();
+            c[4 * G + 1] = (int64_t)L.segs.seg_out.size();
             c[4 * G + 2] = (int64_t)L.head_j.size();
             c[4 * G + 3] = (int64_t)L.zero_rows.size() + (&L == &H.L[0] ? H.zero_tail_n : 0);
             c += 4 * G + 4;

@@ -1,93 +1,42 @@
-// kernels.cu -- the hot path of arrow_spmm on sm_100a (B200).
+// kernels.cu -- the small sm_100a kernels around K-A (seg_kernel.cu): zero rows (K-Z), the
+// iterate-mode activation pass, and the row movers / gather-adds / cross-GPU barrier of the
+// distributed transports (S6).
 //
-// Per level i of the decomposition A X = sum_i P_{pi_i} (B_i (P_{pi_i}^T X))  (Eq. (1)):
-//   K-H  head stage      D0 = X[head_i] (Alg. 1 line 1 "Broadcast(D^(0))"), C0 = 0
-//   K-A  segment stream  body rows  y_p = B^(p,0) D0 + B^(p,p) X_p  -> Y[perm_i[p]] (store at level 0,
-//                        read-modify-write at levels >= 1: Alg. 2's reverse aggregation)
-//                        head rows  C0[j] += B^(0,t) X_t, one tile window t at a time (Alg. 1 line 2,
-//                        P:464), combined with fp atomics in L2 (C0 is L2-resident)
-//   K-C  head epilogue   Y[head_i] (= or +=) C0 (Alg. 1 line 3 "Reduce(C^(0))")
-// The permutations P_pi^T X / P_pi Y are folded into the column and output indices at plan
-// time (S4): no permuted copy of X or Y ever exists.
-//
-// The path is HBM-bound (<= 2 FLOP/B), so there are no tensor cores: the design
-// goal is that every X row of a tile is fetched from DRAM once (window-ordered work keeps the
-// tile's rows L2-hot while all its users run) and that each warp keeps many 16-byte loads in
-// flight.  A "sub-warp" of LPE lanes owns one row slab of LPE*VEC elements: LPE=32 lanes x float4
-// covers a 512-byte row (k=128 fp32) with one coalesced request per entry.
+// Per level i of the decomposition A X = sum_i P_{pi_i} (B_i (P_{pi_i}^T X))  (Eq. (1))
+// the work is done by K-A; on one GPU the head block of Alg. 1 line 1 is read straight from
+// X (columns are folded to X rows) and the head-row partials of line 2 are added into
+// Y[head] by K-A's L2 reductions, so the stage (K-H) and epilogue (K-C) of Alg. 1 are folded away;
+// in distributed mode D0 is pushed to every rank (k_push_rows) and C0 is combined by the transport.
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
-#include <cstdlib>
-#include <string>
 
 #include "arrow_internal.h"
+#include "dev_common.cuh"
 
 namespace arrow {
+
+// SM count of the current device (cached per device)
+int device_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cache[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
 namespace {
 
-template <typename T, int VEC> struct VecT;
-template <> struct VecT<float, 4> { using type = float4; };
-template <> struct VecT<float, 2> { using type = float2; };
-template <> struct VecT<float, 1> { using type = float; };
-template <> struct VecT<double, 2> { using type = double2; };
-template <> struct VecT<double, 1> { using type = double; };
-
-template <typename T, int VEC> struct Frag {
-    T v[VEC];
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) v[i] = T(0);
-    }
-};
-
-template <typename T, int VEC>
-__device__ __forceinline__ Frag<T, VEC> ld_x(const T *p) {  // read-only path, 16 B per lane at VEC*sizeof(T)=16
-    using V = typename VecT<T, VEC>::type;
-    V r = __ldg(reinterpret_cast<const V *>(p));
-    Frag<T, VEC> f;
-    static_assert(sizeof(V) == sizeof(f), "frag size");
-    memcpy(&f, &r, sizeof(V));
-    return f;
-}
-
-template <typename T, int VEC>
-__device__ __forceinline__ Frag<T, VEC> ld_plain(const T *p) {
-    using V = typename VecT<T, VEC>::type;
-    V r = *reinterpret_cast<const V *>(p);
-    Frag<T, VEC> f;
-    memcpy(&f, &r, sizeof(V));
-    return f;
-}
-
-template <typename T, int VEC>
-__device__ __forceinline__ void st_stream(T *p, const Frag<T, VEC> &f) {  // evict-first: Y is write-once
-    using V = typename VecT<T, VEC>::type;
-    V r;
-    memcpy(&r, &f, sizeof(V));
-    __stcs(reinterpret_cast<V *>(p), r);
-}
-
-template <typename T, int VEC>
-__device__ __forceinline__ void st_plain(T *p, const Frag<T, VEC> &f) {
-    using V = typename VecT<T, VEC>::type;
-    V r;
-    memcpy(&r, &f, sizeof(V));
-    *reinterpret_cast<V *>(p) = r;
-}
-
-template <typename T, int VEC>
-__device__ __forceinline__ void atomic_add_frag(T *p, const Frag<T, VEC> &f) {
-    if constexpr (sizeof(T) == 4 && VEC == 4) {
-        atomicAdd(reinterpret_cast<float4 *>(p), make_float4(f.v[0], f.v[1], f.v[2], f.v[3]));
-    } else if constexpr (sizeof(T) == 4 && VEC == 2) {
-        atomicAdd(reinterpret_cast<float2 *>(p), make_float2(f.v[0], f.v[1]));
-    } else {
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) atomicAdd(p + i, f.v[i]);
-    }
-}
+using dev::Frag;
+using dev::ld_plain;
+using dev::ld_x;
+using dev::st_plain;
+using dev::st_stream;
 
 // K-Z: zero the listed Y rows (level 0: head rows, which then accumulate head slices atomically,
 // and rows with no entry in B_0, incl. A-isolated vertices).
@@ -110,129 +59,14 @@ __global__ void __launch_bounds__(256) k_zero_rows(const int32_t *__restrict__ r
     }
 }
 
-// ------------------------------------------------------------------------------------ K-H / K-C
-template <typename T, int VEC>
-__global__ void __launch_bounds__(256) k_head_stage(const T *__restrict__ X, const int32_t *__restrict__ head,
-                                                    int64_t h, int64_t k, T *__restrict__ D0, T *__restrict__ C0) {
-    const int64_t kv = k / VEC, total = h * kv;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = t / kv, c = (t - j * kv) * VEC;
-        const Frag<T, VEC> x = ld_x<T, VEC>(X + (int64_t)__ldg(head + j) * k + c);
-        st_plain<T, VEC>(D0 + j * k + c, x);
-        Frag<T, VEC> z;
-        z.zero();
-        st_plain<T, VEC>(C0 + j * k + c, z);
-    }
-}
-
-template <typename T, int VEC>
-__global__ void __launch_bounds__(256) k_head_epilogue(const T *__restrict__ C0, const int32_t *__restrict__ head,
-                                                       int64_t h, int64_t k, int add, T *__restrict__ Y) {
-    const int64_t kv = k / VEC, total = h * kv;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = t / kv, c = (t - j * kv) * VEC;
-        Frag<T, VEC> a = ld_plain<T, VEC>(C0 + j * k + c);
-        T *p = Y + (int64_t)__ldg(head + j) * k + c;
-        if (add) {
-            Frag<T, VEC> y = ld_plain<T, VEC>(p);
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) a.v[i] += y.v[i];
-        }
-        st_plain<T, VEC>(p, a);
-    }
-}
-
-// ------------------------------------------------------------------------------------ dispatch
-inline int pick_vec(int dtype, int64_t k, std::initializer_list<const void *> ptrs) {
-    const int es = dtype == 1 ? 8 : 4;
-    int vec = 16 / es;
-    while (vec > 1) {
-        bool ok = (k % vec) == 0;
-        for (const void *p : ptrs) ok = ok && ((reinterpret_cast<uintptr_t>(p) % (vec * es)) == 0);
-        if (ok) break;
-        vec >>= 1;
-    }
-    return vec;
-}
-
-inline int pick_lpe(int64_t k, int vec) {
-    const int64_t need = (k + vec - 1) / vec;
-    int lpe = 1;
-    while (lpe < 32 && lpe < need) lpe <<= 1;
-    return lpe;
-}
-
-inline unsigned grid_for(int64_t total) {
-    int64_t g = (total + 255) / 256;
-    if (g > 148 * 16) g = 148 * 16;
-    if (g < 1) g = 1;
-    return (unsigned)g;
-}
-
 }  // namespace
-
-StreamCfg pick_stream_cfg(int dtype, int64_t k, const void *X, const void *Y, const void *D0, const void *C0) {
-    const int es = dtype == 1 ? 8 : 4;
-    const int64_t rb = k * es;
-    auto aligned = [&](int a) {
-        for (const void *p : {X, Y, D0, C0})
-            if (p && (reinterpret_cast<uintptr_t>(p) % a) != 0) return false;
-        return true;
-    };
-    int vb = 4;
-    if (rb % 16 == 0 && aligned(16)) vb = 16;
-    else if (rb % 8 == 0 && aligned(8)) vb = 8;
-    if (vb < es) vb = es;
-    const int64_t rv = rb / vb;  // vectors per row
-    StreamCfg c{vb, 1, 1, 8};
-    if (vb == 16) {
-        if (rv >= 17) c = {16, 8, 4, 4};
-        else if (rv >= 9) c = {16, 4, 4, 4};
-        else if (rv >= 5) c = {16, 2, 4, 4};
-        else if (rv >= 3) c = {16, 1, 4, 4};
-        else c = {16, 1, 1, 8};
-    } else {
-        if (rv >= 17) c = {vb, 32, 1, 8};
-        else if (rv >= 3) c = {vb, 8, 1, 8};
-        else c = {vb, 1, 1, 8};
-    }
-    // experiment hook: ARROW_KA_CFG="lpe,nv,d" for 16-byte rows (must be an instantiated config)
-    if (vb == 16) {
-        if (const char *e = std::getenv("ARROW_KA_CFG")) {
-            int l = 0, nv = 0, d = 0;
-            if (std::sscanf(e, "%d,%d,%d", &l, &nv, &d) == 3) c = {16, l, nv, d};
-        }
-    }
-    return c;
-}
-
-int launch_stream(int dtype, int dist, const DeviceLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                  int64_t k, int num_sms, unsigned *counter, void *stream) {
-    if (L.nbatch == 0 || k == 0) return 0;
-    StreamArgs a{L.keys, L.vals, L.bstart, L.nbatch, X, D0, Y, C0, k, counter, num_sms, L.mode, dist};
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    // TMA bulk-gather kernel when rows are 16-byte multiples of at most 1 KiB on 16-byte aligned
-    // buffers; otherwise the register-pipelined record-stream kernel.
-    const int es = dtype == 1 ? 8 : 4;
-    const int64_t rb = k * es;
-    bool tma = rb % 16 == 0 && rb <= 1024;
-    for (const void *p : {X, (const void *)Y, D0, (const void *)C0})
-        if (p && (reinterpret_cast<uintptr_t>(p) % 16) != 0) tma = false;
-    // kernel choice: ARROW_KA=rec (default for 16-byte rows <= 1 KiB), tma, stream
-    const char *ka = std::getenv("ARROW_KA");
-    const std::string kas = ka ? ka : "seg";
-    StreamCfg c = pick_stream_cfg(dtype, k, X, Y, dist ? D0 : nullptr, dist ? C0 : nullptr);
-    if (tma && kas == "rec") c = StreamCfg{16, -1, 0, 0};
-    else if (tma && kas == "tma") c = StreamCfg{16, 0, 0, 0};
-    return dtype == 1 ? launch_stream_f64(a, c, st) : launch_stream_f32(a, c, st);
-}
 
 int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, void *Y, void *stream, int blocks) {
     if (nrows == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int vec = pick_vec(dtype, k, {Y});
     int64_t gw = (nrows + 31) / 32;  // 8 warps x 4 rows per block pass
-    if (gw > 148 * 8) gw = 148 * 8;
+    if (gw > (int64_t)device_sms() * 8) gw = (int64_t)device_sms() * 8;
     unsigned g = (unsigned)std::max<int64_t>(gw, 1);
     if (blocks > 0 && (unsigned)blocks < g) g = (unsigned)blocks;
     if (dtype == 0) {
@@ -246,46 +80,12 @@ int launch_zero_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, v
     return (int)cudaGetLastError();
 }
 
-int launch_head_stage(int dtype, const void *X, const int32_t *head_rows, int64_t h, int64_t k, void *D0, void *C0,
-                      void *stream) {
-    if (h == 0 || k == 0) return 0;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int vec = pick_vec(dtype, k, {X, D0, C0});
-    const unsigned g = grid_for(h * (k / vec));
-    if (dtype == 0) {
-        if (vec == 4) k_head_stage<float, 4><<<g, 256, 0, st>>>((const float *)X, head_rows, h, k, (float *)D0, (float *)C0);
-        else if (vec == 2) k_head_stage<float, 2><<<g, 256, 0, st>>>((const float *)X, head_rows, h, k, (float *)D0, (float *)C0);
-        else k_head_stage<float, 1><<<g, 256, 0, st>>>((const float *)X, head_rows, h, k, (float *)D0, (float *)C0);
-    } else {
-        if (vec == 2) k_head_stage<double, 2><<<g, 256, 0, st>>>((const double *)X, head_rows, h, k, (double *)D0, (double *)C0);
-        else k_head_stage<double, 1><<<g, 256, 0, st>>>((const double *)X, head_rows, h, k, (double *)D0, (double *)C0);
-    }
-    return (int)cudaGetLastError();
-}
-
-int launch_head_epilogue(int dtype, const void *C0, const int32_t *head_rows, int64_t h, int64_t k, int add, void *Y,
-                         void *stream) {
-    if (h == 0 || k == 0) return 0;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int vec = pick_vec(dtype, k, {C0, Y});
-    const unsigned g = grid_for(h * (k / vec));
-    if (dtype == 0) {
-        if (vec == 4) k_head_epilogue<float, 4><<<g, 256, 0, st>>>((const float *)C0, head_rows, h, k, add, (float *)Y);
-        else if (vec == 2) k_head_epilogue<float, 2><<<g, 256, 0, st>>>((const float *)C0, head_rows, h, k, add, (float *)Y);
-        else k_head_epilogue<float, 1><<<g, 256, 0, st>>>((const float *)C0, head_rows, h, k, add, (float *)Y);
-    } else {
-        if (vec == 2) k_head_epilogue<double, 2><<<g, 256, 0, st>>>((const double *)C0, head_rows, h, k, add, (double *)Y);
-        else k_head_epilogue<double, 1><<<g, 256, 0, st>>>((const double *)C0, head_rows, h, k, add, (double *)Y);
-    }
-    return (int)cudaGetLastError();
-}
-
 // generic row mover for the distributed path: dst[didx ? didx[i] : i] (= | +=) src[sidx ? sidx[i] : i]
 namespace {
 constexpr int kRowsInFlight = 4;
 inline unsigned warp_row_grid(int64_t n) {  // 8 warps per block, kRowsInFlight rows per warp pass
     int64_t g = (n + 8 * kRowsInFlight - 1) / (8 * kRowsInFlight);
-    if (g > 148 * 8) g = 148 * 8;
+    if (g > (int64_t)device_sms() * 8) g = (int64_t)device_sms() * 8;
     if (g < 1) g = 1;
     return (unsigned)g;
 }
@@ -464,7 +264,7 @@ int launch_gather_add_peers(int dtype, const PeerPtrs &bases, int64_t par_shift,
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     int vec = pick_vec(dtype, k, {Y});
     for (const void *p : bases.p) vec = std::min(vec, pick_vec(dtype, k, {p}));
-    const unsigned g = grid_for(n * (k / vec));
+    const unsigned g = grid_for(n * (k / vec), device_sms());
     if (dtype == 0) {
         if (vec == 4) k_gather_add_peers<float, 4><<<g, 256, 0, st>>>(bases, par_shift, ptr, src, drow, n, k, (float *)Y);
         else if (vec == 2) k_gather_add_peers<float, 2><<<g, 256, 0, st>>>(bases, par_shift, ptr, src, drow, n, k, (float *)Y);
@@ -504,7 +304,7 @@ int launch_act_rows(int dtype, const int32_t *rows, int64_t nrows, int64_t k, in
     if (nrows == 0 || k == 0 || act == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int vec = pick_vec(dtype, k, {Y});
-    const unsigned g = grid_for(nrows * (k / vec));
+    const unsigned g = grid_for(nrows * (k / vec), device_sms());
     if (dtype == 0) {
         if (vec == 4) k_act_rows<float, 4><<<g, 256, 0, st>>>(rows, nrows, k, act, (float *)Y);
         else if (vec == 2) k_act_rows<float, 2><<<g, 256, 0, st>>>(rows, nrows, k, act, (float *)Y);
@@ -521,7 +321,7 @@ int launch_gather_add(int dtype, const void *src, const int32_t *ptr, const int3
     if (n == 0 || k == 0) return 0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int vec = pick_vec(dtype, k, {src, dst});
-    const unsigned g = grid_for(n * (k / vec));
+    const unsigned g = grid_for(n * (k / vec), device_sms());
     if (dtype == 0) {
         if (vec == 4) k_gather_add<float, 4><<<g, 256, 0, st>>>((const float *)src, ptr, sidx, drow, n, k, (float *)dst);
         else if (vec == 2) k_gather_add<float, 2><<<g, 256, 0, st>>>((const float *)src, ptr, sidx, drow, n, k, (float *)dst);

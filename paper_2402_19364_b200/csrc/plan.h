@@ -16,7 +16,6 @@ arrow_status set_error(arrow_status s, const std::string &msg);  // thread-local
 
 constexpr int64_t kDefaultWindowRows = 16384;
 constexpr int32_t kDefaultHeadChunk = 32;  // measured best at config R (k = 8, 32, 128): sweep in DESIGN.md §7
-constexpr int32_t kDefaultBatchRecords = 256;
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -54,23 +53,20 @@ struct arrow_plan_s {
     // device memory
     void *arena = nullptr;
     int64_t arena_bytes = 0;
-    std::vector<SegLevel> seg;     // segment-descriptor layout of the K-A kernels (default)
+    std::vector<SegLevel> seg;     // K-A segment layout per launch level
     int32_t *post_rows = nullptr;  // rows last written by a head-row partial (iterate's activation pass)
     int64_t n_post = 0;
-    // staged tail (single GPU): levels >= 1 as one launch into staging rows next to level 0, then
-    // one CSR gather-add into Y (arrow_api.cpp::build_stage_tail)
-    bool tail_on = false;
-    SegLevel tail;
-    int64_t tail_nhead = 0, tail_rows = 0, tail_ndst = 0;
-    int32_t *tail_ptr = nullptr, *tail_src = nullptr, *tail_dst = nullptr;
-    void *stage = nullptr;
-    int64_t stage_k = 0;
     std::vector<void *> seg_allocs;
-    int seg_bseg = 16;
-    int seg_bseg_tail = 0;  // segments per batch in levels >= 1 (0: seg_bseg)
+    arrow::SegLaunch launch;       // per-call K-A options (options.flags)
+    bool use_graphs = true;        // single GPU: replay the call as one CUDA graph (options.flags)
+    bool staged = false;           // single GPU: levels >= 1 into staging rows read by level 0 (flags)
+    int32_t transport = 0;         // ARROW_TRANSPORT_* (distributed plans)
+    int32_t prefetch_batches = 0;  // options.prefetch_batches
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
-    void *ws = nullptr;          // D0 | C0
+    void *ws = nullptr;            // single GPU: staging rows of levels >= 1 (stage_rows x ws_k)
     int64_t ws_k = 0;
+    int64_t stage_rows = 0;        // staging rows: head partials of levels >= 1 first, then their body rows
+    int64_t stage_head_rows = 0;
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
     // arrow_spmm_host_batch: two device slots, two copy streams, per-slot events
@@ -80,10 +76,6 @@ struct arrow_plan_s {
     cudaEvent_t hb_ev[7] = {};  // x[2], c[2], y[2], start/done
     bool no_graph = false;
     cudaStream_t stream = nullptr;
-    // single GPU: the level-0 zero rows that K-A does not touch (entry-less / A-isolated rows) are
-    // written on a side stream next to level 0 (HBM writes under an L2-bound kernel)
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     // CUDA graph of the single-GPU call, keyed by (X, Y, k, stream)
     cudaGraphExec_t gexec = nullptr;
     const void *g_x = nullptr;
@@ -117,10 +109,6 @@ struct arrow_plan_s {
         if (hb_d2h) cudaStreamDestroy(hb_d2h);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (post_rows) cudaFree(post_rows);
-        if (stage) cudaFree(stage);
-        if (fork_ev) cudaEventDestroy(fork_ev);
-        if (join_ev) cudaEventDestroy(join_ev);
-        if (side) cudaStreamDestroy(side);
     }
     size_t esize() const { return dtype == ARROW_F64 ? 8 : 4; }
 };

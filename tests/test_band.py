@@ -184,3 +184,60 @@ def test_strict_save_load_and_errors(tmp_path):
     assert not h.value
     with pytest.raises(KeyError):
         ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 64, band="tridiagonal")
+
+
+# ---------------------------------------------------------------- the band boundary |p - q| = b, b + 1
+BOUNDARY = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "band_boundary.json")))
+
+
+def _boundary_graph():
+    """tests/golden/band_boundary.json: hubs joined to each other and to every tree vertex + the tree."""
+    n, hubs = BOUNDARY["n"], BOUNDARY["hubs"]
+    tree = [v for v in range(n) if v not in hubs]
+    edges = [(h1, h2) for i, h1 in enumerate(hubs) for h2 in hubs[i + 1:]]
+    edges += [(h, v) for h in hubs for v in tree] + [tuple(e) for e in BOUNDARY["tree_edges"]]
+    u, v = _sym(edges)
+    a = np.ones(len(u))
+    rp, col, val = _csr_from_edges(n, u, v, a)
+    return n, rp, col, val
+
+
+def _level1_edges(levels):
+    """undirected original-id edges of level 1 (the level-0 remainder)"""
+    perm, rp, col = levels[1][0], levels[1][1], levels[1][2]
+    out = set()
+    for p in range(len(perm)):
+        for e in range(rp[p], rp[p + 1]):
+            a, b = int(perm[p]), int(perm[col[e]])
+            out.add((min(a, b), max(a, b)))
+    return sorted(out)
+
+
+@pytest.mark.parametrize("band", ["strict", "block"])
+def test_band_boundary_worked_example_oracle(band):
+    n, rp, col, val = _boundary_graph()
+    b = BOUNDARY["b"]
+    dec = oracle.la_decompose(n, rp, col, val, b, band=band)
+    assert dec.order == BOUNDARY["expected_order"]
+    assert dec.levels[0].perm.tolist() == BOUNDARY["expected_level0_perm"]
+    levels = [(L.perm, L.row_ptr, L.col) for L in dec.levels]
+    assert _level1_edges(levels) == [tuple(e) for e in BOUNDARY[f"expected_{band}_remainder"]]
+    assert dec.levels[1].perm[:dec.levels[1].n_i].tolist() == BOUNDARY[f"expected_{band}_level1_perm"]
+    # the predicate itself at the boundary (positions >= b): distance b in, b + 1 out (strict)
+    p, q = np.array([8, 8, 4]), np.array([12, 13, 8])
+    want = {"strict": [True, False, True], "block": [False, False, False]}[band]
+    assert oracle.captured(p, q, b, band=band).tolist() == want
+
+
+@pytest.mark.parametrize("band", ["strict", "block"])
+def test_band_boundary_worked_example_decomposer(band):
+    """The C++ decomposer (C ABI) on the same hand-derived instance: pins its step-3 rule at the
+    boundary independently of the oracle."""
+    n, rp, col, val = _boundary_graph()
+    d = ab.Decomposition(n, rp, col, val, BOUNDARY["b"], band=band)
+    assert d.info()["levels"] == BOUNDARY["expected_order"]
+    levels = [d.export_level(i)[:3] for i in range(2)]
+    assert levels[0][0].tolist() == BOUNDARY["expected_level0_perm"]
+    assert _level1_edges(levels) == [tuple(e) for e in BOUNDARY[f"expected_{band}_remainder"]]
+    li = d.level_info(1)
+    assert levels[1][0][:li["n_i"]].tolist() == BOUNDARY[f"expected_{band}_level1_perm"]

@@ -19,7 +19,7 @@ def test_dist_parity(world, transport):
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), os.path.join(ROOT, "tests", "dist_worker.py")]
-    env = dict(os.environ, ARROW_DIST_TRANSPORT=transport, ARROW_DIST_TRACE="1")
+    env = dict(os.environ, ARROW_TEST_TRANSPORT=transport, ARROW_DIST_TRACE="1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and out.count("DIST_OK") == world, out[-4000:]

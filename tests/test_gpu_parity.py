@@ -324,3 +324,92 @@ def test_strict_band_parity(spec, b, k, order):
     out = np.empty_like(Y32)
     out[perm0] = Y32
     check_fp32(g, out, X32)
+
+
+# ---------------------------------------------------------------- offsets beyond 32 bits, config W
+_BIG = {}
+
+
+def _big_decomposition(spec, b):
+    if (spec, b) not in _BIG:
+        _BIG.clear()
+        g = datagen.make_graph(spec)
+        _BIG[(spec, b)] = (g, ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b))
+    return _BIG[(spec, b)]
+
+
+def _sampled_check(g, plan, X, dtype, extra_rows=()):
+    """Run the plan on X and compare sampled rows (random, the last 2000 -- the largest X/Y byte
+    offsets --, every level's head vertices, extra_rows) with O1: fp64 bitwise (dyadic data),
+    fp32 within the Frobenius and element-wise bounds."""
+    Xd = torch.from_numpy(X).cuda()
+    Y = plan.spmm(Xd)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    lv = plan.info()["levels"]
+    heads = np.concatenate([plan.export_level(i)[0][:plan.level_info(i)["head"]] for i in range(lv)])
+    rows = np.unique(np.concatenate([heads, rng.integers(0, g.n, 20000), np.arange(max(0, g.n - 2000), g.n),
+                                     np.asarray(extra_rows, np.int64)])).astype(np.int64)
+    Ys = Y[torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64)
+    del Xd, Y
+    torch.cuda.empty_cache()
+    ref = oracle.spmm_rows(g.row_ptr, g.col, g.val, X, rows)
+    if dtype == "f64":
+        assert np.array_equal(Ys, ref)
+        return
+    assert np.linalg.norm(Ys - ref) / np.linalg.norm(ref) <= FP32_FRO
+    bound = oracle.spmm_rows(g.row_ptr, g.col, np.abs(g.val), np.abs(X).astype(np.float64), rows)
+    assert np.all(np.abs(Ys - ref) <= FP32_ELEM * bound + 1e-30)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("spec,b,k,dtype", [("RMAT(23,8,1)", 32768, 256, "f32"),   # full-warp rows, 2 slabs
+                                            ("RMAT(23,8,1)", 32768, 128, "f64"),   # fp64 full-warp rows
+                                            ("PATH(33554432,1)", 4096, 64, "f32")])  # 8-byte-lane rows
+def test_offsets_beyond_4GiB(spec, b, k, dtype):
+    """X and Y of 8 GiB each (n k s > 2^32): every gather, store and read-modify-write address above
+    4 GiB must be formed in 64 bits.  Sampled rows include the last 2000 rows (largest offsets)."""
+    g, dec = _big_decomposition(spec, b)
+    assert g.n * k * (8 if dtype == "f64" else 4) > 2 ** 32
+    plan = ab.Plan(decomposition=dec, dtype=dtype)
+    X = datagen.make_x(g.n, k, dtype=np.float64 if dtype == "f64" else np.float32)
+    _sampled_check(g, plan, X, dtype)
+    plan.close()
+
+
+@pytest.mark.slow
+def test_config_W_sampled():
+    """Config W (web-like WEB(24,1): 168 M nnz, b = 65536, 5 levels, k = 32 fp32) at the bench's
+    launch configuration, on sampled rows (the short-row kernel k_segsmall), plus fp64 bitwise."""
+    g, dec = _big_decomposition("WEB(24,1)", 65536)
+    for dtype in ("f32", "f64"):
+        plan = ab.Plan(decomposition=dec, dtype=dtype)
+        X = datagen.make_x(g.n, 32, dtype=np.float64 if dtype == "f64" else np.float32)
+        _sampled_check(g, plan, X, dtype)
+        plan.close()
+    _BIG.clear()
+
+
+def test_capture_inside_torch_cuda_graph():
+    """a caller that captures arrow_spmm into its own CUDA graph (torch.cuda.graph) gets the
+    kernels in that graph (the library skips its internal graph while the stream is capturing);
+    arrow_plan_reserve sizes every workspace first.  Replays with new X contents match O1 bitwise."""
+    g = datagen.rmat(12, 8, 7)
+    plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, 128, dtype="f64")
+    k = 16
+    plan.reserve(k)
+    X = torch.from_numpy(datagen.make_x(g.n, k, s_x=21)).cuda()
+    Y = torch.empty_like(X)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    plan.spmm(X, Y, stream=s)  # warm-up outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        plan.spmm(X, Y, stream=s)
+    for r in range(3):
+        Xh = datagen.make_x(g.n, k, s_x=30 + r)
+        X.copy_(torch.from_numpy(Xh))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy(), oracle.spmm(g.n, g.row_ptr, g.col, g.val, Xh)), r
