@@ -84,24 +84,18 @@ typedef struct {
     int32_t residual;           /* ARROW_RESIDUAL_*; default ERROR */
     int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (16384) */
     int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32) */
-    int32_t batch_segments;     /* segments per K-A work batch: 0 = default (16) or a power of two <= 32 */
+    int32_t batch_segments;     /* segments per K-A work batch of full-warp rows: 0 = default = 16 (the only
+                                   value accepted; short rows are taken 32 at a time) */
     int32_t band;               /* ARROW_BAND_*: step 3's band; default BLOCK */
     int32_t flags;              /* ARROW_FLAG_* bits; default 0 */
     int32_t transport;          /* ARROW_TRANSPORT_* (distributed plans); default AUTO */
-    int32_t prefetch_batches;   /* staged single-GPU schedule: L2 prefetch distance of K-A in work batches
-                                   (> 0: batch b prefetches the rows first gathered in batch b + distance);
-                                   0 = off (default; measured slower on B200) */
-    int32_t reserved[2];
+    int32_t reserved[3];
 } arrow_options;
 
 /* options.flags */
 enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each call directly instead of
                                           replaying one CUDA graph per (X, Y, k, stream) */
-       ARROW_FLAG_STAGED = 2,          /* single GPU schedule: levels >= 1 in one launch into staging rows
-                                          that level 0 adds (instead of one read-modify-write launch per level) */
-       ARROW_FLAG_KA_BROADCAST = 4,    /* full-warp rows: entries read by broadcast 16-byte loads (k_ka)
-                                          instead of coalesced loads + shuffles (k_seg32) */
-       ARROW_FLAGS_ALL = 7 };
+       ARROW_FLAGS_ALL = 1 };
 /* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
  * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
 enum { ARROW_TRANSPORT_AUTO = 0, ARROW_TRANSPORT_P2P = 1, ARROW_TRANSPORT_NCCL = 2 };

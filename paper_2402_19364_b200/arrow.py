@@ -22,7 +22,7 @@ ARROW_F32, ARROW_F64 = 0, 1
 ORDER = {"original": 0, "permuted": 1}
 RESIDUAL = {"error": 0, "csr": 1}
 BAND = {"block": 0, "strict": 1}    # ARROW_BAND_* (step 3 of LA-Decompose; strict = P:253 / Fig. 3)
-FLAG_NO_GRAPHS, FLAG_STAGED, FLAG_KA_BROADCAST = 1, 2, 4   # ARROW_FLAG_*
+FLAG_NO_GRAPHS = 1   # ARROW_FLAG_*
 TRANSPORT = {"auto": 0, "p2p": 1, "nccl": 2}
 STATUS = ["ARROW_OK", "ARROW_E_INVALID_ARG", "ARROW_E_BAD_CSR", "ARROW_E_NOT_SYMMETRIC", "ARROW_E_LEVELS",
           "ARROW_E_CUDA", "ARROW_E_NCCL", "ARROW_E_NOMEM", "ARROW_E_STATE", "ARROW_E_UNSUPPORTED"]
@@ -57,8 +57,7 @@ class Options(ctypes.Structure):
     _fields_ = [("compute", ctypes.c_int), ("seed", ctypes.c_uint64), ("order", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("window_rows", ctypes.c_int64), ("head_chunk", ctypes.c_int32),
                 ("batch_segments", ctypes.c_int32), ("band", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("transport", ctypes.c_int32), ("prefetch_batches", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("transport", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -168,7 +167,7 @@ def _dtype_code(dtype) -> int:
 
 def options(dtype=None, seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
             head_chunk: int = 0, batch_segments: int = 0, band: str = "block", flags: int = 0,
-            transport: str = "auto", prefetch_batches: int = 0) -> Options:
+            transport: str = "auto") -> Options:
     o = Options()
     _check(lib().arrow_options_default(ctypes.byref(o)), "arrow_options_default")
     o.compute = _dtype_code(dtype)
@@ -181,7 +180,6 @@ def options(dtype=None, seed: int = 4, order: str = "original", residual: str = 
     o.band = BAND[band]
     o.flags = flags
     o.transport = TRANSPORT[transport]
-    o.prefetch_batches = prefetch_batches
     return o
 
 
@@ -300,10 +298,9 @@ class Plan:
                  seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
                  head_chunk: int = 0, batch_segments: int = 0, comm=None,
                  decomposition: Optional[Decomposition] = None, band: str = "block", flags: int = 0,
-                 transport: str = "auto", prefetch_batches: int = 0):
+                 transport: str = "auto"):
         self._h = ctypes.c_void_p()
-        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments, band, flags, transport,
-                      prefetch_batches)
+        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments, band, flags, transport)
         comm_h = comm.handle if comm is not None else None
         if decomposition is not None:
             _check(lib().arrow_plan_create_from(decomposition._h, ctypes.byref(opt), comm_h, ctypes.byref(self._h)),

@@ -47,8 +47,6 @@ struct BuiltLevel {
     std::vector<uint32_t> keys;    // record stream (arrow_internal.h)
     std::vector<uint8_t> vals;     // plan dtype
     std::vector<int32_t> zero_rows;
-    std::vector<int64_t> wseg;     // [NW + 1] first segment of each tile window (stream order)
-    std::vector<int64_t> wpos;     // [NW + 1] first position of each window's rows (>= head)
     int64_t rows = 0, n_i = 0, head = 0, nnz = 0, head_nnz = 0, tiles = 0, nseg = 0;
     int mode = 0;
 };
@@ -115,9 +113,6 @@ void build_level(const HostLevel &L, int level_idx, int64_t b, int64_t window_ro
     for (int64_t w = 0; w < NW; ++w) { wrec[w + 1] += wrec[w]; wseg[w + 1] += wseg[w]; }
     const int64_t nrec = wrec[NW];
     B.nseg = wseg[NW];
-    B.wseg = wseg;
-    B.wpos.resize(NW + 1);
-    for (int64_t w = 0; w <= NW; ++w) B.wpos[w] = std::min(n_i, std::max(h, w * W));
     B.keys.resize(nrec);
     B.vals.assign(nrec * (pdt == ARROW_F64 ? 8 : 4), 0);
 #pragma omp parallel for schedule(dynamic, 1)
@@ -331,7 +326,7 @@ static int validate_decomposition(const arrow_decomposition_s &D, std::string &e
 // Single-GPU schedule, level by level (default): K-A level 0 stores every Y row it owns, then one
 // K-A launch per level >= 1 adds its rows into Y (read-modify-write, in level order) -- Alg. 2's
 // reverse aggregation with the permutations folded into the output rows (S4, S5).
-static arrow_status build_single_gpu_rmw(arrow_plan P, std::vector<BuiltLevel> &built, int bs) {
+static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &built, int bs) {
     const size_t es = P->esize();
     const size_t nlv = built.size();
     {
@@ -380,199 +375,10 @@ static arrow_status build_single_gpu_rmw(arrow_plan P, std::vector<BuiltLevel> &
         std::vector<uint8_t>().swap(B.vals);
         SegLevel S;
         std::string err;
-        const int e = upload_seg_level(hs, (int)es, bs, li == 0 ? 0 : 1, P->seg_allocs, S, err);
+        const int e = upload_seg_level(hs, (int)es, bs, li == 0 ? 0 : 1, P->n, P->seg_allocs, S, err);
         if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
         P->seg.push_back(S);
     }
-    P->n_post = (int64_t)post_rows.size();
-    if (P->n_post) {
-        CUDA_TRY(cudaMalloc(&P->post_rows, post_rows.size() * 4));
-        CUDA_TRY(cudaMemcpy(P->post_rows, post_rows.data(), post_rows.size() * 4, cudaMemcpyHostToDevice));
-    }
-    return ARROW_OK;
-}
-
-// Single-GPU schedule: levels >= 1 first, ONE K-A launch over all of them, writing
-// every body row into its own staging row and every head-row partial (atomically) into a per-(level,
-// head row) staging row; then K-A level 0, whose body row r ends with one pseudo-entry (staging row,
-// value 1) per level >= 1 that contributes to r, so that Y[r] is written exactly once, as
-//     Y[r] = sum_{level 0 entries} a X[c]  +  sum_{i >= 1} (P_{pi_i} Y_i)[r]        (Eq. (1))
-// -- Alg. 2's reverse aggregation of the level results done in registers instead of a
-// read-modify-write of Y per level.  Body staging rows are numbered in level 0's consumption order,
-// so level 0 reads them front to back.  Rows with contributions but no level-0 entries get a
-// level-0 segment of pseudo-entries only (appended after the windows).
-static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &built, int bs,
-                                     const arrow_decomposition_s &D, const std::vector<int32_t> *pos0) {
-    (void)D;
-    (void)pos0;
-    // L2 prefetch distance in batches (layout.cpp); off by default (measured slower)
-    const int64_t ahead = P->prefetch_batches > 0 ? P->prefetch_batches : 0;
-    const size_t es = P->esize();
-    const int64_t n = P->n;
-    const size_t nlv = built.size();
-    // zero-row list and the work counters (level 0 and the merged levels >= 1)
-    // contributions of levels >= 1 per output row, in level order: head slot (>= 0) or ~(body sequence)
-    std::vector<int64_t> cptr((size_t)n + 1, 0);
-    std::vector<int32_t> stamp((size_t)n, -1);  // level that last gave the row a head slot
-    std::vector<int64_t> hslot((size_t)n, -1);  // that head slot
-    for (size_t li = 1; li < nlv; ++li)
-        for (const uint32_t key : built[li].keys)
-            if (key & kPseudoRec) {
-                const uint32_t row = key & (kAuxRec - 1);
-                if (key & kAuxRec) {  // one contribution per (level, head row), however many chunks
-                    if (stamp[row] == (int32_t)li) continue;
-                    stamp[row] = (int32_t)li;
-                }
-                cptr[row + 1] += 1;
-            }
-    for (int64_t r = 0; r < n; ++r) cptr[r + 1] += cptr[r];
-    const int64_t ncontrib = cptr[n];
-    std::vector<int64_t> citem((size_t)ncontrib);
-    std::vector<int64_t> cfill(cptr.begin(), cptr.end() - 1);
-    int64_t nhead_slots = 0, nbody = 0;
-    std::fill(stamp.begin(), stamp.end(), -1);
-    for (size_t li = 1; li < nlv; ++li)
-        for (const uint32_t key : built[li].keys)
-            if (key & kPseudoRec) {
-                const uint32_t row = key & (kAuxRec - 1);
-                if (key & kAuxRec) {
-                    if (stamp[row] == (int32_t)li) continue;
-                    stamp[row] = (int32_t)li;
-                    hslot[row] = nhead_slots;
-                    citem[cfill[row]++] = nhead_slots++;
-                } else {
-                    citem[cfill[row]++] = ~nbody++;
-                }
-            }
-    // staging rows: [0, nhead_slots) head partials (zeroed every call), then body rows in level-0 order
-    std::vector<int64_t> body_slot((size_t)nbody, -1);
-    int64_t next_slot = nhead_slots;
-    std::vector<uint8_t> one(es);
-    put_val(one, 0, P->dtype, 1.0);
-    HostSegs h0;
-    std::vector<uint8_t> has_seg((size_t)n, 0);
-    auto append_staging = [&](uint32_t row) {
-        for (int64_t c = cptr[row]; c < cptr[row + 1]; ++c) {
-            int64_t slot = citem[c];
-            if (slot < 0) {
-                int64_t &bsl = body_slot[(size_t)~slot];
-                bsl = next_slot++;
-                slot = bsl;
-            }
-            h0.ent_col.push_back((int32_t)(kFlag | (uint32_t)slot));
-            h0.ent_val.insert(h0.ent_val.end(), one.begin(), one.end());
-        }
-    };
-    {
-        BuiltLevel &B = built[0];
-        h0.ent_val.reserve(B.vals.size() + (size_t)ncontrib * es);
-        for (size_t r = 0; r < B.keys.size(); ++r) {
-            const uint32_t key = B.keys[r];
-            if (key & kPseudoRec) {
-                const uint32_t row = key & (kAuxRec - 1);
-                // level 0 is every row's last write: body rows are final (iterate's activation)
-                if (!(key & kAuxRec)) {
-                    append_staging(row);
-                    has_seg[row] = 1;
-                }
-                h0.seg_out.push_back((int32_t)(((key & kAuxRec) ? kFlag : kFinalBit) | row));
-                h0.seg_end.push_back((uint32_t)h0.ent_col.size());
-            } else {
-                h0.ent_col.push_back((int32_t)(key & (kAuxRec - 1)));
-                h0.ent_val.insert(h0.ent_val.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
-            }
-        }
-        // rows with level >= 1 contributions but no level-0 entries: segments of pseudo-entries only.
-        // (A level-0 head row never has any: its entries are all captured at level 0.)
-        for (int64_t t = 0; t < std::min<int64_t>(B.head, (int64_t)B.zero_rows.size()); ++t)
-            if (cptr[B.zero_rows[t] + 1] > cptr[B.zero_rows[t]]) return fail(ARROW_E_STATE, "internal: level-0 head row with later contributions");
-        for (int64_t row = 0; row < n; ++row)
-            if (!has_seg[row] && cptr[row + 1] > cptr[row]) {
-                append_staging((uint32_t)row);
-                h0.seg_out.push_back((int32_t)(kFinalBit | (uint32_t)row));
-                h0.seg_end.push_back((uint32_t)h0.ent_col.size());
-                has_seg[row] = 2;
-            }
-        for (const int64_t v : body_slot)
-            if (v < 0) return fail(ARROW_E_STATE, "internal: a level >= 1 row without a level-0 reader");
-        // level-0 zero rows: its head rows first (they receive the head-row partials atomically), then
-        // the rows nothing writes
-        std::vector<int32_t> z(B.zero_rows.begin(), B.zero_rows.begin() + std::min<int64_t>(B.head, (int64_t)B.zero_rows.size()));
-        for (size_t t = z.size(); t < B.zero_rows.size(); ++t)
-            if (has_seg[B.zero_rows[t]] != 2) z.push_back(B.zero_rows[t]);
-        B.zero_rows.swap(z);
-        std::vector<uint32_t>().swap(B.keys);
-        std::vector<uint8_t>().swap(B.vals);
-    }
-    P->stage_rows = next_slot;
-    P->stage_head_rows = nhead_slots;
-    h0.pf_ahead = ahead;
-    // levels >= 1 (+ residual), concatenated in level order: body rows -> their staging rows (stores),
-    // head-row chunks -> their level's head staging rows (L2 reductions)
-    HostSegs ht;
-    {
-        int64_t seq = 0, hbase = 0;
-        for (size_t li = 1; li < nlv; ++li) {
-            BuiltLevel &B = built[li];
-            if (li > 1) ht.level_seg.push_back((int64_t)ht.seg_out.size());
-            int64_t nh = 0;
-            for (size_t r = 0; r < B.keys.size(); ++r) {
-                const uint32_t key = B.keys[r];
-                if (key & kPseudoRec) {
-                    const uint32_t row = key & (kAuxRec - 1);
-                    int64_t slot = -1;
-                    if (key & kAuxRec) {  // head slots of a level are numbered in first-chunk order
-                        if (stamp[row] != (int32_t)(nlv + li)) {
-                            stamp[row] = (int32_t)(nlv + li);
-                            hslot[row] = hbase + nh++;
-                        }
-                        slot = hslot[row];
-                        ht.seg_out.push_back((int32_t)(kFlag | (uint32_t)slot));
-                    } else {
-                        slot = body_slot[(size_t)seq++];
-                        ht.seg_out.push_back((int32_t)slot);
-                    }
-                    ht.seg_end.push_back((uint32_t)ht.ent_col.size());
-                } else {
-                    ht.ent_col.push_back((int32_t)(key & (kAuxRec - 1)));
-                    ht.ent_val.insert(ht.ent_val.end(), B.vals.begin() + r * es, B.vals.begin() + (r + 1) * es);
-                }
-            }
-            hbase += nh;
-            std::vector<uint32_t>().swap(B.keys);
-            std::vector<uint8_t>().swap(B.vals);
-        }
-    }
-    ht.pf_ahead = ahead;
-    if (P->stage_rows >= (int64_t)kRowMask30) return fail(ARROW_E_UNSUPPORTED, "staging rows exceed 2^30");
-    // device: zero rows + counters (arena), then the two segment layouts
-    {
-        const BuiltLevel &B = built[0];
-        const int64_t zb = align_up(std::max<int64_t>((int64_t)B.zero_rows.size() * 4, 1), 256);
-        const int64_t total = zb + 256;
-        cudaError_t e = cudaMalloc(&P->arena, (size_t)total);
-        if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(plan arena): ") + cudaGetErrorString(e));
-        P->arena_bytes = total;
-        DeviceLevel L0 = P->meta[0];
-        L0.zero_rows = reinterpret_cast<int32_t *>(P->arena);
-        L0.nzero = (int64_t)B.zero_rows.size();
-        CUDA_TRY(cudaMemcpy(L0.zero_rows, B.zero_rows.data(), B.zero_rows.size() * 4, cudaMemcpyHostToDevice));
-        P->levels.push_back(L0);
-        P->counters = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(P->arena) + zb);
-    }
-    std::string err;
-    SegLevel S0, ST;
-    int e = upload_seg_level(h0, (int)es, bs, 0, P->seg_allocs, S0, err);
-    if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
-    P->seg.push_back(S0);
-    if (!ht.seg_out.empty()) {
-        e = upload_seg_level(ht, (int)es, bs, 0, P->seg_allocs, ST, err);
-        if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
-        P->seg.push_back(ST);
-    }
-    // iterate mode: rows last written by head-row partials (level 0's head rows) get a post pass
-    std::vector<int32_t> post_rows(built[0].zero_rows.begin(),
-                                   built[0].zero_rows.begin() + std::min<int64_t>(built[0].head, (int64_t)built[0].zero_rows.size()));
     P->n_post = (int64_t)post_rows.size();
     if (P->n_post) {
         CUDA_TRY(cudaMalloc(&P->post_rows, post_rows.size() * 4));
@@ -594,8 +400,8 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         return fail(ARROW_E_INVALID_ARG, "bad options.order");
     if (opt.window_rows < 0 || opt.head_chunk < 0 || opt.batch_segments < 0)
         return fail(ARROW_E_INVALID_ARG, "negative window/chunk/batch");
-    if (opt.batch_segments > 32 || (opt.batch_segments & (opt.batch_segments - 1)) != 0)
-        return fail(ARROW_E_INVALID_ARG, "options.batch_segments must be 0 or a power of two <= 32");
+    if (opt.batch_segments != 0 && opt.batch_segments != kDefaultBatchSegs)
+        return fail(ARROW_E_INVALID_ARG, "options.batch_segments must be 0 or 16");
     if ((opt.flags & ~ARROW_FLAGS_ALL) != 0) return fail(ARROW_E_INVALID_ARG, "unknown options.flags bits");
     if (opt.transport < ARROW_TRANSPORT_AUTO || opt.transport > ARROW_TRANSPORT_NCCL)
         return fail(ARROW_E_INVALID_ARG, "bad options.transport");
@@ -623,10 +429,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         P->b = b;
         P->isolated = D.isolated;
         P->use_graphs = (opt.flags & ARROW_FLAG_NO_GRAPHS) == 0;
-        P->staged = (opt.flags & ARROW_FLAG_STAGED) != 0 && !comm;
-        P->launch.kernel = (opt.flags & ARROW_FLAG_KA_BROADCAST) ? 1 : 0;
         P->transport = opt.transport;
-        P->prefetch_batches = opt.prefetch_batches;
         P->nnz = (int64_t)D.res_u.size();
         for (auto &L : D.levels) P->nnz += L.row_ptr[L.rows];
         if (order == ARROW_ORDER_PERMUTED && !D.levels.empty()) {
@@ -678,7 +481,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     }
 
     if (!comm && !built.empty()) {
-        arrow_status st = P->staged ? build_single_gpu(P.get(), built, bs, D, pos0p) : build_single_gpu_rmw(P.get(), built, bs);
+        arrow_status st = build_single_gpu(P.get(), built, bs);
         if (st != ARROW_OK) return st;
     }
     P->local_begin = 0;
@@ -904,22 +707,8 @@ arrow_status arrow_plan_set_stream(arrow_plan plan, void *stream) {
     return ARROW_OK;
 }
 
-// single GPU: the staging rows of levels >= 1 (stage_rows x k), sized for the largest k seen
-static arrow_status ensure_ws(arrow_plan P, int64_t k) {
-    if (k <= P->ws_k || P->dist || P->stage_rows == 0) return ARROW_OK;
-    const int64_t bytes = P->stage_rows * k * (int64_t)P->esize();
-    if (P->ws) {
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
-        cudaFree(P->ws);
-        P->ws = nullptr;
-        P->ws_k = 0;
-    }
-    cudaError_t e = cudaMalloc(&P->ws, (size_t)bytes);
-    if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(staging rows): ") + cudaGetErrorString(e));
-    P->ws_k = k;
-    return ARROW_OK;
-}
+// k-dependent workspaces: none on one GPU (distributed plans size theirs in dist_spmm)
+static arrow_status ensure_ws(arrow_plan, int64_t) { return ARROW_OK; }
 
 arrow_status arrow_plan_reserve(arrow_plan plan, int64_t k_max) {
     if (!plan) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
@@ -975,45 +764,9 @@ static arrow_status enqueue_rmw(arrow_plan P, const void *X, void *Y, int64_t k,
 }
 
 static arrow_status enqueue_single(arrow_plan P, const void *X, void *Y, int64_t k, cudaStream_t st, int act = 0) {
-    const int dt = P->dtype == ARROW_F64 ? 1 : 0;
     if (P->profiling) P->prof_acc.calls += 1;
     P->prof_pos = 0;
-    if (!P->staged) return enqueue_rmw(P, X, Y, k, st, act);
-    const DeviceLevel &L0 = P->levels[0];
-    const bool staged = P->seg.size() > 1;
-    cudaEvent_t a = nullptr;
-    int e = 0;
-    CUDA_TRY(cudaMemsetAsync(P->counters, 0, 2 * sizeof(unsigned), st));
-    if (staged) {
-        // levels >= 1 in one launch: body rows -> staging rows, head-row partials -> the zeroed
-        // head staging rows (L2 reductions)
-        prof_begin(P, st, a);
-        if (P->stage_head_rows > 0)
-            CUDA_TRY(cudaMemsetAsync(P->ws, 0, (size_t)(P->stage_head_rows * k * (int64_t)P->esize()), st));
-        e = launch_seg(dt, 0, P->seg[1], X, nullptr, P->ws, nullptr, k, P->num_sms, P->counters + 1, st, P->launch);
-        prof_end(P, st, ARROW_K_SEGMENTS, a);
-        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A levels >= 1: ") + cudaGetErrorString((cudaError_t)e)); }
-    }
-    // S0/S3 on one GPU: level 0's head rows start at zero (its head-row slices add into them); the
-    // rows nothing writes are zeroed inside K-A level 0, a share per batch grab
-    const int64_t nh = std::min<int64_t>(L0.head, L0.nzero);
-    if (nh > 0) {
-        prof_begin(P, st, a);
-        e = launch_zero_rows(dt, L0.zero_rows, nh, k, Y, st);
-        prof_end(P, st, ARROW_K_HEAD_STAGE, a);
-        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
-    }
-    // level 0 (the last write of every Y row): its own entries + the staged rows of levels >= 1
-    prof_begin(P, st, a);
-    e = launch_seg(dt, staged ? 3 : 0, P->seg[0], X, staged ? P->ws : nullptr, Y, nullptr, k, P->num_sms, P->counters,
-                   st, P->launch, nullptr, act, L0.zero_rows + nh, L0.nzero - nh);
-    prof_end(P, st, ARROW_K_SEGMENTS, a);
-    if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A level 0: ") + cudaGetErrorString((cudaError_t)e)); }
-    if (act && P->n_post) {  // iterate mode: rows last written by head-row partials
-        e = launch_act_rows(dt, P->post_rows, P->n_post, k, act, Y, st);
-        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("activation pass: ") + cudaGetErrorString((cudaError_t)e)); }
-    }
-    return ARROW_OK;
+    return enqueue_rmw(P, X, Y, k, st, act);
 }
 
 arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void *stream) {
@@ -1038,18 +791,12 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
         if (e) return fail(ARROW_E_CUDA, cudaGetErrorString((cudaError_t)e));
         return ARROW_OK;
     }
-    // Single GPU: the whole call (memsets, K-Z, the two K-A launches) is captured once into a CUDA
+    // Single GPU: the whole call (memset, K-Z, one K-A launch per level) is captured once into a CUDA
     // graph per (X, Y, k, stream) and replayed.  Not while profiling (per-kernel events), on the
     // legacy stream, or when the caller is itself capturing `st` (its graph then receives the
-    // kernels directly; the staging rows must then exist already: arrow_plan_reserve).
+    // kernels directly).
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (st != nullptr) CUDA_TRY(cudaStreamIsCapturing(st, &cap));
-    if (P->ws_k < k && P->stage_rows > 0) {
-        if (cap != cudaStreamCaptureStatusNone)
-            return fail(ARROW_E_STATE, "staging rows for this k not reserved before stream capture (arrow_plan_reserve)");
-        arrow_status ws = ensure_ws(P, k);
-        if (ws != ARROW_OK) return ws;
-    }
     if (P->use_graphs && !P->profiling && !P->no_graph && st != nullptr && cap == cudaStreamCaptureStatusNone) {
         if (P->gexec && P->g_x == X && P->g_y == Y && P->g_k == k && P->g_stream == st) {
             CUDA_TRY(cudaGraphLaunch(P->gexec, st));
@@ -1109,8 +856,6 @@ arrow_status arrow_spmm_iterate(arrow_plan P, void *X, void *Y, int64_t k, int32
     CUDA_TRY(cudaGetDevice(&cur));
     if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    arrow_status ws = ensure_ws(P, k);
-    if (ws != ARROW_OK) return ws;
     for (int32_t t = 0; t < iters; ++t) {  // X_{t+1} = act(A X_t), ping-pong between X and Y
         const void *src = (t & 1) ? Y : X;
         void *dst = (t & 1) ? X : Y;

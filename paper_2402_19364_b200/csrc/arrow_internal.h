@@ -50,7 +50,7 @@ constexpr uint32_t kPseudoRec = 0x80000000u;
 constexpr uint32_t kFlag = 0x80000000u;
 constexpr uint32_t kAuxRec = 0x40000000u;
 constexpr int64_t kMaxRows = (int64_t)1 << 30;
-constexpr int kDefaultBatchSegs = 16;  // segments per K-A work batch (measured: 16-32 flat, 8 and 4 slower)
+constexpr int kDefaultBatchSegs = 16;  // segments per K-A work batch of full-warp rows (measured: 16 > 32)
 
 // metadata of one level (introspection) and its level-0 zero-row list
 struct DeviceLevel {
@@ -61,29 +61,26 @@ struct DeviceLevel {
 };
 
 // Segment layout of one level (the K-A input).  Segments (an output row, or one window's chunk of a
-// head row; never empty) are cut into batches of `bs` consecutive segments; each batch's entries
-// are contiguous and start at a multiple of 8 entries (the gap before a batch is padding).
+// head row; never empty) in tile-window order, their (col, val) entries contiguous; work batch b is
+// segments [b (bs+1), b (bs+1) + bs), starting at a multiple of 8 entries, and is followed by one
+// padding segment (output kDiscard) that fills the gap to the next batch.
 //   seg_out[nseg]  output row (bit 31: head-row partial, added atomically; bit 30: final write, iterate)
-//   seg_end[nseg]  end offset of the segment's entries (absolute, in the padded entry arrays)
+//   seg_end[nseg]  end offset of the segment's entries
 //   ent_col[nent]  X row of each entry (bit 31, distributed: row of the head block D0)
 //   ent_val[nent]  value (plan dtype)
 //   gmask[nent/8]  bit t of byte g: entry 8g + t is the last entry of its segment
-//   bat[2*nbatch]  (first entry, end entry) of batch b
-//   pf_rng[2*nbatch], pf_rows: L2 prefetch plan -- batch b requests rows pf_rows[pf_rng[2b] ..
-//                  pf_rng[2b+1]) (X rows; bit 31: a row of the second source, e.g. staging): the rows
-//                  whose first gather of their level is in batch b + ahead (null: no prefetch)
+//   bat[2*nbatch]  (first entry, end entry) of batch b's real segments
 struct SegLevel {
     int64_t nseg = 0, nent = 0, nbatch = 0;
     int bs = kDefaultBatchSegs;
     int mode = 0;
+    int64_t max_x_row = (int64_t)1 << 40;  // bound on the X / D0 rows referenced (32-bit offsets below 4 GiB)
     int32_t *seg_out = nullptr;
     uint32_t *seg_end = nullptr;
     int32_t *ent_col = nullptr;
     void *ent_val = nullptr;
     uint8_t *gmask = nullptr;
     uint32_t *bat = nullptr;
-    int32_t *pf_rows = nullptr;
-    uint32_t *pf_rng = nullptr;
 };
 
 // host form of a level's segment list before padding (layout.cpp input): seg_end relative to ent_col
@@ -92,15 +89,11 @@ struct HostSegs {
     std::vector<uint32_t> seg_end;
     std::vector<int32_t> ent_col;
     std::vector<uint8_t> ent_val;  // plan dtype, element size es
-    // L2 prefetch plan (optional): ahead > 0 batches; level boundaries (first segment of each level
-    // after the first) restart the first-reference bookkeeping
-    int64_t pf_ahead = 0;
-    std::vector<int64_t> level_seg;
 };
-// Pad into the batch layout and upload (cudaMalloc'ed pointers appended to `allocs`, freed by the
+// Build the end masks and batch table, and upload (cudaMalloc'ed pointers appended to `allocs`, freed by the
 // owner).  Returns 0 or a cudaError_t; `err` gets a message for layout errors (offsets beyond 32 bits).
-int upload_seg_level(const HostSegs &h, int es, int bs, int mode, std::vector<void *> &allocs, SegLevel &out,
-                     std::string &err);
+int upload_seg_level(const HostSegs &h, int es, int bs, int mode, int64_t max_x_row, std::vector<void *> &allocs,
+                     SegLevel &out, std::string &err);
 
 // Peer (NVLink) addressing of the distributed P2P transport: an encoded row is
 // (rank << kPeerShift | row) into the per-rank base pointers of a PeerPtrs; kParityBit marks a row
@@ -121,15 +114,13 @@ struct PeerPtrs {
 // single GPU: a body segment whose row receives no later contribution (arrow_spmm_iterate's
 // activation is applied when it is flushed); activations: 0 identity, 1 ReLU
 constexpr uint32_t kFinalBit = 0x40000000u;
+constexpr uint32_t kDiscard = 0x7fffffffu;  // seg_out of a padding segment: its result is dropped
 constexpr uint32_t kRowMask30 = 0x3fffffffu;
-// per-call K-A options (from arrow_options.flags)
-struct SegLaunch {
-    int kernel = 0;  // full-warp rows: 0 shuffle-entry k_seg32, 1 broadcast-entry k_ka
-};
+// per-call K-A options (from arrow_options; none at present)
+struct SegLaunch {};
 // dist: 0 single GPU, 1 distributed (head columns from D0, head partials into C0), 2 as 1 with
 // body rows stored through `outs` (encoded rows, levels >= 1 of the P2P transport) or, with
-// kLocalRmwBit, added into Y (rows whose home is this rank), 3 single GPU level 0 of the staged
-// schedule (entries with bit 31 read the staging rows passed as D0; flushes as 0)
+// kLocalRmwBit, added into Y (rows whose home is this rank)
 int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
                int num_sms, unsigned *counter, void *stream, const SegLaunch &opt, const PeerPtrs *outs = nullptr,
                int act = 0, const int32_t *zrows = nullptr, int64_t nzero = 0);

@@ -52,6 +52,12 @@ struct DistHostLevel {
 
 struct DistHost {
     int G = 1, me = 0;
+    // D0 / C0 row of head j of level i: NCCL transport = owner-major (level 0's heads first, then the
+    // heads of levels >= 1, each block ordered by owning rank), so Alg. 1's broadcast of D^(0) and
+    // reduction of C^(0) are one ncclBroadcast / ncclReduce per owner (rows [blk[r], blk[r+1]) of a
+    // block); P2P transport = level-major (d0_off[i] + j)
+    std::vector<std::vector<int32_t>> d0_index;
+    std::vector<int64_t> blk0, blk1;  // [G + 1] owner ranges of the level-0 block / levels >= 1 block
     int64_t lo = 0, hi = 0;
     std::vector<DistHostLevel> L;
     // peer-major, levels >= 1 concatenated per peer:
@@ -82,6 +88,7 @@ struct DistState {
     int nl = 0;
     int p2p = 0;
     std::vector<int64_t> h, d0_off;  // head rows per level, offset of the level inside D0 / C0
+    std::vector<int64_t> blk0, blk1; // NCCL: owner ranges of the level-0 / levels >= 1 head blocks
     int64_t d0_rows = 0;
     std::vector<SegLevel> seg;
     std::vector<int64_t> send_peer, recv_peer, out_peer, in_peer;
@@ -336,6 +343,36 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     // offset (source-major) inside rank t's buffers
     H.p2p = p2p;
     for (int i = 0; i < nl; ++i) H.d0_rows += D.levels[i].head;
+    H.d0_index.assign(nl, {});
+    H.blk0.assign(G + 1, 0);
+    H.blk1.assign(G + 1, 0);
+    {
+        int64_t off = 0;
+        if (p2p) {
+            for (int i = 0; i < nl; ++i) {
+                H.d0_index[i].resize(D.levels[i].head);
+                for (int64_t j = 0; j < D.levels[i].head; ++j) H.d0_index[i][j] = (int32_t)(off + j);
+                off += D.levels[i].head;
+            }
+        } else {
+            // two blocks (level 0 | levels >= 1), each owner-major; heads keep level, then j order
+            for (int blk = 0; blk < 2; ++blk) {
+                std::vector<int64_t> &bnd = blk == 0 ? H.blk0 : H.blk1;
+                const int i0 = blk == 0 ? 0 : 1, i1 = blk == 0 ? std::min(nl, 1) : nl;
+                const int64_t base = off;
+                for (int r = 0; r < G; ++r) {
+                    bnd[r] = off - base;
+                    for (int i = i0; i < i1; ++i) {
+                        const HostLevel &L = D.levels[i];
+                        H.d0_index[i].resize(L.head, -1);
+                        for (int64_t j = 0; j < L.head; ++j)
+                            if (owner(pos0[L.perm[j]]) == r) H.d0_index[i][j] = (int32_t)(off++);
+                    }
+                }
+                bnd[G] = off - base;
+            }
+        }
+    }
     std::vector<std::vector<std::vector<int64_t>>> HBt, SBt;
     if (p2p) {
         HBt.assign(G, std::vector<std::vector<int64_t>>(G, std::vector<int64_t>(nl, 0)));
@@ -408,8 +445,6 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                     out_slot[q - ha] = (int32_t)((p2p ? ((uint32_t)home << kPeerShift) : 0u) | (uint32_t)(ocur[home]++));
             }
         }
-        int64_t d0_off = 0;
-        for (int i2 = 0; i2 < i; ++i2) d0_off += D.levels[i2].head;
         for (int64_t j = 0; j < h; ++j) {
             const int64_t P0 = pos0[L.perm[j]];
             if (owner(P0) != me) continue;
@@ -418,9 +453,9 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             if (p2p)
                 for (int t = 0; t < G; ++t) {
                     H.d0push_src.push_back((int32_t)(P0 - lo));
-                    H.d0push_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)(d0_off + j)));
+                    H.d0push_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)H.d0_index[i][j]));
                     H.post.emplace_back((int32_t)(P0 - lo), (int32_t)(((uint32_t)t << kPeerShift) | kParityBit |
-                                                                       (uint32_t)(H.d0_rows + d0_off + j)));
+                                                                       (uint32_t)(H.d0_rows + H.d0_index[i][j])));
                 }
         }
         if (i == 0) {  // level 0: entry-less body rows of my home range; the A-isolated tail is a range
@@ -430,7 +465,7 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             H.zero_tail_n = std::max<int64_t>(0, hi - std::max(lo, L.n_i));
         }
         auto colmap = [&](int32_t q) -> int32_t {
-            if (q < h) return (int32_t)(kFlag | (uint32_t)q);
+            if (q < h) return (int32_t)(kFlag | (uint32_t)H.d0_index[i][q]);
             return (i == 0) ? (int32_t)(q - lo) : halo_slot[q - ha];
         };
         auto push_val = [&](double v) {
@@ -455,7 +490,7 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                 while (x0 < x1) {
                     const int64_t x2 = std::min<int64_t>(x1, x0 + head_chunk);
                     for (int64_t e = x0; e < x2; ++e) { DL.segs.ent_col.push_back(colmap(L.col[e])); push_val(L.val[e]); }
-                    DL.segs.seg_out.push_back((int32_t)(kFlag | (uint32_t)j));
+                    DL.segs.seg_out.push_back((int32_t)(kFlag | (uint32_t)H.d0_index[i][j]));
                     DL.segs.seg_end.push_back((uint32_t)DL.segs.ent_col.size());
                     x0 = x2;
                 }
@@ -605,6 +640,8 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         S->d0_off.push_back(S->d0_rows);
         S->d0_rows += H.L[i].h;
     }
+    S->blk0 = H.blk0;
+    S->blk1 = H.blk1;
     S->send_peer = H.send_peer;
     S->recv_peer = H.recv_peer;
     S->out_peer = H.out_peer;
@@ -647,11 +684,11 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         if (S->ws_rows >= ((int64_t)1 << 31))
             return set_error(ARROW_E_UNSUPPORTED, "distributed workspace exceeds 2^31 rows");
         // pre-exchange row mover: D0 (owned heads from X, the rest zero), C0 = 0, pack for peers and self
-        for (int i = 0; i < nl; ++i) {
-            std::vector<int32_t> own(S->h[i], -1);
-            for (size_t m = 0; m < H.L[i].head_j.size(); ++m) own[H.L[i].head_j[m]] = H.L[i].head_row[m];
-            for (int64_t j = 0; j < S->h[i]; ++j) { pre_src.push_back(own[j]); pre_dst.push_back((int32_t)(S->o_d0 + S->d0_off[i] + j)); }
-        }
+        for (int i = 0; i < nl; ++i)
+            for (size_t m = 0; m < H.L[i].head_j.size(); ++m) {
+                pre_src.push_back(H.L[i].head_row[m]);
+                pre_dst.push_back((int32_t)(S->o_d0 + H.d0_index[i][H.L[i].head_j[m]]));
+            }
         for (int64_t r = 0; r < S->d0_rows; ++r) { pre_src.push_back(-1); pre_dst.push_back((int32_t)(S->o_c0 + r)); }
         for (int64_t m = 0; m < n_send; ++m) { pre_src.push_back(H.send_idx_peers[m]); pre_dst.push_back((int32_t)(S->o_send + m)); }
         for (size_t m = 0; m < H.send_idx_self.size(); ++m) {
@@ -666,7 +703,7 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         for (int64_t m = 0; m < n_in; ++m) cpost.emplace_back(H.in_rows_peers[m], (int32_t)(S->o_in + m));
         for (int i = 0; i < nl; ++i)
             for (size_t m = 0; m < H.L[i].head_j.size(); ++m)
-                cpost.emplace_back(H.L[i].head_row[m], (int32_t)(S->o_c0 + S->d0_off[i] + H.L[i].head_j[m]));
+                cpost.emplace_back(H.L[i].head_row[m], (int32_t)(S->o_c0 + H.d0_index[i][H.L[i].head_j[m]]));
         build_csr(cself, sp, ss, sd);
         build_csr(cpost, pp, ps, pd);
     }
@@ -676,7 +713,9 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         // every output row is written once (mode 0): local Y (level 0) or a staging buffer
         SegLevel sg;
         std::string err;
-        const int e = upload_seg_level(H.L[i].segs, (int)P->esize(), bs, 0, S->allocs, sg, err);
+        // level 0 reads the local X rows (and D0), levels >= 1 the halo inside the workspace
+        const int64_t xr = (i == 0) ? std::max<int64_t>(S->hi - S->lo, S->d0_rows) : S->ws_rows;
+        const int e = upload_seg_level(H.L[i].segs, (int)P->esize(), bs, 0, xr, S->allocs, sg, err);
         if (e) return set_error(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
         H.L[i].segs = HostSegs();
         S->seg.push_back(sg);
@@ -829,7 +868,7 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     DCUDA(cudaStreamWaitEvent(st, S->ev[1], 0));
     const int m3 = M(st);
     for (int i = 1; i < nl; ++i)
-        DK(launch_seg(dt, 2, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), Y, row(c0 + S->d0_off[i]),
+        DK(launch_seg(dt, 2, S->seg[i], row(S->o_halo), row(S->o_d0), Y, row(c0),
                       k, sms, S->counters + i, st, P->launch, &S->ws_peer));
     const int m4 = M(st), m4b = M(st);
     // the A-isolated tail of Y (no level writes it) is zeroed while the other ranks finish
@@ -899,7 +938,13 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     // 2. (C) D0 of level 0; forward rows + D0 of the other levels
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
     const int m2 = M(S->cs);
-    DNCCL(ncclAllReduce(row(S->o_d0), row(S->o_d0), S->h[0] * k, nt, ncclSum, S->comm, S->cs));
+    // Alg. 1 line 1, Broadcast(D^(0)): every owner broadcasts its head rows of level 0 (owner-major block)
+    DNCCL(ncclGroupStart());
+    for (int r = 0; r < G; ++r)
+        if (S->blk0[r + 1] > S->blk0[r])
+            DNCCL(ncclBroadcast(row(S->o_d0 + S->blk0[r]), row(S->o_d0 + S->blk0[r]), (S->blk0[r + 1] - S->blk0[r]) * k,
+                                nt, r, S->comm, S->cs));
+    DNCCL(ncclGroupEnd());
     DCUDA(cudaEventRecord(S->ev[1], S->cs));
     DNCCL(ncclGroupStart());
     int64_t so = 0, ro = 0;
@@ -910,9 +955,10 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         so += S->send_peer[g];
         ro += S->recv_peer[g];
     }
-    if (S->d0_rows > S->h[0])
-        DNCCL(ncclAllReduce(row(S->o_d0 + S->h[0]), row(S->o_d0 + S->h[0]), (S->d0_rows - S->h[0]) * k, nt, ncclSum,
-                            S->comm, S->cs));
+    for (int r = 0; r < G; ++r)  // the other levels' head blocks, by owner
+        if (S->blk1[r + 1] > S->blk1[r])
+            DNCCL(ncclBroadcast(row(S->o_d0 + S->blk0[G] + S->blk1[r]), row(S->o_d0 + S->blk0[G] + S->blk1[r]),
+                                (S->blk1[r + 1] - S->blk1[r]) * k, nt, r, S->comm, S->cs));
     DNCCL(ncclGroupEnd());
     const int m3 = M(S->cs);
     DCUDA(cudaEventRecord(S->ev[2], S->cs));
@@ -924,8 +970,8 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
     DCUDA(cudaStreamWaitEvent(st, S->ev[2], 0));
     const int m6 = M(st);
     for (int i = 1; i < nl; ++i)
-        DK(launch_seg(dt, 1, S->seg[i], row(S->o_halo), row(S->o_d0 + S->d0_off[i]), row(S->o_out),
-                      row(S->o_c0 + S->d0_off[i]), k, sms, S->counters + i, st, P->launch));
+        DK(launch_seg(dt, 1, S->seg[i], row(S->o_halo), row(S->o_d0), row(S->o_out), row(S->o_c0), k, sms,
+                      S->counters + i, st, P->launch));
     const int m7 = M(st), m7b = M(st);
     DCUDA(cudaEventRecord(S->ev[3], st));
     // 4. (C) staging rows go home, head partials are reduced
@@ -941,7 +987,15 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
         so += S->out_peer[g];
         ro += S->in_peer[g];
     }
-    DNCCL(ncclAllReduce(row(S->o_c0), row(S->o_c0), S->d0_rows * k, nt, ncclSum, S->comm, S->cs));
+    // Alg. 1 line 3, Reduce(C^(0)): each head block's partials are reduced onto the rank that owns it
+    for (int r = 0; r < G; ++r) {
+        if (S->blk0[r + 1] > S->blk0[r])
+            DNCCL(ncclReduce(row(S->o_c0 + S->blk0[r]), row(S->o_c0 + S->blk0[r]), (S->blk0[r + 1] - S->blk0[r]) * k, nt,
+                             ncclSum, r, S->comm, S->cs));
+        if (S->blk1[r + 1] > S->blk1[r])
+            DNCCL(ncclReduce(row(S->o_c0 + S->blk0[G] + S->blk1[r]), row(S->o_c0 + S->blk0[G] + S->blk1[r]),
+                             (S->blk1[r + 1] - S->blk1[r]) * k, nt, ncclSum, r, S->comm, S->cs));
+    }
     DNCCL(ncclGroupEnd());
     const int m9 = M(S->cs);
     DCUDA(cudaEventRecord(S->ev[4], S->cs));

@@ -59,14 +59,10 @@ struct arrow_plan_s {
     std::vector<void *> seg_allocs;
     arrow::SegLaunch launch;       // per-call K-A options (options.flags)
     bool use_graphs = true;        // single GPU: replay the call as one CUDA graph (options.flags)
-    bool staged = false;           // single GPU: levels >= 1 into staging rows read by level 0 (flags)
     int32_t transport = 0;         // ARROW_TRANSPORT_* (distributed plans)
-    int32_t prefetch_batches = 0;  // options.prefetch_batches
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
-    void *ws = nullptr;            // single GPU: staging rows of levels >= 1 (stage_rows x ws_k)
+    void *ws = nullptr;            // (unused on one GPU; distributed plans keep theirs in DistState)
     int64_t ws_k = 0;
-    int64_t stage_rows = 0;        // staging rows: head partials of levels >= 1 first, then their body rows
-    int64_t stage_head_rows = 0;
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
     // arrow_spmm_host_batch: two device slots, two copy streams, per-slot events

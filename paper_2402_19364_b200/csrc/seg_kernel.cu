@@ -50,27 +50,6 @@ __device__ __forceinline__ void apply_act(Frag<T, VEC> &f, int act) {
     }
 }
 
-// First entry of segment s: batch starts are padded to a multiple of 8 entries, so a segment that
-// opens a layout batch starts at bat[s / bs].x, any other one where its predecessor ended.
-__device__ __forceinline__ uint32_t seg_begin(const uint32_t *__restrict__ seg_end, const uint2 *__restrict__ bat,
-                                              int bs, int64_t s) {
-    return (s % bs == 0) ? __ldg(&bat[s / bs].x) : __ldg(seg_end + s - 1);
-}
-
-// L2 prefetch plan (SegLevel::pf_*): batch wb requests the rows whose first gather in their level
-// happens `ahead` batches later -- X rows, or (bit 31) rows of the second source S (level 0's staging
-// rows) -- one prefetch.global.L2 per 128-byte line, so those gathers hit L2 instead of waiting on DRAM.
-__device__ __forceinline__ void prefetch_ahead(const int32_t *__restrict__ pf_rows, const uint32_t *__restrict__ pf_rng,
-                                               int64_t wb, const void *X, const void *S, uint32_t rb, int lane) {
-    if (pf_rng == nullptr) return;
-    const uint2 r = __ldg(reinterpret_cast<const uint2 *>(pf_rng) + wb);
-    for (uint32_t i = r.x + (uint32_t)lane; i < r.y; i += 32u) {
-        const int32_t row = __ldg(pf_rows + i);
-        const char *p = reinterpret_cast<const char *>(row < 0 ? S : X) + (uint64_t)((uint32_t)row & 0x7fffffffu) * rb;
-        for (uint32_t o = 0; o < rb; o += 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
-    }
-}
-
 // Folded K-Z: grab g of ngrab zeroes its share of outs.zrows (streaming stores of zero rows, no
 // dependence on anything the warp computes, so they drain while the warp gathers).  Lanes fetch
 // up to 32 row ids at once; the whole warp then stores row by row (lanes with col < k).
@@ -109,8 +88,9 @@ __device__ __forceinline__ void zero_share(const PeerPtrs &outs, int64_t g, int6
 template <typename T, int VEC, int MODE, int DIST>
 __device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T *Y, T *C0, int64_t k, int64_t col0,
                                           const PeerPtrs &outs) {
+    if (o == (int32_t)kDiscard) return;  // a padding segment
     if (o < 0) {
-        T *dst = (DIST == 1 || DIST == 2) ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
+        T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
         atomic_add_frag<T, VEC>(dst + col0, acc);
     } else if (DIST == 2 && (o & kLocalRmwBit)) {
         T *py = Y + (int64_t)(o & kPeerRowMask) * k + col0;
@@ -123,8 +103,8 @@ __device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T 
         st_stream<T, VEC>(base + (int64_t)(o & kPeerRowMask) * k + col0, acc);
     } else {
         // single GPU: bit 30 marks the row's final segment (iterate mode applies the activation)
-        const bool fin = (DIST == 0 || DIST == 3) && (o & kFinalBit) && outs.act;
-        T *py = Y + (int64_t)((DIST == 0 || DIST == 3) ? (o & kRowMask30) : o) * k + col0;
+        const bool fin = DIST == 0 && (o & kFinalBit) && outs.act;
+        T *py = Y + (int64_t)(DIST == 0 ? (o & kRowMask30) : o) * k + col0;
         Frag<T, VEC> y = acc;
         if (MODE != 0) {
             y = ld_plain<T, VEC>(py);
@@ -192,6 +172,7 @@ __device__ __forceinline__ const char *row_addr(int32_t c, const char *Xl, const
     return Xl + (uint64_t)(uint32_t)c * rb;
 }
 
+// One group of 8 entries starting at e (a multiple of 8); the first n are this warp's; m = end mask.
 template <typename T, int VEC, int MODE, int DIST, bool FULL>
 __device__ __forceinline__ void ka_group(const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
                                          uint32_t e, int n, unsigned m, const char *Xl, const char *Dl, uint32_t rb,
@@ -225,28 +206,30 @@ __device__ __forceinline__ void ka_group(const int32_t *__restrict__ ent_col, co
     }
 }
 
+// A warp takes one work batch of (up to) 16 segments at a time (measured: 16 better than 32 at
+// k = 128); a batch starts at a multiple of 8 entries and usually ends inside a group of 8.
 template <typename T, int VEC, int MODE, int DIST>
-__global__ void __launch_bounds__(256, (sizeof(T) == 8 || DIST == 1 || DIST == 2) ? 3 : 4) k_ka(const int32_t *__restrict__ seg_out, int64_t nseg,
+__global__ void __launch_bounds__(256, (sizeof(T) == 8 || DIST) ? 3 : 4) k_ka(const int32_t *__restrict__ seg_out,
+                                               const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
                                                const uint8_t *__restrict__ gmask, const uint2 *__restrict__ bat,
-                                               int bs, const int32_t *__restrict__ pf_rows,
-                                               const uint32_t *__restrict__ pf_rng, const T *__restrict__ X,
-                                               const T *__restrict__ D0, T *__restrict__ Y, T *__restrict__ C0,
-                                               int64_t k, unsigned *__restrict__ counter, const PeerPtrs outs) {
+                                               int64_t nbatch, const T *__restrict__ X, const T *__restrict__ D0,
+                                               T *__restrict__ Y, T *__restrict__ C0, int64_t k, uint32_t rb,
+                                               unsigned *__restrict__ counter, const PeerPtrs outs) {
+    // rb = k * sizeof(T), a 32-bit parameter: every gather address is then ONE IMAD.WIDE.U32
     const int lane = threadIdx.x & 31;
-    const int64_t nbatch = (nseg + bs - 1) / bs;
-    const uint32_t rb = (uint32_t)(k * (int64_t)sizeof(T));
+    (void)seg_end;
     for (;;) {
         unsigned wb = 0;
         if (lane == 0) wb = atomicAdd(counter, 1u);
         wb = __shfl_sync(0xffffffffu, wb, 0);
         if ((int64_t)wb >= nbatch) break;
-        const int64_t s0 = (int64_t)wb * bs;
-        const int nb = (nseg - s0 < bs) ? (int)(nseg - s0) : bs;
-        const int32_t my_out = (lane < nb) ? __ldg(seg_out + s0 + lane) : 0;
+        // batch wb: segments [wb * 17, wb * 17 + 16) (the last batch may be shorter), entries be
+        const int64_t s0 = (int64_t)wb * 17;
+        const int32_t my_out = (lane < 16 && s0 + lane < nseg) ? __ldg(seg_out + s0 + lane) : 0;
         const uint2 be = __ldg(bat + wb);
-        prefetch_ahead(pf_rows, pf_rng, wb, X, D0, rb, lane);
-        if (MODE == 0 && (DIST == 0 || DIST == 3)) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
+        const uint32_t e_lo = be.x, e_hi = be.y;
+        if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
 
         for (int64_t c0 = 0; c0 < k; c0 += 32 * VEC) {
             const int64_t col0 = c0 + (int64_t)lane * VEC;
@@ -258,17 +241,18 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 8 || DIST == 1 || DIST == 2
             Frag<T, VEC> acc;
             acc.zero();
             int cur = 0;
-            uint32_t e = be.x;
+            uint32_t e = e_lo;  // (a multiple of 8)
 #pragma unroll 1
-            for (; e + 8u <= be.y; e += 8u) {
+            for (; e + 8u <= e_hi; e += 8u) {
                 const unsigned m = __ldg(gmask + (e >> 3));
                 ka_group<T, VEC, MODE, DIST, true>(ent_col, ent_val, e, 8, m, Xl, Dl, rb, acc, cur, my_out, Y, C0, k,
                                                     col0, outs);
             }
-            if (e < be.y) {
-                const unsigned m = __ldg(gmask + (e >> 3));
-                ka_group<T, VEC, MODE, DIST, false>(ent_col, ent_val, e, (int)(be.y - e), m, Xl, Dl, rb, acc, cur,
-                                                     my_out, Y, C0, k, col0, outs);
+            if (e < e_hi) {  // the last group: the padding segment's end bit beyond it is masked off
+                const int n = (int)(e_hi - e);
+                const unsigned m = __ldg(gmask + (e >> 3)) & ((1u << n) - 1u);
+                ka_group<T, VEC, MODE, DIST, false>(ent_col, ent_val, e, n, m, Xl, Dl, rb, acc, cur, my_out, Y, C0, k,
+                                                     col0, outs);
             }
         }
     }
@@ -283,135 +267,152 @@ int run_ka(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
         if (b <= 0) b = 1;
     }
-    const int64_t nbatch = (L.nseg + L.bs - 1) / L.bs;
-    int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (nbatch + 7) / 8);
+    int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (L.nbatch + 7) / 8);
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.nseg, L.ent_col, reinterpret_cast<const T *>(L.ent_val),
-                                           L.gmask, reinterpret_cast<const uint2 *>(L.bat), L.bs, L.pf_rows, L.pf_rng,
+    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col, reinterpret_cast<const T *>(L.ent_val),
+                                           L.gmask, reinterpret_cast<const uint2 *>(L.bat), L.nbatch,
                                            reinterpret_cast<const T *>(X), reinterpret_cast<const T *>(D0),
-                                           reinterpret_cast<T *>(Y), reinterpret_cast<T *>(C0), k, counter, outs);
+                                           reinterpret_cast<T *>(Y), reinterpret_cast<T *>(C0), k,
+                                           (uint32_t)(k * (int64_t)sizeof(T)), counter, outs);
     return (int)cudaGetLastError();
 }
 
-// ------------------------------------------------------------------------------------ K-A (full warp, shuffle entries)
-// The same full-warp rows as k_ka, with the batch's (col, val) pairs loaded coalesced -- one pair
-// per lane per 32-entry chunk -- and handed to the warp by shuffles (two SHFL per entry); a per-chunk
-// bit mask of segment ends (__reduce_or_sync) drives the flushes.  Groups of 8 entries are gathered
-// before their first use; groups without a segment end skip the end tests.
-template <typename T, int VEC, int MODE, int DIST>
-__device__ __forceinline__ void seg32_group(int32_t mycol, T myval, int u0, int n, unsigned grp, const char *Xl,
-                                            const char *Dl, uint32_t rb, Frag<T, VEC> &acc, int &cur, int32_t my_out,
-                                            T *Y, T *C0, int64_t k, int64_t col0, const PeerPtrs &outs) {
-    Frag<T, VEC> xv[8];
-    T av[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const int32_t col = __shfl_sync(0xffffffffu, mycol, (u0 + t) & 31);
-        av[t] = __shfl_sync(0xffffffffu, myval, (u0 + t) & 31);
-        if (t < n) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(row_addr<T, VEC, DIST>(col, Xl, Dl, rb)));
-        else xv[t].zero();
-    }
-    if (n == 8 && grp == 0u) {  // warp-uniform: no segment ends in this group
-#pragma unroll
-        for (int t = 0; t < 8; ++t) fma_frag<T, VEC>(acc, av[t], xv[t]);
-        return;
-    }
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        if (t < n) fma_frag<T, VEC>(acc, av[t], xv[t]);
-        if ((grp >> t) & 1u) {  // (only set for t < n)
-            const int32_t o = __shfl_sync(0xffffffffu, my_out, cur & 31);
-            flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
-            acc.zero();
-            ++cur;
-        }
-    }
+template <typename T, int VEC>
+int run_ka_mode(int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
+                unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
+    if (dist == 2) return run_ka<T, VEC, 0, 2>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
+    if (dist) return run_ka<T, VEC, 0, 1>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
+    return L.mode == 0 ? run_ka<T, VEC, 0, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, st)
+                       : run_ka<T, VEC, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
 }
 
-template <typename T, int VEC, int MODE, int DIST>
-__global__ void __launch_bounds__(256, (sizeof(T) == 8 || DIST == 1 || DIST == 2) ? 3 : 4)
-k_seg32(const int32_t *__restrict__ seg_out, const uint32_t *__restrict__ seg_end, int64_t nseg,
-        const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val, const uint2 *__restrict__ bat, int bs,
-        const T *__restrict__ X, const T *__restrict__ D0, T *__restrict__ Y, T *__restrict__ C0, int64_t k,
-        unsigned *__restrict__ counter, const PeerPtrs outs) {
+// ------------------------------------------------------------------------------------ K-A
+// Segment stream.  A sub-warp of LPE lanes owns a row slab of LPE*VEC elements.  Work is a list
+// of non-empty segments in tile-window order, cut into batches of LPE consecutive segments.
+// Warps grab batches dynamically from a per-launch counter (one atomic per warp per grab), so
+// all resident warps work on a narrow, advancing front of the window-ordered list and the X rows
+// of the current window stay L2-resident while every user of them runs (the IO lemma's "tiles
+// stay resident").  Lane s of a sub-warp holds the output row and end offset of
+// segment s of its batch; the batch's entries are contiguous and are streamed in chunks of LPE
+// (one coalesced load of col and val per lane).  A per-chunk bit mask of segment ends
+// (__reduce_or_sync) tells the accumulate loop where to flush; UNROLL row loads are issued
+// before their FMAs so short rows do not serialise on latency.
+//   out >= 0             : store (MODE 0, level 0) or read-modify-write (MODE 1) Y[out]
+//   out <  0, DIST == 0  : atomic add into Y[out & 0x7fffffff]  (head-row slice of one window)
+//   out <  0, DIST == 1  : atomic add into C0[out & 0x7fffffff] (head partial, reduced over ranks)
+//   col <  0 (DIST only) : the row comes from the head block D0 (broadcast), else from X
+//   DIST == 2            : out >= 0 encodes (rank << kPeerShift | row): the row is stored into
+//                          rank's staging buffer outs.p[rank] -- over NVLink for a peer rank;
+//                          with kLocalRmwBit it is added into Y[row] (a row homed on this GPU)
+template <typename T, int VEC, int LPE, int MODE, int DIST>
+__global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__ seg_out,
+                                                     const uint32_t *__restrict__ seg_end, int64_t nseg,
+                                                     const int32_t *__restrict__ ent_col,
+                                                     const T *__restrict__ ent_val, const T *__restrict__ X,
+                                                     const T *__restrict__ D0, T *__restrict__ Y,
+                                                     T *__restrict__ C0, int64_t k, unsigned *__restrict__ counter,
+                                                     int bseg, const PeerPtrs outs) {
+    constexpr int UNROLL = (LPE == 32) ? 8 : 4;
+    constexpr int SLAB = LPE * VEC;
+    constexpr int SUBS = 32 / LPE;
     const int lane = threadIdx.x & 31;
-    const int64_t nbatch = (nseg + bs - 1) / bs;
-    const uint32_t rb = (uint32_t)(k * (int64_t)sizeof(T));
+    const int sl = lane % LPE;
+    const int sub = lane / LPE;
+    const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (sub * LPE));
+    const int64_t nbatch = (nseg + bseg - 1) / bseg;
+    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
+
     for (;;) {
         unsigned wb = 0;
         if (lane == 0) wb = atomicAdd(counter, 1u);
         wb = __shfl_sync(0xffffffffu, wb, 0);
-        if ((int64_t)wb >= nbatch) break;
-        const int64_t s0 = (int64_t)wb * bs;
-        const int nb = (nseg - s0 < bs) ? (int)(nseg - s0) : bs;
-        const int32_t my_out = (lane < nb) ? __ldg(seg_out + s0 + lane) : 0;
-        const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
-        const uint2 be = __ldg(bat + wb);
-        if (MODE == 0 && (DIST == 0 || DIST == 3)) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
-        for (int64_t c0 = 0; c0 < k; c0 += 32 * VEC) {
-            const int64_t col0 = c0 + (int64_t)lane * VEC;
-            const char *Xl, *Dl;
-            asm("mov.b64 %0, %1;" : "=l"(Xl) : "l"(reinterpret_cast<const char *>(X + col0)));
-            asm("mov.b64 %0, %1;" : "=l"(Dl) : "l"(reinterpret_cast<const char *>(DIST ? D0 + col0 : X + col0)));
+        const int64_t bt = (int64_t)wb * SUBS + sub;
+        if ((int64_t)wb * SUBS >= nbatch) break;       // warp-uniform exit
+        if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, (nbatch + SUBS - 1) / SUBS, Y, k, lane);
+        if (bt >= nbatch) continue;                    // sub-warp idle this round
+        const int64_t s0 = bt * bseg;
+        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
+        const int32_t my_out = (sl < nb) ? __ldg(seg_out + s0 + sl) : 0;
+        const uint32_t my_end = (sl < nb) ? __ldg(seg_end + s0 + sl) : 0xffffffffu;
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(mask, my_end, nb - 1, LPE);
+
+        for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
+            const int64_t col0 = c0 + (int64_t)sl * VEC;
+            const bool active = col0 < k;
+            const char *xlane = reinterpret_cast<const char *>(X + (active ? col0 : 0));
+            const char *dlane = reinterpret_cast<const char *>(D0 + (active ? col0 : 0));
             Frag<T, VEC> acc;
             acc.zero();
             int cur = 0;
-            for (uint32_t cb = be.x; cb < be.y; cb += 32) {
-                const int cnt = (be.y - cb < 32u) ? (int)(be.y - cb) : 32;
+            for (uint32_t cb = e_begin; cb < e_end; cb += LPE) {
+                const int cnt = (e_end - cb < (uint32_t)LPE) ? (int)(e_end - cb) : LPE;
                 int32_t mycol = 0;
                 T myval = T(0);
-                if (lane < cnt) {
-                    mycol = __ldcs(ent_col + cb + lane);
-                    myval = __ldcs(ent_val + cb + lane);
+                if (sl < cnt) {
+                    mycol = __ldcs(ent_col + cb + sl);
+                    myval = __ldcs(ent_val + cb + sl);
                 }
-                const uint32_t rel = my_end - 1u - cb;
-                const unsigned endmask = __reduce_or_sync(0xffffffffu, (rel < 32u) ? (1u << rel) : 0u);
+                const uint32_t rel = my_end - 1u - cb;  // position of my segment's last entry in this chunk
+                const unsigned endmask = __reduce_or_sync(mask, (rel < (uint32_t)LPE) ? (1u << rel) : 0u);
 #pragma unroll 1
-                for (int u0 = 0; u0 < cnt; u0 += 8) {
-                    const unsigned grp = (endmask >> u0) & 0xffu;
-                    seg32_group<T, VEC, MODE, DIST>(mycol, myval, u0, min(cnt - u0, 8), grp, Xl, Dl, rb, acc, cur,
-                                                    my_out, Y, C0, k, col0, outs);
+                for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
+                    Frag<T, VEC> xv[UNROLL];
+                    T av[UNROLL];
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+                        const int idx = u0 + t;
+                        const uint32_t cc = (uint32_t)__shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
+                        const T a = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
+                        const bool ok = idx < cnt;
+                        av[t] = ok ? a : T(0);
+                        const char *p;
+                        if (DIST && (int32_t)cc < 0) p = dlane + (uint64_t)(cc & 0x7fffffffu) * rowbytes;
+                        else p = xlane + (uint64_t)cc * rowbytes;
+                        if (ok && active) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
+                        else xv[t].zero();
+                    }
+#pragma unroll
+                    for (int t = 0; t < UNROLL; ++t) {
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
+                        if ((u0 + t < cnt) && ((endmask >> ((u0 + t) & 31)) & 1u)) {   // sub-warp uniform
+                            const int32_t o = __shfl_sync(mask, my_out, cur, LPE);
+                            if (active && o != (int32_t)kDiscard) {
+                                if (o < 0) {
+                                    T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
+                                    atomic_add_frag<T, VEC>(dst + col0, acc);
+                                } else if (DIST == 2 && (o & kLocalRmwBit)) {
+                                    T *py = Y + (int64_t)(o & kPeerRowMask) * k + col0;
+                                    Frag<T, VEC> y = ld_plain<T, VEC>(py);
+#pragma unroll
+                                    for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                    st_plain<T, VEC>(py, y);
+                                } else if (DIST == 2) {
+                                    T *base = reinterpret_cast<T *>(outs.p[(uint32_t)o >> kPeerShift]);
+                                    st_stream<T, VEC>(base + (int64_t)(o & kPeerRowMask) * k + col0, acc);
+                                } else {
+                                    const bool fin = DIST == 0 && (o & kFinalBit) && outs.act;
+                                    T *py = Y + (int64_t)(DIST == 0 ? (o & kRowMask30) : o) * k + col0;
+                                    Frag<T, VEC> y = acc;
+                                    if (MODE != 0) {
+                                        y = ld_plain<T, VEC>(py);
+#pragma unroll
+                                        for (int i = 0; i < VEC; ++i) y.v[i] += acc.v[i];
+                                    }
+                                    if (fin) apply_act<T, VEC>(y, outs.act);
+                                    if (MODE == 0) st_stream<T, VEC>(py, y);
+                                    else st_plain<T, VEC>(py, y);
+                                }
+                            }
+                            acc.zero();
+                            ++cur;
+                        }
+                    }
                 }
             }
         }
     }
-}
-
-template <typename T, int VEC, int MODE, int DIST>
-int run_seg32(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-              unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    auto kern = k_seg32<T, VEC, MODE, DIST>;
-    static int b = 0;
-    if (b == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
-        if (b <= 0) b = 1;
-    }
-    const int64_t nbatch = (L.nseg + L.bs - 1) / L.bs;
-    int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (nbatch + 7) / 8);
-    if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col, reinterpret_cast<const T *>(L.ent_val),
-                                           reinterpret_cast<const uint2 *>(L.bat), L.bs, reinterpret_cast<const T *>(X),
-                                           reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
-                                           reinterpret_cast<T *>(C0), k, counter, outs);
-    return (int)cudaGetLastError();
-}
-
-// full-warp rows: the broadcast-entry kernel (k_ka) or the shuffle-entry kernel (k_seg32)
-template <typename T, int VEC, int MODE, int DIST>
-int run_full(int kern, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-             unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    return kern == 1 ? run_ka<T, VEC, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st)
-                     : run_seg32<T, VEC, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-}
-
-template <typename T, int VEC>
-int run_ka_mode(int kern, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                int num_sms, unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    if (dist == 3) return run_full<T, VEC, 0, 3>(kern, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    if (dist == 2) return run_full<T, VEC, 0, 2>(kern, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    if (dist) return run_full<T, VEC, 0, 1>(kern, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    return L.mode == 0 ? run_full<T, VEC, 0, 0>(kern, L, X, D0, Y, C0, k, num_sms, counter, outs, st)
-                       : run_full<T, VEC, 1, 0>(kern, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
 }
 
 // ------------------------------------------------------------------------------------ K-A (short rows)
@@ -420,9 +421,7 @@ int run_ka_mode(int kern, int dist, const SegLevel &L, const void *X, const void
 // warp instruction gathers G rows.  Sub-warps keep private partial sums while no segment ends in
 // a step; in a step with ends, the partials are folded (butterfly over the sub-warps), the step's
 // products are combined by a segmented inclusive scan across the sub-warps, and every sub-warp
-// whose entry closes a segment flushes that row -- several rows per step, in parallel.  The next
-// chunk's (col, val) pairs are requested before this chunk's rows are gathered, and a whole
-// 32-entry chunk's rows are loaded before the first is used.
+// whose entry closes a segment flushes that row -- several rows per step, in parallel.
 template <typename T, int VEC>
 __device__ __forceinline__ Frag<T, VEC> shfl_frag(const Frag<T, VEC> &f, int src_or_delta, int mode) {
     Frag<T, VEC> r;
@@ -434,23 +433,24 @@ __device__ __forceinline__ Frag<T, VEC> shfl_frag(const Frag<T, VEC> &f, int src
     return r;
 }
 
-template <typename T, int VEC, int LPE, int MODE, int DIST>
+template <typename T, int VEC, int LPE, int MODE, int DIST, bool OFF32, bool PF>
 __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__ seg_out,
                                                      const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                      const int32_t *__restrict__ ent_col,
-                                                     const T *__restrict__ ent_val, const uint2 *__restrict__ bat,
-                                                     int bs, const int32_t *__restrict__ pf_rows,
-                                                     const uint32_t *__restrict__ pf_rng, const T *__restrict__ X,
+                                                     const T *__restrict__ ent_val, const T *__restrict__ X,
                                                      const T *__restrict__ D0, T *__restrict__ Y, T *__restrict__ C0,
-                                                     int64_t k, unsigned *__restrict__ counter, const PeerPtrs outs) {
+                                                     int64_t k, unsigned *__restrict__ counter, int bseg,
+                                                     const PeerPtrs outs) {
     constexpr int G = 32 / LPE;
-    constexpr int U = (32 / G) < 8 ? (32 / G) : 8;  // steps whose rows are loaded together
+    // steps whose rows are loaded together (PF: a whole 32-entry chunk when it fits in 8 steps)
+    constexpr int UMAX = PF ? 8 : 4;
+    constexpr int U = (32 / G) < UMAX ? (32 / G) : UMAX;
     const int lane = threadIdx.x & 31;
     const int q = lane / LPE;   // sub-warp: entry slot within a step
     const int sl = lane % LPE;  // 16-byte slice of the row
     const int64_t col0 = (int64_t)sl * VEC;
     const uint32_t lane_off = (uint32_t)(col0 * (int64_t)sizeof(T));
-    const int64_t nbatch = (nseg + bs - 1) / bs;
+    const int64_t nbatch = (nseg + bseg - 1) / bseg;
     const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
     const char *Xc = reinterpret_cast<const char *>(X);
     const char *Dc = reinterpret_cast<const char *>(D0);
@@ -460,39 +460,48 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
         if (lane == 0) wb = atomicAdd(counter, 1u);
         wb = __shfl_sync(0xffffffffu, wb, 0);
         if ((int64_t)wb >= nbatch) break;
-        const int64_t s0 = (int64_t)wb * bs;
-        const int nb = (nseg - s0 < bs) ? (int)(nseg - s0) : bs;
+        const int64_t s0 = (int64_t)wb * bseg;
+        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
         const int32_t my_out = (lane < nb) ? __ldg(seg_out + s0 + lane) : 0;
         const uint32_t my_end = (lane < nb) ? __ldg(seg_end + s0 + lane) : 0xffffffffu;
-        const uint2 be = __ldg(bat + wb);
-        const uint32_t e_begin = be.x, e_end = be.y;
-        prefetch_ahead(pf_rows, pf_rng, wb, X, D0, rowbytes, lane);
-        if (MODE == 0 && (DIST == 0 || DIST == 3)) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
-        if (MODE == 1 && DIST == 0 && lane < nb && my_out >= 0)  // RMW levels: the batch's Y rows into L2
+        const uint32_t e_begin = (s0 == 0) ? 0u : __ldg(seg_end + s0 - 1);
+        const uint32_t e_end = __shfl_sync(0xffffffffu, my_end, nb - 1);
+        if (MODE == 0 && DIST == 0) zero_share<T, VEC>(outs, wb, nbatch, Y, k, lane);
+        if (MODE == 1 && DIST == 0 && lane < nb && my_out >= 0 && my_out != (int32_t)kDiscard)  // RMW: Y rows into L2
             asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const char *>(Y) +
                                                                   (uint64_t)(uint32_t)(my_out & kRowMask30) * rowbytes));
 
         Frag<T, VEC> acc;
         acc.zero();
         int cur = 0;  // segments of the batch closed so far
+        // PF: the next chunk's (col, val) are requested before this chunk's rows are gathered, so a
+        // chunk costs one memory latency (its gathers) instead of two
         int32_t pcol = 0;
         T pval = T(0);
-        if (e_begin + lane < e_end) {
+        if (PF && e_begin + lane < e_end) {
             pcol = __ldcs(ent_col + e_begin + lane);
             pval = __ldcs(ent_val + e_begin + lane);
         }
         for (uint32_t cb = e_begin; cb < e_end; cb += 32) {
             const int cnt = (e_end - cb < 32u) ? (int)(e_end - cb) : 32;
-            const int32_t mycol = pcol;
-            const T myval = pval;
-            if (cb + 32 + lane < e_end) {
-                pcol = __ldcs(ent_col + cb + 32 + lane);
-                pval = __ldcs(ent_val + cb + 32 + lane);
+            int32_t mycol = 0;
+            T myval = T(0);
+            if (PF) {
+                mycol = pcol;
+                myval = pval;
+                if (cb + 32 + lane < e_end) {
+                    pcol = __ldcs(ent_col + cb + 32 + lane);
+                    pval = __ldcs(ent_val + cb + 32 + lane);
+                }
+            } else if (lane < cnt) {
+                mycol = __ldcs(ent_col + cb + lane);
+                myval = __ldcs(ent_val + cb + lane);
             }
             const uint32_t rel = my_end - 1u - cb;
             const unsigned endmask = __reduce_or_sync(0xffffffffu, (rel < 32u) ? (1u << rel) : 0u);
 #pragma unroll 1
             for (int g0 = 0; g0 < cnt; g0 += G * U) {
+                // U steps' rows are requested before the first is used (memory-level parallelism)
                 Frag<T, VEC> xs[U];
                 T vals[U];
 #pragma unroll
@@ -502,6 +511,7 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
                     vals[t] = __shfl_sync(0xffffffffu, myval, e & 31);
                     const char *p;
                     if (DIST && col < 0) p = Dc + (uint64_t)((uint32_t)col & 0x7fffffffu) * rowbytes + lane_off;
+                    else if (OFF32) p = Xc + (uint32_t)((uint32_t)col * rowbytes + lane_off);
                     else p = Xc + (uint64_t)(uint32_t)col * rowbytes + lane_off;
                     if (e < cnt) xs[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
                     else xs[t].zero();
@@ -581,129 +591,40 @@ __global__ void __launch_bounds__(256, 4) k_segsmall(const int32_t *__restrict__
 
 template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segsmall(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-                 unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    auto kern = k_segsmall<T, VEC, LPE, MODE, DIST>;
-    static int b = 0;
+                 unsigned *counter, const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    const int bseg = 32;
+    // the next chunk's entries requested one chunk ahead, whole-chunk row loads (PF)
+    auto kern = off32 ? k_segsmall<T, VEC, LPE, MODE, DIST, true, true> : k_segsmall<T, VEC, LPE, MODE, DIST, false, true>;
+    static int bps[2] = {0, 0};
+    int &b = bps[off32 ? 1 : 0];
     if (b == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0);
         if (b <= 0) b = 1;
     }
-    const int64_t nbatch = (L.nseg + L.bs - 1) / L.bs;
+    const int64_t nbatch = (L.nseg + bseg - 1) / bseg;
     int64_t blocks = std::min<int64_t>((int64_t)num_sms * b, (nbatch + 7) / 8);
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
-                                           reinterpret_cast<const T *>(L.ent_val),
-                                           reinterpret_cast<const uint2 *>(L.bat), L.bs, L.pf_rows, L.pf_rng,
-                                           reinterpret_cast<const T *>(X), reinterpret_cast<const T *>(D0),
-                                           reinterpret_cast<T *>(Y), reinterpret_cast<T *>(C0), k, counter, outs);
+                                           reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                           reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
+                                           reinterpret_cast<T *>(C0), k, counter, bseg, outs);
     return (int)cudaGetLastError();
 }
 
 template <typename T, int VEC, int LPE>
 int run_segsmall_mode(int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                      int num_sms, unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    if (dist == 3) return run_segsmall<T, VEC, LPE, 0, 3>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    if (dist == 2) return run_segsmall<T, VEC, LPE, 0, 2>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    if (dist) return run_segsmall<T, VEC, LPE, 0, 1>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    return L.mode == 0 ? run_segsmall<T, VEC, LPE, 0, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, st)
-                       : run_segsmall<T, VEC, LPE, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-}
-
-// ------------------------------------------------------------------------------------ K-A (generic)
-// Any k and alignment: a sub-warp of LPE lanes owns a row slab of LPE*VEC elements and a batch of
-// LPE consecutive segments (lane s holds segment s's output row and end offset); the batch's entries
-// are streamed in chunks of LPE (one coalesced load of col and val per lane), a per-chunk bit mask
-// of segment ends (__reduce_or_sync) tells the accumulate loop where to flush, and UNROLL row loads
-// are issued before their FMAs.
-template <typename T, int VEC, int LPE, int MODE, int DIST>
-__global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__ seg_out,
-                                                     const uint32_t *__restrict__ seg_end, int64_t nseg,
-                                                     const int32_t *__restrict__ ent_col,
-                                                     const T *__restrict__ ent_val, const uint2 *__restrict__ bat,
-                                                     int bs, const T *__restrict__ X, const T *__restrict__ D0,
-                                                     T *__restrict__ Y, T *__restrict__ C0, int64_t k,
-                                                     unsigned *__restrict__ counter, int bseg, const PeerPtrs outs) {
-    constexpr int UNROLL = (LPE == 32) ? 8 : 4;
-    constexpr int SLAB = LPE * VEC;
-    constexpr int SUBS = 32 / LPE;
-    const int lane = threadIdx.x & 31;
-    const int sl = lane % LPE;
-    const int sub = lane / LPE;
-    const unsigned mask = (LPE == 32) ? 0xffffffffu : (((1u << LPE) - 1u) << (sub * LPE));
-    const int64_t nbatch = (nseg + bseg - 1) / bseg;
-    const uint32_t rowbytes = (uint32_t)(k * (int64_t)sizeof(T));
-
-    for (;;) {
-        unsigned wb = 0;
-        if (lane == 0) wb = atomicAdd(counter, 1u);
-        wb = __shfl_sync(0xffffffffu, wb, 0);
-        const int64_t bt = (int64_t)wb * SUBS + sub;
-        if ((int64_t)wb * SUBS >= nbatch) break;       // warp-uniform exit
-        if (MODE == 0 && (DIST == 0 || DIST == 3)) zero_share<T, VEC>(outs, wb, (nbatch + SUBS - 1) / SUBS, Y, k, lane);
-        if (bt >= nbatch) continue;                    // sub-warp idle this round
-        const int64_t s0 = bt * bseg;
-        const int nb = (nseg - s0 < bseg) ? (int)(nseg - s0) : bseg;
-        const int32_t my_out = (sl < nb) ? __ldg(seg_out + s0 + sl) : 0;
-        const uint32_t my_end = (sl < nb) ? __ldg(seg_end + s0 + sl) : 0xffffffffu;
-        const uint32_t e_begin = seg_begin(seg_end, bat, bs, s0);
-        const uint32_t e_end = __shfl_sync(mask, my_end, nb - 1, LPE);
-
-        for (int64_t c0 = 0; c0 < k; c0 += SLAB) {
-            const int64_t col0 = c0 + (int64_t)sl * VEC;
-            const bool active = col0 < k;
-            const char *xlane = reinterpret_cast<const char *>(X + (active ? col0 : 0));
-            const char *dlane = reinterpret_cast<const char *>(D0 + (active ? col0 : 0));
-            Frag<T, VEC> acc;
-            acc.zero();
-            int cur = 0;
-            for (uint32_t cb = e_begin; cb < e_end; cb += LPE) {
-                const int cnt = (e_end - cb < (uint32_t)LPE) ? (int)(e_end - cb) : LPE;
-                int32_t mycol = 0;
-                T myval = T(0);
-                if (sl < cnt) {
-                    mycol = __ldcs(ent_col + cb + sl);
-                    myval = __ldcs(ent_val + cb + sl);
-                }
-                const uint32_t rel = my_end - 1u - cb;  // position of my segment's last entry in this chunk
-                const unsigned endmask = __reduce_or_sync(mask, (rel < (uint32_t)LPE) ? (1u << rel) : 0u);
-#pragma unroll 1
-                for (int u0 = 0; u0 < cnt; u0 += UNROLL) {
-                    Frag<T, VEC> xv[UNROLL];
-                    T av[UNROLL];
-#pragma unroll
-                    for (int t = 0; t < UNROLL; ++t) {
-                        const int idx = u0 + t;
-                        const uint32_t cc = (uint32_t)__shfl_sync(mask, mycol, idx & (LPE - 1), LPE);
-                        const T a = __shfl_sync(mask, myval, idx & (LPE - 1), LPE);
-                        const bool ok = idx < cnt;
-                        av[t] = ok ? a : T(0);
-                        const char *p;
-                        if (DIST && (int32_t)cc < 0) p = dlane + (uint64_t)(cc & 0x7fffffffu) * rowbytes;
-                        else p = xlane + (uint64_t)cc * rowbytes;
-                        if (ok && active) xv[t] = ld_x<T, VEC>(reinterpret_cast<const T *>(p));
-                        else xv[t].zero();
-                    }
-#pragma unroll
-                    for (int t = 0; t < UNROLL; ++t) {
-#pragma unroll
-                        for (int i = 0; i < VEC; ++i) acc.v[i] = fma(av[t], xv[t].v[i], acc.v[i]);
-                        if ((u0 + t < cnt) && ((endmask >> ((u0 + t) & 31)) & 1u)) {   // sub-warp uniform
-                            const int32_t o = __shfl_sync(mask, my_out, cur, LPE);
-                            if (active) flush_row<T, VEC, MODE, DIST>(o, acc, Y, C0, k, col0, outs);
-                            acc.zero();
-                            ++cur;
-                        }
-                    }
-                }
-            }
-        }
-    }
+                      int num_sms, unsigned *counter, const PeerPtrs &outs, bool off32, cudaStream_t st) {
+    if (dist == 2) return run_segsmall<T, VEC, LPE, 0, 2>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st);
+    if (dist) return L.mode == 0 ? run_segsmall<T, VEC, LPE, 0, 1>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st)
+                                 : run_segsmall<T, VEC, LPE, 1, 1>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st);
+    return L.mode == 0 ? run_segsmall<T, VEC, LPE, 0, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st)
+                       : run_segsmall<T, VEC, LPE, 1, 0>(L, X, D0, Y, C0, k, num_sms, counter, outs, off32, st);
 }
 
 template <typename T, int VEC, int LPE, int MODE, int DIST>
 int run_segments(const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k, int num_sms,
-                 unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    const int bseg = std::min(LPE, L.bs);  // divides the layout's batch size (both powers of two)
+                 unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
+    if (bseg <= 0 || bseg > LPE) bseg = LPE;
     auto kern = k_segments<T, VEC, LPE, MODE, DIST>;
     static int bps = 0;
     if (bps == 0) {
@@ -715,36 +636,37 @@ int run_segments(const SegLevel &L, const void *X, const void *D0, void *Y, void
     int64_t blocks = std::min<int64_t>((int64_t)num_sms * bps, (nbatch + batches_per_block - 1) / batches_per_block);
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, 256, 0, st>>>(L.seg_out, L.seg_end, L.nseg, L.ent_col,
-                                            reinterpret_cast<const T *>(L.ent_val),
-                                            reinterpret_cast<const uint2 *>(L.bat), L.bs,
-                                            reinterpret_cast<const T *>(X), reinterpret_cast<const T *>(D0),
-                                            reinterpret_cast<T *>(Y), reinterpret_cast<T *>(C0), k, counter, bseg,
-                                            outs);
+                                            reinterpret_cast<const T *>(L.ent_val), reinterpret_cast<const T *>(X),
+                                            reinterpret_cast<const T *>(D0), reinterpret_cast<T *>(Y),
+                                            reinterpret_cast<T *>(C0), k, counter, bseg, outs);
     return (int)cudaGetLastError();
 }
 
 template <typename T, int VEC, int MODE, int DIST>
 int run_segments_lpe(int lpe, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0, int64_t k,
-                     int num_sms, unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
+                     int num_sms, unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
     switch (lpe) {
-        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, outs, st);
+        case 32: return run_segments<T, VEC, 32, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 16: return run_segments<T, VEC, 16, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 8: return run_segments<T, VEC, 8, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 4: return run_segments<T, VEC, 4, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        case 2: return run_segments<T, VEC, 2, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+        default: return run_segments<T, VEC, 1, MODE, DIST>(L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
     }
 }
 
 template <typename T, int VEC>
 int run_segments_mode(int lpe, int dist, const SegLevel &L, const void *X, const void *D0, void *Y, void *C0,
-                      int64_t k, int num_sms, unsigned *counter, const PeerPtrs &outs, cudaStream_t st) {
-    if (dist == 3) return run_segments_lpe<T, VEC, 0, 3>(lpe, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    if (dist == 2) return run_segments_lpe<T, VEC, 0, 2>(lpe, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    if (dist) return run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
-    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, outs, st)
-                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, outs, st);
+                      int64_t k, int num_sms, unsigned *counter, int bseg, const PeerPtrs &outs, cudaStream_t st) {
+    if (dist == 2) return run_segments_lpe<T, VEC, 0, 2>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+    if (dist) {
+        return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st)
+                           : run_segments_lpe<T, VEC, 1, 1>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
+    }
+    return L.mode == 0 ? run_segments_lpe<T, VEC, 0, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st)
+                       : run_segments_lpe<T, VEC, 1, 0>(lpe, L, X, D0, Y, C0, k, num_sms, counter, bseg, outs, st);
 }
+
 
 }  // namespace
 }  // namespace kseg
@@ -759,46 +681,50 @@ int launch_seg(int dtype, int dist, const SegLevel &L, const void *X, const void
     PeerPtrs po{};
     if (outs) po = *outs;
     po.act = act;
-    if ((dist == 0 || dist == 3) && nzero > 0) {
+    (void)opt;
+    if (dist == 0 && nzero > 0) {
         po.zrows = zrows;
         po.nzero = nzero;
     }
     if (dist == 2 && !outs) return (int)cudaErrorInvalidValue;
-    int vec = dist == 3 ? pick_vec(dtype, k, {X, Y, D0}) : dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
+    int vec = dist ? pick_vec(dtype, k, {X, Y, D0, C0}) : pick_vec(dtype, k, {X, Y});
     if (dist == 2)
         for (const void *p : po.p) vec = std::min(vec, pick_vec(dtype, k, {p}));
     const int lpe = pick_lpe(k, vec);
+    // 32-bit X offsets when every X (and D0) row offset fits
+    const bool off32 = (uint64_t)L.max_x_row * (uint64_t)k * (dtype == 1 ? 8u : 4u) < (1ull << 32) - (1ull << 20);
+    const int bseg = 16;
     // full-warp rows (k = 128 fp32 / 64 fp64 and multiples): the broadcast-entry kernel
     if (lpe == 32 && k % (32 * vec) == 0) {
-        if (dtype == 0 && vec == 4) return run_ka_mode<float, 4>(opt.kernel, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-        if (dtype == 1 && vec == 2) return run_ka_mode<double, 2>(opt.kernel, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+        if (dtype == 0 && vec == 4) return run_ka_mode<float, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+        if (dtype == 1 && vec == 2) return run_ka_mode<double, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
     }
     // short rows (k = 8/16/32 fp32, 4/8/16/32 fp64 with 16-byte lanes): G entries per warp step,
     // segmented scan across the sub-warps
     if (lpe < 32 && lpe >= 2 && k == (int64_t)lpe * vec && vec == 16 / (dtype == 1 ? 8 : 4)) {
         if (dtype == 0) {
-            if (lpe == 16) return run_segsmall_mode<float, 4, 16>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-            if (lpe == 8) return run_segsmall_mode<float, 4, 8>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-            if (lpe == 4) return run_segsmall_mode<float, 4, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-            return run_segsmall_mode<float, 4, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+            if (lpe == 16) return run_segsmall_mode<float, 4, 16>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 8) return run_segsmall_mode<float, 4, 8>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 4) return run_segsmall_mode<float, 4, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            return run_segsmall_mode<float, 4, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
         } else {
-            if (lpe == 16) return run_segsmall_mode<double, 2, 16>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-            if (lpe == 8) return run_segsmall_mode<double, 2, 8>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-            if (lpe == 4) return run_segsmall_mode<double, 2, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-            return run_segsmall_mode<double, 2, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+            if (lpe == 16) return run_segsmall_mode<double, 2, 16>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 8) return run_segsmall_mode<double, 2, 8>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            if (lpe == 4) return run_segsmall_mode<double, 2, 4>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
+            return run_segsmall_mode<double, 2, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, off32, st);
         }
     }
     // fp32 rows of 64 elements: one row per warp with 8-byte lanes (one 256-byte request per entry)
     // instead of 16-lane sub-warps that run different batches in lockstep
     if (dtype == 0 && k == 64 && vec >= 2)
-        return run_ka_mode<float, 2>(opt.kernel, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+        return run_ka_mode<float, 2>(dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
     if (dtype == 0) {
-        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+        if (vec == 4) return run_segments_mode<float, 4>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
+        if (vec == 2) return run_segments_mode<float, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
+        return run_segments_mode<float, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
     }
-    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
-    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, po, st);
+    if (vec == 2) return run_segments_mode<double, 2>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
+    return run_segments_mode<double, 1>(lpe, dist, L, X, D0, Y, C0, k, num_sms, counter, bseg, po, st);
 }
 
 }  // namespace arrow
