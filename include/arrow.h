@@ -95,7 +95,11 @@ typedef struct {
 /* options.flags */
 enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each call directly instead of
                                           replaying one CUDA graph per (X, Y, k, stream) */
-       ARROW_FLAGS_ALL = 1 };
+       ARROW_FLAG_DETERMINISTIC = 2,   /* single GPU: bitwise reproducible results -- the head-row partials of
+                                          each tile window are stored into their own slots and added in a
+                                          fixed order by a per-level epilogue (K-C, Alg. 1 line 3) instead of
+                                          L2 atomics (costs time: DESIGN.md §7) */
+       ARROW_FLAGS_ALL = 3 };
 /* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
  * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
 enum { ARROW_TRANSPORT_AUTO = 0, ARROW_TRANSPORT_P2P = 1, ARROW_TRANSPORT_NCCL = 2 };

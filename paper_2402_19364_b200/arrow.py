@@ -22,7 +22,7 @@ ARROW_F32, ARROW_F64 = 0, 1
 ORDER = {"original": 0, "permuted": 1}
 RESIDUAL = {"error": 0, "csr": 1}
 BAND = {"block": 0, "strict": 1}    # ARROW_BAND_* (step 3 of LA-Decompose; strict = P:253 / Fig. 3)
-FLAG_NO_GRAPHS = 1   # ARROW_FLAG_*
+FLAG_NO_GRAPHS, FLAG_DETERMINISTIC = 1, 2   # ARROW_FLAG_*
 TRANSPORT = {"auto": 0, "p2p": 1, "nccl": 2}
 STATUS = ["ARROW_OK", "ARROW_E_INVALID_ARG", "ARROW_E_BAD_CSR", "ARROW_E_NOT_SYMMETRIC", "ARROW_E_LEVELS",
           "ARROW_E_CUDA", "ARROW_E_NCCL", "ARROW_E_NOMEM", "ARROW_E_STATE", "ARROW_E_UNSUPPORTED"]

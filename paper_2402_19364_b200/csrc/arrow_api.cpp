@@ -355,16 +355,44 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
     std::vector<int32_t> post_rows;
     for (int64_t r = 0; r < P->n; ++r)
         if (last[r] >= 0 && (last[r] & 1)) post_rows.push_back((int32_t)r);
+    P->det_levels.resize(nlv);
     for (size_t li = 0; li < nlv; ++li) {
         BuiltLevel &B = built[li];
         HostSegs hs;
         hs.ent_val.reserve(B.vals.size());
+        // deterministic head partials (ARROW_FLAG_DETERMINISTIC): chunk c of head row j is stored into
+        // slot hstart[j] + (its ordinal among j's chunks); K-C adds the slots of j in order into Y
+        std::vector<int64_t> nchunk, hstart;
+        std::vector<int32_t> hrows;
+        std::vector<int32_t> hidx;  // row -> head index of this level
+        if (P->det) {
+            hidx.assign((size_t)P->n, -1);
+            for (const uint32_t key : B.keys)
+                if ((key & kPseudoRec) && (key & kAuxRec)) {
+                    const uint32_t row = key & (kAuxRec - 1);
+                    if (hidx[row] < 0) {
+                        hidx[row] = (int32_t)hrows.size();
+                        hrows.push_back((int32_t)row);
+                        nchunk.push_back(0);
+                    }
+                    ++nchunk[hidx[row]];
+                }
+            hstart.assign(hrows.size() + 1, 0);
+            for (size_t j = 0; j < hrows.size(); ++j) hstart[j + 1] = hstart[j] + nchunk[j];
+            std::fill(nchunk.begin(), nchunk.end(), 0);
+            P->det_slots = std::max(P->det_slots, hstart.back());
+        }
         for (size_t r = 0; r < B.keys.size(); ++r) {
             const uint32_t key = B.keys[r];
             if (key & kPseudoRec) {
                 const uint32_t row = key & (kAuxRec - 1);
                 const bool fin = !(key & kAuxRec) && last[row] == (int32_t)(2 * li);
-                hs.seg_out.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (fin ? kFinalBit : 0u) | row));
+                if (P->det && (key & kAuxRec)) {
+                    const int32_t j = hidx[row];
+                    hs.seg_out.push_back((int32_t)(kFlag | (uint32_t)(hstart[j] + nchunk[j]++)));
+                } else {
+                    hs.seg_out.push_back((int32_t)(((key & kAuxRec) ? kFlag : 0u) | (fin ? kFinalBit : 0u) | row));
+                }
                 hs.seg_end.push_back((uint32_t)hs.ent_col.size());
             } else {
                 hs.ent_col.push_back((int32_t)(key & (kAuxRec - 1)));
@@ -378,6 +406,24 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
         const int e = upload_seg_level(hs, (int)es, bs, li == 0 ? 0 : 1, P->n, P->seg_allocs, S, err);
         if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
         P->seg.push_back(S);
+        if (P->det && !hrows.empty()) {  // K-C of this level: CSR (head row -> its slots, in order)
+            std::vector<int32_t> ptr(hstart.begin(), hstart.end()), src((size_t)hstart.back());
+            for (size_t t = 0; t < src.size(); ++t) src[t] = (int32_t)t;
+            if (hstart.back() >= ((int64_t)1 << 31)) return fail(ARROW_E_UNSUPPORTED, "too many head-row chunks");
+            DetLevel &DLv = P->det_levels[li];
+            DLv.nh = (int64_t)hrows.size();
+            auto up = [&](const std::vector<int32_t> &v) -> int32_t * {
+                void *d = nullptr;
+                if (cudaMalloc(&d, std::max<size_t>(v.size() * 4, 16)) != cudaSuccess) return nullptr;
+                P->seg_allocs.push_back(d);
+                if (!v.empty() && cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+                return (int32_t *)d;
+            };
+            DLv.ptr = up(ptr);
+            DLv.src = up(src);
+            DLv.rows = up(hrows);
+            if (!DLv.ptr || !DLv.src || !DLv.rows) return fail(ARROW_E_CUDA, "upload of the head-combine lists failed");
+        }
     }
     P->n_post = (int64_t)post_rows.size();
     if (P->n_post) {
@@ -406,7 +452,9 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     if (opt.transport < ARROW_TRANSPORT_AUTO || opt.transport > ARROW_TRANSPORT_NCCL)
         return fail(ARROW_E_INVALID_ARG, "bad options.transport");
     const int64_t window_rows = opt.window_rows > 0 ? opt.window_rows : kDefaultWindowRows;
-    const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : kDefaultHeadChunk;
+    // deterministic head partials: one chunk per (head row, window) unless asked otherwise (fewer slots)
+    const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk
+                               : ((opt.flags & ARROW_FLAG_DETERMINISTIC) && !comm) ? (int32_t)0x3fffffff : kDefaultHeadChunk;
     const int bs = opt.batch_segments > 0 ? opt.batch_segments : kDefaultBatchSegs;
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
     const int64_t n = D.n, b = D.b;
@@ -429,6 +477,7 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
         P->b = b;
         P->isolated = D.isolated;
         P->use_graphs = (opt.flags & ARROW_FLAG_NO_GRAPHS) == 0;
+        P->det = (opt.flags & ARROW_FLAG_DETERMINISTIC) != 0 && !comm;
         P->transport = opt.transport;
         P->nnz = (int64_t)D.res_u.size();
         for (auto &L : D.levels) P->nnz += L.row_ptr[L.rows];
@@ -707,8 +756,21 @@ arrow_status arrow_plan_set_stream(arrow_plan plan, void *stream) {
     return ARROW_OK;
 }
 
-// k-dependent workspaces: none on one GPU (distributed plans size theirs in dist_spmm)
-static arrow_status ensure_ws(arrow_plan, int64_t) { return ARROW_OK; }
+// k-dependent workspace on one GPU: the head-partial slots of the deterministic mode (det_slots x k)
+static arrow_status ensure_ws(arrow_plan P, int64_t k) {
+    if (k <= P->ws_k || P->dist || !P->det || P->det_slots == 0) return ARROW_OK;
+    if (P->ws) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { P->poisoned = true; return fail(ARROW_E_CUDA, cudaGetErrorString(e)); }
+        cudaFree(P->ws);
+        P->ws = nullptr;
+        P->ws_k = 0;
+    }
+    cudaError_t e = cudaMalloc(&P->ws, (size_t)(P->det_slots * k * (int64_t)P->esize()));
+    if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(head-partial slots): ") + cudaGetErrorString(e));
+    P->ws_k = k;
+    return ARROW_OK;
+}
 
 arrow_status arrow_plan_reserve(arrow_plan plan, int64_t k_max) {
     if (!plan) return fail(ARROW_E_INVALID_ARG, "plan is NULL");
@@ -751,10 +813,17 @@ static arrow_status enqueue_rmw(arrow_plan P, const void *X, void *Y, int64_t k,
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-Z: ") + cudaGetErrorString((cudaError_t)e)); }
         }
         prof_begin(P, st, a);
-        e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, nullptr, k, P->num_sms, P->counters + i, st, P->launch, nullptr,
-                       act, i == 0 ? L.zero_rows + nh : nullptr, i == 0 ? L.nzero - nh : 0);
+        e = launch_seg(dt, 0, P->seg[i], X, nullptr, Y, P->det ? P->ws : nullptr, k, P->num_sms, P->counters + i, st,
+                       P->launch, nullptr, act, i == 0 ? L.zero_rows + nh : nullptr, i == 0 ? L.nzero - nh : 0);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
+        if (P->det && P->det_levels[i].nh > 0) {  // S3, K-C: Y[head] += its chunk partials, in chunk order
+            const DetLevel &DLv = P->det_levels[i];
+            prof_begin(P, st, a);
+            e = launch_gather_add(dt, P->ws, DLv.ptr, DLv.src, DLv.rows, DLv.nh, k, Y, st);
+            prof_end(P, st, ARROW_K_HEAD_EPI, a);
+            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-C: ") + cudaGetErrorString((cudaError_t)e)); }
+        }
     }
     if (act && P->n_post) {  // iterate mode: rows last written by head-row partials
         const int e = launch_act_rows(dt, P->post_rows, P->n_post, k, act, Y, st);
@@ -797,6 +866,12 @@ arrow_status arrow_spmm_ex(arrow_plan P, const void *X, void *Y, int64_t k, void
     // kernels directly).
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (st != nullptr) CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    if (P->det && P->ws_k < k) {
+        if (cap != cudaStreamCaptureStatusNone)
+            return fail(ARROW_E_STATE, "workspace for this k not reserved before stream capture (arrow_plan_reserve)");
+        arrow_status ws = ensure_ws(P, k);
+        if (ws != ARROW_OK) return ws;
+    }
     if (P->use_graphs && !P->profiling && !P->no_graph && st != nullptr && cap == cudaStreamCaptureStatusNone) {
         if (P->gexec && P->g_x == X && P->g_y == Y && P->g_k == k && P->g_stream == st) {
             CUDA_TRY(cudaGraphLaunch(P->gexec, st));
@@ -856,6 +931,8 @@ arrow_status arrow_spmm_iterate(arrow_plan P, void *X, void *Y, int64_t k, int32
     CUDA_TRY(cudaGetDevice(&cur));
     if (cur != P->device) return fail(ARROW_E_STATE, "plan used from another device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    arrow_status ws = ensure_ws(P, k);
+    if (ws != ARROW_OK) return ws;
     for (int32_t t = 0; t < iters; ++t) {  // X_{t+1} = act(A X_t), ping-pong between X and Y
         const void *src = (t & 1) ? Y : X;
         void *dst = (t & 1) ? X : Y;

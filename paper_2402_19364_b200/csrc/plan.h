@@ -24,6 +24,12 @@ struct ProfRec {
     cudaEvent_t a, b;
 };
 
+// deterministic mode: K-C of one level (head row r: Y[rows[r]] += slots ptr[r] .. ptr[r+1], in order)
+struct DetLevel {
+    int64_t nh = 0;
+    int32_t *ptr = nullptr, *src = nullptr, *rows = nullptr;
+};
+
 struct DistState;  // dist.cpp
 void dist_free(DistState *d);
 
@@ -61,8 +67,11 @@ struct arrow_plan_s {
     bool use_graphs = true;        // single GPU: replay the call as one CUDA graph (options.flags)
     int32_t transport = 0;         // ARROW_TRANSPORT_* (distributed plans)
     unsigned *counters = nullptr;  // per-level work counters of K-A (zeroed at the start of each call)
-    void *ws = nullptr;            // (unused on one GPU; distributed plans keep theirs in DistState)
+    void *ws = nullptr;            // single GPU, deterministic mode: head-partial slots (det_slots x ws_k)
     int64_t ws_k = 0;
+    bool det = false;              // options.flags & ARROW_FLAG_DETERMINISTIC
+    int64_t det_slots = 0;
+    std::vector<arrow::DetLevel> det_levels;
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
     // arrow_spmm_host_batch: two device slots, two copy streams, per-slot events

@@ -90,6 +90,10 @@ __device__ __forceinline__ void flush_row(int32_t o, const Frag<T, VEC> &acc, T 
                                           const PeerPtrs &outs) {
     if (o == (int32_t)kDiscard) return;  // a padding segment
     if (o < 0) {
+        if (DIST == 0 && C0 != nullptr) {  // deterministic head partial: its own slot, plain store
+            st_plain<T, VEC>(C0 + (int64_t)(o & 0x7fffffff) * k + col0, acc);
+            return;
+        }
         T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
         atomic_add_frag<T, VEC>(dst + col0, acc);
     } else if (DIST == 2 && (o & kLocalRmwBit)) {
@@ -379,7 +383,9 @@ __global__ void __launch_bounds__(256, 4) k_segments(const int32_t *__restrict__
                         if ((u0 + t < cnt) && ((endmask >> ((u0 + t) & 31)) & 1u)) {   // sub-warp uniform
                             const int32_t o = __shfl_sync(mask, my_out, cur, LPE);
                             if (active && o != (int32_t)kDiscard) {
-                                if (o < 0) {
+                                if (o < 0 && DIST == 0 && C0 != nullptr) {  // deterministic head partial
+                                    st_plain<T, VEC>(C0 + (int64_t)(o & 0x7fffffff) * k + col0, acc);
+                                } else if (o < 0) {
                                     T *dst = DIST ? C0 + (int64_t)(o & 0x7fffffff) * k : Y + (int64_t)(o & 0x7fffffff) * k;
                                     atomic_add_frag<T, VEC>(dst + col0, acc);
                                 } else if (DIST == 2 && (o & kLocalRmwBit)) {

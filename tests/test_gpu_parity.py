@@ -413,3 +413,20 @@ def test_capture_inside_torch_cuda_graph():
         graph.replay()
         torch.cuda.synchronize()
         assert np.array_equal(Y.cpu().numpy(), oracle.spmm(g.n, g.row_ptr, g.col, g.val, Xh)), r
+
+
+@pytest.mark.parametrize("k", [128, 32, 8])
+def test_deterministic_flag_bitwise_repeatable(k):
+    """ARROW_FLAG_DETERMINISTIC (S2/S3 without atomics: per-(head row, window) partial slots added in
+    a fixed order by K-C): fp32 results are bitwise identical call to call and within the fp32
+    bounds of O1; fp64 equals O1 bitwise on dyadic data; the k = 8/32 short-row kernels too."""
+    g = datagen.rmat(13, 8, 5)
+    X = datagen.make_x(g.n, k, dtype=np.float32)
+    plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f32", flags=ab.arrow.FLAG_DETERMINISTIC,
+                   window_rows=1024)
+    Y1, Y2 = run(plan, X), run(plan, X)
+    assert np.array_equal(Y1.view(np.uint32), Y2.view(np.uint32))
+    check_fp32(g, Y1, X)
+    p64 = ab.Plan(g.n, g.row_ptr, g.col, g.val, 256, dtype="f64", flags=ab.arrow.FLAG_DETERMINISTIC)
+    X64 = datagen.make_x(g.n, k)
+    assert np.array_equal(run(p64, X64), oracle.spmm(g.n, g.row_ptr, g.col, g.val, X64))
