@@ -317,7 +317,9 @@ def main():
     ap.add_argument("--iterate", type=int, default=10, help="iterations of the fused-ReLU iterate timing (0: skip)")
     ap.add_argument("--no-lib-baseline", action="store_true", help="skip the cuSPARSE (torch.sparse) comparator")
     ap.add_argument("--band", default="block", choices=["block", "strict"],
-                    help="LA-Decompose step 3 band: block-diagonal tiles (R3) or strict |p-q| <= b (NEXT-2, 1 GPU)")
+                    help="LA-Decompose step 3 band: block-diagonal tiles (R3) or strict |p-q| <= b (NEXT-2)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="distributed plans: peer memory over NVLink (p2p) or NCCL broadcast/send/recv/reduce")
     ap.add_argument("--window-rows", type=int, default=0)
     ap.add_argument("--head-chunk", type=int, default=0)
     ap.add_argument("--batch-segments", type=int, default=0)
@@ -358,7 +360,7 @@ def main():
         path = [os.path.join(tempfile.mkdtemp(prefix="arrow_bench_"), "A.dec") if rank == 0 else None]
         dist.broadcast_object_list(path, src=0)
         if rank == 0:
-            dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"])
+            dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"], band=args.band)
             dec.save(path[0])
         dist.barrier()
         if rank != 0:
@@ -370,7 +372,7 @@ def main():
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
                    window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
-                   band=args.band, flags=args.flags)
+                   band=args.band, flags=args.flags, transport=args.transport)
     info = plan.info()
     lo, hi = plan.local_begin, plan.local_end
     if comm is not None or args.order == "permuted":
@@ -540,7 +542,7 @@ def main():
             "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}",
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
-                       "band": args.band if world == 1 else "block",
+                       "band": args.band,
                        "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",
                        "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},
             "hbm_roofline": {"bytes_alg_per_step": b_alg, "achieved_GBs": round(b_alg / (ms_per_step * 1e-3) / 1e9, 1),
@@ -548,7 +550,7 @@ def main():
                              "frac_of_8TBs": round(b_alg / (ms_per_step * 1e-3) / 8e12, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "K-A (k_seg32 for full-warp rows, k_segsmall for short rows, else k_segments)",
+                         "kernel": "K-A (k_ka for full-warp rows, k_segsmall for short rows, else k_segments)",
                          "timing": "K-A share of the step from per-kernel CUDA events (profiled pass) x the "
                                    "graph-replayed step time (timed pass)",
                          "bytes_per_step": ka_bytes, "launches_per_step": ka_launches,

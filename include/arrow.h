@@ -71,7 +71,8 @@ enum { ARROW_ORDER_ORIGINAL = 0,   /* X, Y rows in A's vertex order (default; R1
  * first b rows/columns.  BLOCK: the diagonal b x b tiles (the block-diagonal band Alg. 1 computes,
  * §4.1; reading R3, default).  STRICT: every entry with |p - q| <= b -- the arrow-width
  * definition itself and Fig. 3; fewer levels, body rows read X rows of the
- * neighbouring tiles.  Single-GPU plans only (distributed: ARROW_E_UNSUPPORTED). */
+ * neighbouring tiles.  Distributed plans fetch those rows from the ranks that own
+ * them: level 0 next to the head block D0 (before level 0 runs), levels >= 1 with the forward rows. */
 enum { ARROW_BAND_BLOCK = 0, ARROW_BAND_STRICT = 1 };
 enum { ARROW_RESIDUAL_ERROR = 0,   /* levels cap hit with entries left -> ARROW_E_LEVELS */
        ARROW_RESIDUAL_CSR = 1 };   /* keep the leftover entries as one unstructured CSR level */
@@ -99,7 +100,9 @@ enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each
                                           each tile window are stored into their own slots and added in a
                                           fixed order by a per-level epilogue (K-C, Alg. 1 line 3) instead of
                                           L2 atomics (costs time: DESIGN.md §7) */
-       ARROW_FLAGS_ALL = 3 };
+       ARROW_FLAG_GPU_DECOMPOSE = 4,   /* arrow_plan_create_ex: run LA-Decompose on the current CUDA device
+                                          (arrow_decompose_gpu) instead of the host; same decomposition */
+       ARROW_FLAGS_ALL = 7 };
 /* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
  * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
 enum { ARROW_TRANSPORT_AUTO = 0, ARROW_TRANSPORT_P2P = 1, ARROW_TRANSPORT_NCCL = 2 };
@@ -251,6 +254,16 @@ arrow_status arrow_decompose(const arrow_csr *A, int64_t b, int32_t levels, uint
  * P:253 / Fig. 3); any other value -> ARROW_E_INVALID_ARG.  Saved files record the band. */
 arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
                                 int32_t band, arrow_decomposition *out);
+/* Same as arrow_decompose_ex, computed on the CURRENT CUDA device (§5.1
+ * P:805-814 with §5.3 P:887-896 and §5.4): a bit-identical decomposition -- the same
+ * degree-ordered heads, the same keyed minimum spanning forests (Boruvka under the strict (key, u, v)
+ * order finds the forest Kruskal finds), the same smallest-first tree layout (Euler-tour list ranking
+ * in place of the host's DFS).  A is read from HOST memory and the result lives on the host like
+ * arrow_decompose's; device scratch is allocated and freed inside the call (the default stream,
+ * synchronous).  Errors as arrow_decompose_ex, plus: n >= 2^31 - 1 or nnz >= 2^32 - 1 ->
+ * ARROW_E_INVALID_ARG; no device, allocation or launch failure -> ARROW_E_CUDA. */
+arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                                 int32_t band, arrow_decomposition *out);
 /* n, b, order (number of arrow matrices), residual entries; any pointer may be NULL. */
 arrow_status arrow_decomposition_info(arrow_decomposition d, int64_t *n, int64_t *b, int32_t *levels,
                                       int64_t *residual_nnz);

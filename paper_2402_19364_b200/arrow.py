@@ -22,7 +22,7 @@ ARROW_F32, ARROW_F64 = 0, 1
 ORDER = {"original": 0, "permuted": 1}
 RESIDUAL = {"error": 0, "csr": 1}
 BAND = {"block": 0, "strict": 1}    # ARROW_BAND_* (step 3 of LA-Decompose; strict = P:253 / Fig. 3)
-FLAG_NO_GRAPHS, FLAG_DETERMINISTIC = 1, 2   # ARROW_FLAG_*
+FLAG_NO_GRAPHS, FLAG_DETERMINISTIC, FLAG_GPU_DECOMPOSE = 1, 2, 4   # ARROW_FLAG_*
 TRANSPORT = {"auto": 0, "p2p": 1, "nccl": 2}
 STATUS = ["ARROW_OK", "ARROW_E_INVALID_ARG", "ARROW_E_BAD_CSR", "ARROW_E_NOT_SYMMETRIC", "ARROW_E_LEVELS",
           "ARROW_E_CUDA", "ARROW_E_NCCL", "ARROW_E_NOMEM", "ARROW_E_STATE", "ARROW_E_UNSUPPORTED"]
@@ -38,6 +38,7 @@ SYMBOLS = [
     "arrow_decomposition_load", "arrow_decomposition_destroy", "arrow_plan_create_from", "arrow_comm_unique_id",
     "arrow_comm_create", "arrow_comm_destroy", "arrow_status_string", "arrow_last_error", "arrow_abi_version",
     "arrow_dist_schedule", "arrow_spmm_iterate", "arrow_decompose_ex", "arrow_spmm_host_batch",
+    "arrow_decompose_gpu",
 ]
 
 
@@ -113,6 +114,7 @@ def lib() -> ctypes.CDLL:
             "arrow_plan_kernel_times": [p, p],
             "arrow_decompose": [p, i64, i32, u64, i32, p],
             "arrow_decompose_ex": [p, i64, i32, u64, i32, i32, p],
+            "arrow_decompose_gpu": [p, i64, i32, u64, i32, i32, p],
             "arrow_decomposition_info": [p, p, p, p, p],
             "arrow_decomposition_level_info": [p, i32, p],
             "arrow_decomposition_export_level": [p, i32, p, p, p, p],
@@ -197,18 +199,22 @@ def canonical_sha256(levels) -> str:
 
 
 class Decomposition:
-    """Host LA-Decompose result (arrow_decompose); no GPU needed."""
+    """LA-Decompose result, held on the host.  device="cpu" (arrow_decompose_ex, no GPU needed) or
+    device="cuda" (arrow_decompose_gpu on the current CUDA device; the identical decomposition)."""
 
     def __init__(self, n, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4, keep_residual: bool = False,
-                 band: str = "block", _handle=None):
+                 band: str = "block", device: str = "cpu", _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
             return
         keep: list = []
         A = _csr(n, row_ptr, col, val, keep)
-        _check(lib().arrow_decompose_ex(ctypes.byref(A), b, levels, seed, int(keep_residual), BAND[band],
-                                        ctypes.byref(self._h)), "arrow_decompose_ex")
+        if device not in ("cpu", "cuda"):
+            raise ValueError(f"device must be 'cpu' or 'cuda', not {device!r}")
+        fn = "arrow_decompose_gpu" if device == "cuda" else "arrow_decompose_ex"
+        _check(getattr(lib(), fn)(ctypes.byref(A), b, levels, seed, int(keep_residual), BAND[band],
+                                  ctypes.byref(self._h)), fn)
 
     @classmethod
     def load(cls, path: str) -> "Decomposition":

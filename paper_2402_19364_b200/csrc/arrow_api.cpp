@@ -222,7 +222,7 @@ arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, ar
 }
 
 static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, bool keep_residual,
-                                   int32_t band, std::unique_ptr<arrow_decomposition_s> &D) {
+                                   int32_t band, bool on_gpu, std::unique_ptr<arrow_decomposition_s> &D) {
     const auto t0 = std::chrono::steady_clock::now();
     arrow_status st = validate_args(A, b, levels);
     if (st != ARROW_OK) return st;
@@ -231,6 +231,7 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
     const int64_t n = A->n;
     if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
     if (check_symmetric(n, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_NOT_SYMMETRIC, err);
+    const auto t1 = std::chrono::steady_clock::now();
     try {
         D.reset(new arrow_decomposition_s());
         D->n = n;
@@ -238,7 +239,18 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         D->seed = seed;
         D->band = band;
         HostDecomposition H;
-        if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, H, err)) return fail(ARROW_E_INVALID_ARG, err);
+        if (on_gpu) {
+            if (n >= ((int64_t)1 << 31) - 1 || A->nnz >= ((int64_t)1 << 32) - 1)
+                return fail(ARROW_E_INVALID_ARG, "GPU decomposer: n or nnz beyond 32-bit indices");
+            if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, H, err)) return fail(ARROW_E_CUDA, err);
+        } else if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, H, err)) {
+            return fail(ARROW_E_INVALID_ARG, err);
+        }
+        const auto t2 = std::chrono::steady_clock::now();
+        if (std::getenv("ARROW_DECOMPOSE_TRACE"))
+            fprintf(stderr, "[arrow decompose] %s: checks %.1f ms, LA-Decompose %.1f ms\n", on_gpu ? "gpu" : "host",
+                    std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                    std::chrono::duration<double, std::milli>(t2 - t1).count());
         if (!H.residual.empty() && !keep_residual)
             return fail(ARROW_E_LEVELS, "levels cap " + std::to_string(levels) + " reached with " +
                                             std::to_string(H.residual.size()) + " entries left");
@@ -536,10 +548,6 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     P->local_begin = 0;
     P->local_end = n;
     if (comm) {
-        // the distributed routes assume a level-0 row reads only X rows of its own tile (R3); the
-        // strict band reaches into the neighbouring tiles, i.e. across rank boundaries
-        if (D.band != ARROW_BAND_BLOCK)
-            return fail(ARROW_E_UNSUPPORTED, "distributed plans need ARROW_BAND_BLOCK (strict band: single GPU only)");
         P->comm = comm;
         arrow_status cs = dist_build(P.get(), D, comm, window_rows, head_chunk, bs);
         if (cs != ARROW_OK) return cs;
@@ -560,7 +568,9 @@ arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels,
     if (opt.residual != ARROW_RESIDUAL_ERROR && opt.residual != ARROW_RESIDUAL_CSR)
         return fail(ARROW_E_INVALID_ARG, "bad options.residual");
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, D);
+    if (opt.flags & ~ARROW_FLAGS_ALL) return fail(ARROW_E_INVALID_ARG, "bad options.flags");
+    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band,
+                                     (opt.flags & ARROW_FLAG_GPU_DECOMPOSE) != 0, D);
     if (st != ARROW_OK) return st;
     st = plan_from(*D, &opt, A->dtype, comm, out);
     if (st == ARROW_OK) (*out)->create_seconds += D->seconds;
@@ -586,7 +596,19 @@ arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, u
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, false, D);
+    if (st != ARROW_OK) return st;
+    *out = D.release();
+    return ARROW_OK;
+}
+
+arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                                 int32_t band, arrow_decomposition *out) {
+    g_err.clear();
+    if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    std::unique_ptr<arrow_decomposition_s> D;
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, true, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
     return ARROW_OK;

@@ -33,6 +33,12 @@ struct HostDecomposition {
 int la_decompose(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
                  uint64_t seed, int band, HostDecomposition &out, std::string &err);
 
+// LA-Decompose on the current CUDA device (gdecompose.cu): the same output as
+// la_decompose, bit for bit (same rules and keys; Boruvka + Euler-tour list ranking in place of the
+// sequential Kruskal / BFS / DFS).  n < 2^31 - 1, nnz < 2^32 - 1.  0 on success, else sets `err`.
+int la_decompose_gpu(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
+                     uint64_t seed, int band, HostDecomposition &out, std::string &err);
+
 // Validation helpers (decompose.cpp): 0 ok, 1 bad CSR, 2 not symmetric.
 int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, std::string &err);
 int check_symmetric(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &err);

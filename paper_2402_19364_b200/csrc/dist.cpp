@@ -79,6 +79,12 @@ struct DistHost {
     std::vector<int64_t> send_row, halo_dst_row;        // per peer: my send chunk, its place in the peer's halo
     int64_t send_rows = 0;
     std::vector<std::pair<int32_t, int32_t>> post;      // (local Y row, encoded source row)
+    // strict band, level 0: H0 = the outside rows my level-0 body rows read (ascending q, grouped by
+    // home), at workspace row o_h0 of every rank (P2P: [D0 | C0 x 2 | H0 | halo ...], NCCL:
+    // [D0 | C0 | H0 | halo ...]), h0_max rows reserved on every rank
+    int64_t h0_max = 0, o_h0 = 0;
+    std::vector<int32_t> h0_slot_q;
+    std::vector<int32_t> send0_idx;                     // NCCL: my local X rows for the peers' H0 (peer order)
 };
 
 struct DistState {
@@ -95,6 +101,9 @@ struct DistState {
     // k-dependent workspace (rows).  NCCL: [D0 | C0 | halo | send | staging | recv];
     // P2P: [D0 | C0 (call parity 0) | C0 (parity 1) | halo | stage], shared with the peers
     int64_t o_d0 = 0, o_c0 = 0, o_halo = 0, o_send = 0, o_out = 0, o_in = 0, ws_rows = 0;
+    // strict band: level-0 outside rows (H0) and, NCCL, my packed rows for the peers' H0 (S0)
+    int64_t o_h0 = 0, o_s0 = 0;
+    std::vector<int64_t> send0_peer, recv0_peer;
     // NCCL: pre-exchange row mover (src X, dst workspace)
     int32_t *pre_src = nullptr, *pre_dst = nullptr;
     int64_t n_pre = 0;
@@ -255,7 +264,33 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         return rk[i][std::upper_bound(tbs[i].begin() + 1, tbs[i].end() - 1, q / b) - (tbs[i].begin() + 1)];
     };
     H.L.resize(nl);
-    // RC / OC[i][t * G + h]: rows (all / with entries) of rank t's level-i tiles whose home is h
+    // strict band: a body row p also reads the columns q with |p - q| <= b that lie outside its
+    // rank's tile range [qa, qb) -- only rows within b of the range ends can.  outside(i, t): those
+    // columns of rank t's level-i body rows, heads excluded (D0 serves them), ascending, unique.
+    const bool strict = D.band == ARROW_BAND_STRICT;
+    auto outside = [&](int i, int t) {
+        std::vector<int32_t> o;
+        if (!strict) return o;
+        const HostLevel &L = D.levels[i];
+        int64_t qa, qb;
+        range(i, t, qa, qb);
+        const int64_t ha = std::max(L.head, qa);
+        if (ha >= qb) return o;
+        auto scan = [&](int64_t p0, int64_t p1) {
+            for (int64_t p = p0; p < p1; ++p)
+                for (int64_t e = L.row_ptr[p]; e < L.row_ptr[p + 1]; ++e) {
+                    const int32_t q = L.col[e];
+                    if (q >= L.head && (q < qa || q >= qb)) o.push_back(q);
+                }
+        };
+        const int64_t m1 = std::min(qb, qa + b);
+        scan(ha, m1);
+        scan(std::max(m1, qb - b), qb);
+        std::sort(o.begin(), o.end());
+        o.erase(std::unique(o.begin(), o.end()), o.end());
+        return o;
+    };
+    // RC / OC[i][t * G + h]: halo rows (all) / body rows with entries of rank t's level-i tiles whose home is h
     std::vector<std::vector<int64_t>> RC(nl, std::vector<int64_t>((size_t)G * G, 0)), OC = RC;
     // sl[i][g]: local X rows I own that g's level-i tiles need (g's halo slot order);
     // il[i][g]: local Y rows of g's level-i body rows whose home is me (g's staging order)
@@ -283,27 +318,36 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                 load[ro[j]] += cc[co[j]];
             }
         }
-        int64_t qa, qb;
-        range(i, me, qa, qb);
-        const int64_t h = L.head, ha = std::max(h, qa);
+        const int64_t h = L.head;
         DL.recv_cnt.assign(G, 0);
         DL.out_cnt.assign(G, 0);
-        for (int64_t q = ha; q < qb; ++q) {
-            const int home = owner(pos0[L.perm[q]]);
-            DL.recv_cnt[home]++;
-            if (L.row_ptr[q + 1] > L.row_ptr[q]) DL.out_cnt[home]++;
-        }
         sl[i].assign(G, {});
         il[i].assign(G, {});
-        for (int64_t q = h; q < L.n_i; ++q) {
-            const int64_t P0 = pos0[L.perm[q]];
-            const int home = owner(P0), t = tile_owner(i, q);
-            const bool has = L.row_ptr[q + 1] > L.row_ptr[q];
-            RC[i][(size_t)t * G + home]++;
-            if (has) OC[i][(size_t)t * G + home]++;
-            if (home != me) continue;
-            sl[i][t].push_back((int32_t)(P0 - lo));
-            if (has) il[i][t].push_back((int32_t)(P0 - lo));
+        // halo of rank t = its body rows [max(h, qa), qb) merged with outside(i, t), ascending
+        for (int t = 0; t < G; ++t) {
+            int64_t qa, qb;
+            range(i, t, qa, qb);
+            const int64_t ha = std::max(h, qa);
+            const std::vector<int32_t> ext = outside(i, t);
+            size_t x = 0;
+            auto visit = [&](int64_t q) {
+                const int64_t P0 = pos0[L.perm[q]];
+                const int home = owner(P0);
+                RC[i][(size_t)t * G + home]++;
+                if (t == me) DL.recv_cnt[home]++;
+                if (home == me) sl[i][t].push_back((int32_t)(P0 - lo));
+            };
+            for (int64_t q = ha; q < qb; ++q) {
+                for (; x < ext.size() && ext[x] < q; ++x) visit(ext[x]);
+                visit(q);
+                const int64_t P0 = pos0[L.perm[q]];
+                const int home = owner(P0);
+                if (L.row_ptr[q + 1] == L.row_ptr[q]) continue;
+                OC[i][(size_t)t * G + home]++;
+                if (t == me) DL.out_cnt[home]++;
+                if (home == me) il[i][t].push_back((int32_t)(P0 - lo));
+            }
+            for (; x < ext.size(); ++x) visit(ext[x]);
         }
         DL.send_cnt.assign(G, 0);
         DL.in_cnt.assign(G, 0);
@@ -311,6 +355,24 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             DL.send_cnt[g] = (int64_t)sl[i][g].size();
             DL.in_cnt[g] = (int64_t)il[i][g].size();
         }
+    }
+    // strict band, level 0: rank t's outside rows (H0 of t, ascending = grouped by home) are sent by
+    // their homes before level 0 runs, next to D0
+    std::vector<std::vector<int32_t>> ext0(G);
+    if (nl > 0 && strict) {
+        DistHostLevel &DL = H.L[0];
+        DL.send_cnt.assign(G, 0);
+        DL.recv_cnt.assign(G, 0);
+        for (int t = 0; t < G; ++t) {
+            ext0[t] = outside(0, t);
+            H.h0_max = std::max<int64_t>(H.h0_max, (int64_t)ext0[t].size());
+            for (int32_t q : ext0[t]) {
+                const int home = owner(q);
+                if (t == me) DL.recv_cnt[home]++;
+                if (home == me) DL.send_cnt[t]++;
+            }
+        }
+        H.h0_slot_q = ext0[me];
     }
     // ---- peer-major buffer layout: HB / OB = halo / staging offset of (home g, level i)
     std::vector<std::vector<int64_t>> HB(G, std::vector<int64_t>(nl, 0)), OB(G, std::vector<int64_t>(nl, 0));
@@ -387,7 +449,7 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                     SBt[t][g][i] = H.stage_all[t];
                     if (g != t) H.stage_all[t] += OC[i][(size_t)g * G + t];  // own rows: RMW into Y
                 }
-        const int64_t o_halo = 3 * H.d0_rows;
+        const int64_t o_halo = 3 * H.d0_rows + H.h0_max;
         for (int t = 0; t < G; ++t) {
             if (o_halo + H.halo_all[t] + H.stage_all[t] > (int64_t)kPeerRowMask)
                 return set_error(ARROW_E_UNSUPPORTED, "P2P workspace exceeds 2^27 rows");
@@ -417,6 +479,24 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                     H.post.emplace_back(il[i][s][m], (int32_t)(((uint32_t)me << kPeerShift) | (uint32_t)(o_stage + SBt[me][s][i] + (int64_t)m)));
     }
 
+    // strict band, level 0: H0 offset; my rows for every peer's H0 (P2P: pushed with D0; NCCL: packed
+    // peer-major and sent before level 0)
+    H.o_h0 = (p2p ? 3 : 2) * H.d0_rows;
+    if (strict)
+        for (int t = 0; t < G; ++t) {
+            if (t == me) continue;
+            for (size_t m = 0; m < ext0[t].size(); ++m) {
+                const int32_t q = ext0[t][m];
+                if (owner(q) != me) continue;
+                if (p2p) {
+                    H.d0push_src.push_back((int32_t)(q - lo));
+                    H.d0push_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)(H.o_h0 + (int64_t)m)));
+                } else {
+                    H.send0_idx.push_back((int32_t)(q - lo));
+                }
+            }
+        }
+
     // ---- pass 2: heads, zero rows and descriptor layout of my tiles, per level
     for (int i = 0; i < nl; ++i) {
         const HostLevel &L = D.levels[i];
@@ -425,25 +505,38 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         int64_t qa, qb;
         range(i, me, qa, qb);
         const int64_t ha = std::max(h, qa);
-        std::vector<int32_t> halo_slot, out_slot;
+        std::vector<int32_t> halo_slot, out_slot, ext, ext_slot;
         if (i > 0) {
             std::vector<int64_t> hcur(G), ocur(G);
             for (int g = 0; g < G; ++g) {
                 hcur[g] = HB[g][i];
                 // P2P: staging rows are stored straight into the home rank's buffer
-                ocur[g] = p2p ? 3 * H.d0_rows + H.halo_all[g] + SBt[g][me][i] : OB[g][i];
+                ocur[g] = p2p ? 3 * H.d0_rows + H.h0_max + H.halo_all[g] + SBt[g][me][i] : OB[g][i];
             }
             halo_slot.resize(std::max<int64_t>(0, qb - ha));
             out_slot.assign(std::max<int64_t>(0, qb - ha), -1);
+            // halo slots in the order of pass 1 (body rows merged with the outside rows, ascending)
+            ext = outside(i, me);
+            ext_slot.resize(ext.size());
+            size_t x = 0;
+            auto slot_of = [&](int64_t q) { return (int32_t)(hcur[owner(pos0[L.perm[q]])]++); };
             for (int64_t q = ha; q < qb; ++q) {
-                const int home = owner(pos0[L.perm[q]]);
-                halo_slot[q - ha] = (int32_t)(hcur[home]++);
+                for (; x < ext.size() && ext[x] < q; ++x) ext_slot[x] = slot_of(ext[x]);
+                halo_slot[q - ha] = slot_of(q);
+            }
+            for (; x < ext.size(); ++x) ext_slot[x] = slot_of(ext[x]);
+            for (int64_t q = ha; q < qb; ++q) {
                 if (L.row_ptr[q + 1] == L.row_ptr[q]) continue;
+                const int home = owner(pos0[L.perm[q]]);
                 if (p2p && home == me)  // P2P: my own rows are read-modify-written into Y directly
                     out_slot[q - ha] = (int32_t)(kLocalRmwBit | (uint32_t)(pos0[L.perm[q]] - lo));
                 else
                     out_slot[q - ha] = (int32_t)((p2p ? ((uint32_t)home << kPeerShift) : 0u) | (uint32_t)(ocur[home]++));
             }
+        } else {
+            ext = H.h0_slot_q;
+            ext_slot.resize(ext.size());
+            for (size_t m = 0; m < ext.size(); ++m) ext_slot[m] = (int32_t)(kFlag | (uint32_t)(H.o_h0 + (int64_t)m));
         }
         for (int64_t j = 0; j < h; ++j) {
             const int64_t P0 = pos0[L.perm[j]];
@@ -466,6 +559,7 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         }
         auto colmap = [&](int32_t q) -> int32_t {
             if (q < h) return (int32_t)(kFlag | (uint32_t)H.d0_index[i][q]);
+            if (q < qa || q >= qb) return ext_slot[std::lower_bound(ext.begin(), ext.end(), q) - ext.begin()];
             return (i == 0) ? (int32_t)(q - lo) : halo_slot[q - ha];
         };
         auto push_val = [&](double v) {
@@ -655,7 +749,8 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     if (S->p2p) {
         S->o_d0 = 0;
         S->o_c0 = S->d0_rows;
-        S->o_halo = 3 * S->d0_rows;
+        S->o_h0 = H.o_h0;
+        S->o_halo = 3 * S->d0_rows + H.h0_max;
         S->o_out = S->o_halo + H.halo_all[me];
         S->ws_rows = S->o_out + H.stage_all[me] + H.send_rows;
         S->send_row = H.send_row;
@@ -672,13 +767,20 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         }
         build_csr(H.post, pp, ps, pd);
     } else {
-        // workspace rows: [D0 | C0 | halo | send | staging | recv]
+        // workspace rows: [D0 | C0 | H0 | halo | send | S0 | staging | recv]
         const int64_t n_send = (int64_t)H.send_idx_peers.size(), n_in = (int64_t)H.in_rows_peers.size();
+        const int64_t n_s0 = (int64_t)H.send0_idx.size();
         S->o_d0 = 0;
         S->o_c0 = S->d0_rows;
-        S->o_halo = 2 * S->d0_rows;
+        S->o_h0 = H.o_h0;
+        S->o_halo = 2 * S->d0_rows + H.h0_max;
         S->o_send = S->o_halo + H.halo_rows;
-        S->o_out = S->o_send + n_send;
+        S->o_s0 = S->o_send + n_send;
+        S->o_out = S->o_s0 + n_s0;
+        if (nl > 0 && !H.L[0].send_cnt.empty()) {
+            S->send0_peer = H.L[0].send_cnt;
+            S->recv0_peer = H.L[0].recv_cnt;
+        }
         S->o_in = S->o_out + H.out_rows;
         S->ws_rows = S->o_in + n_in;
         if (S->ws_rows >= ((int64_t)1 << 31))
@@ -691,6 +793,7 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
             }
         for (int64_t r = 0; r < S->d0_rows; ++r) { pre_src.push_back(-1); pre_dst.push_back((int32_t)(S->o_c0 + r)); }
         for (int64_t m = 0; m < n_send; ++m) { pre_src.push_back(H.send_idx_peers[m]); pre_dst.push_back((int32_t)(S->o_send + m)); }
+        for (int64_t m = 0; m < n_s0; ++m) { pre_src.push_back(H.send0_idx[m]); pre_dst.push_back((int32_t)(S->o_s0 + m)); }
         for (size_t m = 0; m < H.send_idx_self.size(); ++m) {
             pre_src.push_back(H.send_idx_self[m]);
             pre_dst.push_back((int32_t)(S->o_halo + H.halo_self_off + (int64_t)m));
@@ -714,7 +817,7 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
         SegLevel sg;
         std::string err;
         // level 0 reads the local X rows (and D0), levels >= 1 the halo inside the workspace
-        const int64_t xr = (i == 0) ? std::max<int64_t>(S->hi - S->lo, S->d0_rows) : S->ws_rows;
+        const int64_t xr = (i == 0) ? std::max<int64_t>(S->hi - S->lo, S->o_halo) : S->ws_rows;
         const int e = upload_seg_level(H.L[i].segs, (int)P->esize(), bs, 0, xr, S->allocs, sg, err);
         if (e) return set_error(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
         H.L[i].segs = HostSegs();
@@ -945,6 +1048,19 @@ arrow_status dist_spmm(arrow_plan P, const void *X, void *Y, int64_t k, cudaStre
             DNCCL(ncclBroadcast(row(S->o_d0 + S->blk0[r]), row(S->o_d0 + S->blk0[r]), (S->blk0[r + 1] - S->blk0[r]) * k,
                                 nt, r, S->comm, S->cs));
     DNCCL(ncclGroupEnd());
+    if (!S->send0_peer.empty()) {  // strict band: level 0's outside rows from their homes (H0)
+        DNCCL(ncclGroupStart());
+        int64_t s0 = 0, r0 = 0;
+        for (int g = 0; g < G; ++g) {
+            if (g != me && S->send0_peer[g])
+                DNCCL(ncclSend(row(S->o_s0 + s0), S->send0_peer[g] * k, nt, g, S->comm, S->cs));
+            if (g != me && S->recv0_peer[g])
+                DNCCL(ncclRecv(row(S->o_h0 + r0), S->recv0_peer[g] * k, nt, g, S->comm, S->cs));
+            s0 += S->send0_peer[g];
+            r0 += S->recv0_peer[g];
+        }
+        DNCCL(ncclGroupEnd());
+    }
     DCUDA(cudaEventRecord(S->ev[1], S->cs));
     DNCCL(ncclGroupStart());
     int64_t so = 0, ro = 0;
@@ -1038,8 +1154,6 @@ extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nrank
     if (!d || !lohi) return arrow::set_error(ARROW_E_INVALID_ARG, "NULL argument");
     if (nranks < 1 || nranks > arrow::kMaxPeers || rank < 0 || rank >= nranks)
         return arrow::set_error(ARROW_E_INVALID_ARG, "nranks must be in [1, 8] and rank in [0, nranks)");
-    if (d->band != ARROW_BAND_BLOCK)
-        return arrow::set_error(ARROW_E_UNSUPPORTED, "distributed schedules need ARROW_BAND_BLOCK");
     arrow::DistHost H;
     arrow_status st = arrow::dist_schedule(*d, nranks, rank, window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
                                            head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, 0, H);

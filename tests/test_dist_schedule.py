@@ -17,12 +17,12 @@ import datagen
 import paper_2402_19364_b200 as ab
 
 
-def _dec(spec="RMAT(12,8,1)", b=64):
+def _dec(spec="RMAT(12,8,1)", b=64, band="block"):
     g = datagen.make_graph(spec)
-    return g, ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b)
+    return g, ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band)
 
 
-def check_schedules(g, D, scheds):
+def check_schedules(g, D, scheds, strict=False):
     G = len(scheds)
     assert scheds[0]["lo"] == 0 and scheds[-1]["hi"] == g.n
     for a in range(G - 1):
@@ -39,19 +39,48 @@ def check_schedules(g, D, scheds):
         assert sum(s["levels"][i]["entries"] for s in scheds) == li["nnz"]
         assert sum(s["levels"][i]["heads"] for s in scheds) == li["head"]
         if i > 0:
-            # every level-i vertex outside the head is fetched exactly once, every non-empty body row goes home once
-            assert sum(int(s["levels"][i]["recv"].sum()) for s in scheds) == li["n_i"] - li["head"]
+            # every level-i vertex outside the head is fetched exactly once (strict band: at least once,
+            # plus the rows within b of a rank's tile range that its body rows read), every non-empty
+            # body row goes home once
+            fetched = sum(int(s["levels"][i]["recv"].sum()) for s in scheds)
+            if strict:
+                assert fetched >= li["n_i"] - li["head"]
+            else:
+                assert fetched == li["n_i"] - li["head"]
             nonempty = int((np.diff(rp)[li["head"]:] > 0).sum())
             assert sum(int(s["levels"][i]["out"].sum()) for s in scheds) == nonempty
-    perm0, rp0, _, _ = D.export_level(0)
+    perm0, rp0, col0, _ = D.export_level(0)
     h0 = D.level_info(0)["head"]
+    n0 = D.level_info(0)["n_i"]
     assert sum(s["levels"][0]["zero_rows"] for s in scheds) == int((np.diff(rp0)[h0:] == 0).sum())
+    # level 0: a rank receives exactly the distinct non-head columns outside its pi_0 range that its
+    # body rows read (none for the block band: a tile never leaves its rank), each from that column's home
+    for a, s in enumerate(scheds):
+        lo, hi = s["lo"], s["hi"]
+        need = set()
+        for p in range(max(h0, lo), min(hi, n0)):
+            for q in col0[rp0[p]:rp0[p + 1]]:
+                if q >= h0 and not lo <= q < hi:
+                    need.add(int(q))
+        if not strict:
+            assert not need
+        homes = np.zeros(len(scheds), np.int64)
+        for q in need:
+            homes[[t for t, z in enumerate(scheds) if z["lo"] <= q < z["hi"]][0]] += 1
+        assert np.array_equal(s["levels"][0]["recv"], homes), (a, s["levels"][0]["recv"], homes)
 
 
 @pytest.mark.parametrize("G", [1, 2, 3, 5, 8])
 def test_schedule_consistency_single_process(G):
     g, D = _dec()
     check_schedules(g, D, [D.dist_schedule(G, r) for r in range(G)])
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+@pytest.mark.parametrize("spec,b", [("RMAT(12,8,1)", 64), ("GRID(48,2)", 32), ("PATH(2000,3)", 16)])
+def test_schedule_strict_band(G, spec, b):
+    g, D = _dec(spec, b, band="strict")
+    check_schedules(g, D, [D.dist_schedule(G, r) for r in range(G)], strict=True)
 
 
 def test_schedule_more_ranks_than_tiles():

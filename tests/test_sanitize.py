@@ -25,7 +25,7 @@ def _build():
     exe = os.path.join(BUILD, "sanitize_main")
     srcs = [os.path.join(CSRC, f) for f in ("decompose.cpp", "arrow_api.cpp", "dist.cpp", "comm.cpp", "layout.cpp")]
     srcs.append(os.path.join(ROOT, "tests", "sanitize", "sanitize_main.cpp"))
-    objs = [os.path.join(ROOT, "build", "arrow_b200", f + ".o") for f in ("seg_kernel.cu", "kernels.cu")]
+    objs = [os.path.join(ROOT, "build", "arrow_b200", f + ".o") for f in ("seg_kernel.cu", "kernels.cu", "gdecompose.cu")]
     inc_nccl, lib_nccl = b.nccl_paths()
     cuda = b.CUDA
     cmd = ["g++", "-std=c++17", "-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
