@@ -324,6 +324,9 @@ def main():
     ap.add_argument("--head-chunk", type=int, default=0)
     ap.add_argument("--batch-segments", type=int, default=0)
     ap.add_argument("--flags", type=int, default=0, help="arrow_options.flags (ARROW_FLAG_*)")
+    ap.add_argument("--home-aware", action="store_true",
+                    help="N > 1: decompose with home-set-aware levels >= 1 for the N ranks (R25)")
+    ap.add_argument("--gpu-decompose", action="store_true", help="N > 1: rank 0 decomposes on its GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -353,6 +356,7 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         comm = ab.Comm(world, rank, uid[0])
     dec = None
+    decompose_s = [None]
     if world > 1:
         # one host decomposition for the node: rank 0 computes and checkpoints it, the others load it
         # (arrow_decomposition_save/load), instead of G processes decomposing the same A at once
@@ -360,7 +364,11 @@ def main():
         path = [os.path.join(tempfile.mkdtemp(prefix="arrow_bench_"), "A.dec") if rank == 0 else None]
         dist.broadcast_object_list(path, src=0)
         if rank == 0:
-            dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"], band=args.band)
+            t0 = time.perf_counter()
+            dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"], band=args.band,
+                                   homes=world if args.home_aware else 1,
+                                   device="cuda" if args.gpu_decompose else "cpu")
+            decompose_s[0] = time.perf_counter() - t0
             dec.save(path[0])
         dist.barrier()
         if rank != 0:
@@ -543,6 +551,8 @@ def main():
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
                        "band": args.band,
+                       "arrangement": ("home-aware (R25) for %d ranks" % world) if (args.home_aware and world > 1)
+                                      else "random spanning forest, smallest-first (R6-R12)",
                        "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",
                        "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},
             "hbm_roofline": {"bytes_alg_per_step": b_alg, "achieved_GBs": round(b_alg / (ms_per_step * 1e-3) / 1e9, 1),
@@ -569,6 +579,8 @@ def main():
             "nvlink": nvl,
             "create_seconds": round(info["create_seconds"], 2),
         }
+        if decompose_s[0] is not None:
+            line["decompose_seconds"] = round(decompose_s[0], 3)
         print(json.dumps(line), flush=True)
     plan.close()
     if comm is not None:

@@ -102,7 +102,9 @@ enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each
                                           L2 atomics (costs time: DESIGN.md §7) */
        ARROW_FLAG_GPU_DECOMPOSE = 4,   /* arrow_plan_create_ex: run LA-Decompose on the current CUDA device
                                           (arrow_decompose_gpu) instead of the host; same decomposition */
-       ARROW_FLAGS_ALL = 7 };
+       ARROW_FLAG_HOME_AWARE = 8,      /* arrow_plan_create_ex with a comm: home-set-aware arrangement for the
+                                          comm's ranks (arrow_decompose_homes, homes = nranks) */
+       ARROW_FLAGS_ALL = 15 };
 /* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
  * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
 enum { ARROW_TRANSPORT_AUTO = 0, ARROW_TRANSPORT_P2P = 1, ARROW_TRANSPORT_NCCL = 2 };
@@ -264,6 +266,22 @@ arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, u
  * ARROW_E_INVALID_ARG; no device, allocation or launch failure -> ARROW_E_CUDA. */
 arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
                                  int32_t band, arrow_decomposition *out);
+/* The general form: homes = G in [1, 8] lays levels >= 1 out for G ranks (reading
+ * R25 of DESIGN.md §3; an extension, not in the paper): after level 0 every vertex gets the home range
+ * of its pi_0 position -- G contiguous ranges of whole level-0 tiles balanced by level-0 work plus
+ * every vertex's entries left for levels >= 1 -- and the trees of every level >= 1 are laid out by
+ * (home of the root, size desc, min id asc) instead of (size desc, min id asc), so a distributed
+ * plan for G ranks computes each level's home-g trees on rank g and moves few rows over NVLink.
+ * homes = 1 is arrow_decompose_ex.  device: 0 = host, 1 = the current CUDA device (as
+ * arrow_decompose_gpu; the same decomposition).  Errors as arrow_decompose_ex / _gpu; homes outside
+ * [1, 8] or device not 0/1 -> ARROW_E_INVALID_ARG.  Saved files (format 3) record the homes. */
+arrow_status arrow_decompose_homes(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                                   int32_t band, int32_t homes, int32_t device, arrow_decomposition *out);
+/* homes of a decomposition (*homes, may be NULL) and, when homes > 1 and ranges != NULL, level = -1:
+ * the pi_0 home ranges ranges[0..homes]; level >= 1: the first position of each home's trees
+ * (ranges[g] .. ranges[g+1] hold home g's trees, ranges[0] = head, ranges[homes] = n_i); level 0 ->
+ * ARROW_E_INVALID_ARG. */
+arrow_status arrow_decomposition_homes(arrow_decomposition d, int32_t level, int32_t *homes, int64_t *ranges);
 /* n, b, order (number of arrow matrices), residual entries; any pointer may be NULL. */
 arrow_status arrow_decomposition_info(arrow_decomposition d, int64_t *n, int64_t *b, int32_t *levels,
                                       int64_t *residual_nnz);

@@ -34,7 +34,8 @@ import numpy as np
 
 from .decompose import (Decomposition, Level, la_decompose, decomposition_sha256,  # noqa: F401
                         prune_head, captured, extract, forest_layout, minimum_spanning_forest,
-                        spmm_through_decomposition, reconstruct_entries, splitmix64_int)
+                        spmm_through_decomposition, reconstruct_entries, splitmix64_int,
+                        level0_tile_costs, home_ranges, homes_of)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIBPATH = os.path.join(_HERE, "_lib", "liboracle.so")

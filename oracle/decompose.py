@@ -26,6 +26,15 @@ listed in DESIGN.md §3:
                  (band="strict": p < b or q < b or |p - q| <= b, P:253 / Fig. 3; NEXT-2)
       otherwise (u,v,a) -> E_{i+1}                                                  -- step 4
     level 0 is presented with n rows: positions n_0..n-1 hold A-isolated vertices in id order.
+
+Home-set-aware arrangement (homes = G > 1, reading R25 in DESIGN.md §3 --
+an extension for G GPUs, not in the paper): after level 0, every vertex gets a home
+g = home_of(pi_0 position) from the G contiguous pi_0 ranges of home_ranges() (level-0 tiles
+split by level-0 work plus the remainder degrees); for levels i >= 1 the spanning forest is
+taken over the edges of G'_i whose endpoints share a home (so every tree lies in one home) and
+the trees are sorted by (home of the root, size desc, min id asc) instead of R11's (size desc,
+min id asc); home_start[g] records where home g's trees begin.  Edges between homes wait for a
+later level (or a head).  homes = 1 is the decomposition above.
 """
 from __future__ import annotations
 
@@ -63,6 +72,7 @@ class Level:
     col: np.ndarray          # int64[nnz_i] positions, sorted within each row
     val: np.ndarray          # float64[nnz_i]
     head: int                # h_i = min(b, n_i)
+    home_start: np.ndarray | None = None   # int64[G+1] (homes > 1, levels >= 1): trees of home g at [hs[g], hs[g+1])
 
     @property
     def rows(self) -> int:
@@ -80,6 +90,8 @@ class Decomposition:
     levels: list = field(default_factory=list)
     residual: tuple | None = None    # (u, v, a) original-id triples left when the level cap is hit
     band: str = "block"              # step 3's band (captured())
+    homes: int = 1                   # G of the home-set-aware arrangement (R25); 1 = R11
+    home_los: np.ndarray | None = None   # int64[G+1] pi_0 home ranges (homes > 1)
 
     @property
     def order(self) -> int:
@@ -113,12 +125,15 @@ def minimum_spanning_forest(n: int, eu: np.ndarray, ev: np.ndarray, key: np.ndar
 
 
 # ---------------------------------------------------------------------------- tree layout
-def forest_layout(vertices: np.ndarray, fu: np.ndarray, fv: np.ndarray, n: int) -> np.ndarray:
+def forest_layout(vertices: np.ndarray, fu: np.ndarray, fv: np.ndarray, n: int, home=None, G: int = 1):
     """Linear arrangement of a spanning forest on `vertices`:
     trees in decreasing size (ties: smaller min id), each tree in smallest-first order
-    rooted at its min id, children by (subtree size asc, id asc); iterative DFS (R12)."""
+    rooted at its min id, children by (subtree size asc, id asc); iterative DFS (R12).
+    With `home` (int array over vertex ids, R25): trees sorted by (home[root], size desc, root)
+    instead; then also returns home_start (offsets of each home's trees, length G+1)."""
     if len(vertices) == 0:
-        return np.zeros(0, dtype=np.int64)
+        empty = np.zeros(0, dtype=np.int64)
+        return empty if home is None else (empty, np.zeros(G + 1, dtype=np.int64))
     adj = [[] for _ in range(n)]
     for a, b in zip(fu.tolist(), fv.tolist()):
         adj[a].append(b)
@@ -156,8 +171,63 @@ def forest_layout(vertices: np.ndarray, fu: np.ndarray, fv: np.ndarray, n: int) 
             ch = sorted(children[x], key=lambda c: (size[c], c))
             stack.extend(reversed(ch))
         trees.append((len(order), r, pre))
-    trees.sort(key=lambda t: (-t[0], t[1]))
-    return np.array([x for t in trees for x in t[2]], dtype=np.int64)
+    if home is None:
+        trees.sort(key=lambda t: (-t[0], t[1]))
+        return np.array([x for t in trees for x in t[2]], dtype=np.int64)
+    trees.sort(key=lambda t: (int(home[t[1]]), -t[0], t[1]))
+    start = np.zeros(G + 1, dtype=np.int64)
+    for size, root, _ in trees:
+        start[int(home[root]) + 1:] += size
+    return np.array([x for t in trees for x in t[2]], dtype=np.int64), start
+
+
+# ---------------------------------------------------------------------------- homes (R25)
+def level0_tile_costs(lv: Level, b: int, rem_deg: np.ndarray) -> np.ndarray:
+    """Work of each level-0 tile t (positions [t b, (t+1) b) of [0, n_0)), R25: every body row
+    p >= h costs its entries + 4; every head-row entry costs 1 in the tile of its column; every
+    vertex at a position of the tile adds its remainder degree rem_deg (its entries left for
+    levels >= 1, which its home computes under the home-aware arrangement)."""
+    T = -(-lv.n_i // b)
+    cost = np.zeros(T, dtype=np.int64)
+    for p in range(lv.head, lv.n_i):
+        cost[p // b] += int(lv.row_ptr[p + 1] - lv.row_ptr[p]) + 4
+    for j in range(lv.head):
+        for q in lv.col[lv.row_ptr[j]:lv.row_ptr[j + 1]]:
+            cost[int(q) // b] += 1
+    for p in range(lv.n_i):
+        cost[p // b] += int(rem_deg[lv.perm[p]])
+    return cost
+
+
+def home_ranges(lv0: Level, n: int, b: int, G: int, rem_deg: np.ndarray) -> np.ndarray:
+    """R25: G contiguous pi_0 ranges los[0..G] made of whole level-0 tiles.  The tile costs of
+    level0_tile_costs() plus one last pseudo-tile for the A-isolated positions [n_0, n) (cost 1
+    each); prefix sums pre[0..T']; boundary g (0 < g < G) is the first t with pre[t] >= g/G of
+    the total, moved one tile back if pre[t-1] is strictly nearer to g/G of the total, and never
+    before boundary g-1.  los[g] = min(n_0, t_g b); los[0] = 0, los[G] = n."""
+    cost = list(level0_tile_costs(lv0, b, rem_deg)) + [n - lv0.n_i]
+    Tp = len(cost)
+    pre = [0]
+    for c in cost:
+        pre.append(pre[-1] + c)
+    tot = pre[-1]
+    tb = [0] * (G + 1)
+    tb[G] = Tp
+    for g in range(1, G):
+        t = next(t for t in range(Tp + 1) if pre[t] * G >= tot * g)
+        if t > 0 and tot * g - pre[t - 1] * G < pre[t] * G - tot * g:
+            t -= 1
+        tb[g] = min(max(t, tb[g - 1]), Tp)
+    los = np.array([min(lv0.n_i, t * b) for t in tb], dtype=np.int64)
+    los[0], los[G] = 0, n
+    return los
+
+
+def homes_of(lv0: Level, los: np.ndarray, n: int) -> np.ndarray:
+    """home[v] = the range g with los[g] <= pi_0(v) < los[g+1] (the last such g if ranges are empty)."""
+    pos0 = np.empty(n, dtype=np.int64)
+    pos0[lv0.perm] = np.arange(n, dtype=np.int64)
+    return np.searchsorted(los[1:-1], pos0, side="right").astype(np.int64)
 
 
 # ---------------------------------------------------------------------------- steps 1 and 3
@@ -202,9 +272,11 @@ def extract(eu, ev, ea, order, b: int, band: str = "block"):
 
 # ---------------------------------------------------------------------------- LA-Decompose
 def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4,
-                 band: str = "block") -> Decomposition:
+                 band: str = "block", homes: int = 1) -> Decomposition:
     if band not in BANDS:
         raise ValueError(f"unknown band {band!r}")
+    if not 1 <= homes <= 8:
+        raise ValueError("homes must be in [1, 8]")
     if b < 2:
         raise ValueError("arrow width b must be >= 2 (P:807)")
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
@@ -213,7 +285,8 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
     ea = np.asarray(val, dtype=np.float64)
     deg_a = np.diff(row_ptr)
     isolated_a = np.flatnonzero(deg_a == 0)
-    dec = Decomposition(n=n, b=b, band=band)
+    dec = Decomposition(n=n, b=b, band=band, homes=homes)
+    home = None                        # R25: vertex homes, set after level 0 when homes > 1
     i = 0
     while True:
         if len(eu) == 0:
@@ -230,12 +303,20 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
         in_h[H] = True
         # step 2: arrangement of G'_i = G_i[V_i \ H_i] by a random spanning forest
         m = (eu < ev) & ~in_h[eu] & ~in_h[ev]
+        if home is not None:           # R25: the forest of each home set
+            m &= home[eu] == home[ev]
         gu, gv = eu[m], ev[m]
         s_i = splitmix64_int((seed + i) & _M64)
         key = splitmix64_vec(np.uint64(s_i) ^ ((gu.astype(np.uint64) << np.uint64(32)) | gv.astype(np.uint64)))
         fu, fv = minimum_spanning_forest(n, gu, gv, key)
         rest = V[~in_h[V]]
-        order_i = np.concatenate([H, forest_layout(rest, fu, fv, n)])
+        hs = None
+        if home is None:
+            order_i = np.concatenate([H, forest_layout(rest, fu, fv, n)])
+        else:
+            lay, hs = forest_layout(rest, fu, fv, n, home, homes)
+            order_i = np.concatenate([H, lay])
+            hs = hs + h
         assert len(order_i) == n_i
         pos = np.full(n, -1, dtype=np.int64)
         pos[order_i] = np.arange(n_i, dtype=np.int64)
@@ -250,9 +331,12 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
         bp, bq, ba = bp[srt], bq[srt], ba[srt]
         rp = np.zeros(rows + 1, dtype=np.int64)
         np.cumsum(np.bincount(bp, minlength=rows), out=rp[1:])
-        dec.levels.append(Level(n_i=n_i, perm=perm, row_ptr=rp, col=bq, val=ba, head=h))
+        dec.levels.append(Level(n_i=n_i, perm=perm, row_ptr=rp, col=bq, val=ba, head=h, home_start=hs))
         # step 4: the remainder A_{i+1} = A_i - P B_i P^T, kept in original ids
         eu, ev, ea = eu[~cap], ev[~cap], ea[~cap]
+        if i == 0 and homes > 1:     # R25: homes from level 0 and the remainder's degrees
+            dec.home_los = home_ranges(dec.levels[0], n, b, homes, np.bincount(eu, minlength=n))
+            home = homes_of(dec.levels[0], dec.home_los, n)
         i += 1
     return dec
 

@@ -22,7 +22,7 @@ ARROW_F32, ARROW_F64 = 0, 1
 ORDER = {"original": 0, "permuted": 1}
 RESIDUAL = {"error": 0, "csr": 1}
 BAND = {"block": 0, "strict": 1}    # ARROW_BAND_* (step 3 of LA-Decompose; strict = P:253 / Fig. 3)
-FLAG_NO_GRAPHS, FLAG_DETERMINISTIC, FLAG_GPU_DECOMPOSE = 1, 2, 4   # ARROW_FLAG_*
+FLAG_NO_GRAPHS, FLAG_DETERMINISTIC, FLAG_GPU_DECOMPOSE, FLAG_HOME_AWARE = 1, 2, 4, 8   # ARROW_FLAG_*
 TRANSPORT = {"auto": 0, "p2p": 1, "nccl": 2}
 STATUS = ["ARROW_OK", "ARROW_E_INVALID_ARG", "ARROW_E_BAD_CSR", "ARROW_E_NOT_SYMMETRIC", "ARROW_E_LEVELS",
           "ARROW_E_CUDA", "ARROW_E_NCCL", "ARROW_E_NOMEM", "ARROW_E_STATE", "ARROW_E_UNSUPPORTED"]
@@ -38,7 +38,7 @@ SYMBOLS = [
     "arrow_decomposition_load", "arrow_decomposition_destroy", "arrow_plan_create_from", "arrow_comm_unique_id",
     "arrow_comm_create", "arrow_comm_destroy", "arrow_status_string", "arrow_last_error", "arrow_abi_version",
     "arrow_dist_schedule", "arrow_spmm_iterate", "arrow_decompose_ex", "arrow_spmm_host_batch",
-    "arrow_decompose_gpu",
+    "arrow_decompose_gpu", "arrow_decompose_homes", "arrow_decomposition_homes",
 ]
 
 
@@ -115,6 +115,8 @@ def lib() -> ctypes.CDLL:
             "arrow_decompose": [p, i64, i32, u64, i32, p],
             "arrow_decompose_ex": [p, i64, i32, u64, i32, i32, p],
             "arrow_decompose_gpu": [p, i64, i32, u64, i32, i32, p],
+            "arrow_decompose_homes": [p, i64, i32, u64, i32, i32, i32, i32, p],
+            "arrow_decomposition_homes": [p, i32, p, p],
             "arrow_decomposition_info": [p, p, p, p, p],
             "arrow_decomposition_level_info": [p, i32, p],
             "arrow_decomposition_export_level": [p, i32, p, p, p, p],
@@ -199,11 +201,12 @@ def canonical_sha256(levels) -> str:
 
 
 class Decomposition:
-    """LA-Decompose result, held on the host.  device="cpu" (arrow_decompose_ex, no GPU needed) or
-    device="cuda" (arrow_decompose_gpu on the current CUDA device; the identical decomposition)."""
+    """LA-Decompose result, held on the host.  device="cpu" (no GPU needed) or device="cuda" (the
+    current CUDA device; the identical decomposition).  homes = G > 1: home-set-aware levels >= 1 for
+    a G-rank plan (arrow_decompose_homes, reading R25)."""
 
     def __init__(self, n, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4, keep_residual: bool = False,
-                 band: str = "block", device: str = "cpu", _handle=None):
+                 band: str = "block", device: str = "cpu", homes: int = 1, _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
@@ -212,6 +215,11 @@ class Decomposition:
         A = _csr(n, row_ptr, col, val, keep)
         if device not in ("cpu", "cuda"):
             raise ValueError(f"device must be 'cpu' or 'cuda', not {device!r}")
+        if homes != 1:
+            _check(lib().arrow_decompose_homes(ctypes.byref(A), b, levels, seed, int(keep_residual), BAND[band], homes,
+                                               1 if device == "cuda" else 0, ctypes.byref(self._h)),
+                   "arrow_decompose_homes")
+            return
         fn = "arrow_decompose_gpu" if device == "cuda" else "arrow_decompose_ex"
         _check(getattr(lib(), fn)(ctypes.byref(A), b, levels, seed, int(keep_residual), BAND[band],
                                   ctypes.byref(self._h)), fn)
@@ -231,6 +239,18 @@ class Decomposition:
         _check(lib().arrow_decomposition_info(self._h, ctypes.byref(n), ctypes.byref(b), ctypes.byref(L),
                                               ctypes.byref(r)), "arrow_decomposition_info")
         return {"n": n.value, "b": b.value, "levels": L.value, "residual_nnz": r.value}
+
+    def homes(self, level: int = -1):
+        """(G, ranges): level -1 -> the pi_0 home ranges; level >= 1 -> first position of each home's
+        trees (G + 1 values); ranges is None when G == 1."""
+        G = ctypes.c_int32()
+        _check(lib().arrow_decomposition_homes(self._h, level, ctypes.byref(G), None), "arrow_decomposition_homes")
+        if G.value == 1:
+            return 1, None
+        r = np.zeros(G.value + 1, np.int64)
+        _check(lib().arrow_decomposition_homes(self._h, level, ctypes.byref(G), r.ctypes.data),
+               "arrow_decomposition_homes")
+        return G.value, r
 
     def level_info(self, i: int) -> dict:
         li = LevelInfo()

@@ -222,11 +222,12 @@ arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, ar
 }
 
 static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, bool keep_residual,
-                                   int32_t band, bool on_gpu, std::unique_ptr<arrow_decomposition_s> &D) {
+                                   int32_t band, int32_t homes, bool on_gpu, std::unique_ptr<arrow_decomposition_s> &D) {
     const auto t0 = std::chrono::steady_clock::now();
     arrow_status st = validate_args(A, b, levels);
     if (st != ARROW_OK) return st;
     if (band != ARROW_BAND_BLOCK && band != ARROW_BAND_STRICT) return fail(ARROW_E_INVALID_ARG, "bad band");
+    if (homes < 1 || homes > 8) return fail(ARROW_E_INVALID_ARG, "homes must be in [1, 8]");
     std::string err;
     const int64_t n = A->n;
     if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
@@ -242,8 +243,9 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         if (on_gpu) {
             if (n >= ((int64_t)1 << 31) - 1 || A->nnz >= ((int64_t)1 << 32) - 1)
                 return fail(ARROW_E_INVALID_ARG, "GPU decomposer: n or nnz beyond 32-bit indices");
-            if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, H, err)) return fail(ARROW_E_CUDA, err);
-        } else if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, H, err)) {
+            if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, H, err))
+                return fail(ARROW_E_CUDA, err);
+        } else if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, H, err)) {
             return fail(ARROW_E_INVALID_ARG, err);
         }
         const auto t2 = std::chrono::steady_clock::now();
@@ -275,6 +277,8 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         }
         for (int64_t v = 0; v < n; ++v) D->isolated += (A->row_ptr[v + 1] == A->row_ptr[v]) ? 1 : 0;
         D->levels = std::move(H.levels);
+        D->homes = H.homes;
+        D->home_los = std::move(H.home_los);
     } catch (const std::bad_alloc &) {
         D.reset();
         return fail(ARROW_E_NOMEM, "host allocation failed during decomposition");
@@ -326,6 +330,27 @@ static int validate_decomposition(const arrow_decomposition_s &D, std::string &e
     if (D.res_u.size() != D.res_v.size() || D.res_u.size() != D.res_a.size()) {
         err = "residual array sizes";
         return 1;
+    }
+    if (D.homes < 1 || D.homes > 8) {
+        err = "homes out of range";
+        return 1;
+    }
+    auto ranges_ok = [&](const std::vector<int64_t> &r, int64_t lo, int64_t hi) {
+        if ((int)r.size() != D.homes + 1 || r[0] != lo || r[D.homes] != hi) return false;
+        for (int g = 0; g < D.homes; ++g)
+            if (r[g] > r[g + 1]) return false;
+        return true;
+    };
+    if (D.homes > 1) {
+        if (!D.levels.empty() && !ranges_ok(D.home_los, 0, n)) {
+            err = "home ranges";
+            return 1;
+        }
+        for (size_t i = 1; i < D.levels.size(); ++i)
+            if (!ranges_ok(D.levels[i].home_start, D.levels[i].head, D.levels[i].n_i)) {
+                err = "level " + std::to_string(i) + ": home starts";
+                return 1;
+            }
     }
     for (size_t t = 0; t < D.res_u.size(); ++t)
         if (D.res_u[t] < 0 || D.res_u[t] >= n || D.res_v[t] < 0 || D.res_v[t] >= n) {
@@ -569,7 +594,9 @@ arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels,
         return fail(ARROW_E_INVALID_ARG, "bad options.residual");
     std::unique_ptr<arrow_decomposition_s> D;
     if (opt.flags & ~ARROW_FLAGS_ALL) return fail(ARROW_E_INVALID_ARG, "bad options.flags");
-    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band,
+    int32_t homes = 1;
+    if ((opt.flags & ARROW_FLAG_HOME_AWARE) && comm) homes = comm->nranks;
+    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, homes,
                                      (opt.flags & ARROW_FLAG_GPU_DECOMPOSE) != 0, D);
     if (st != ARROW_OK) return st;
     st = plan_from(*D, &opt, A->dtype, comm, out);
@@ -596,7 +623,7 @@ arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, u
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, false, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, 1, false, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
     return ARROW_OK;
@@ -608,9 +635,36 @@ arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, 
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, true, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, 1, true, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
+    return ARROW_OK;
+}
+
+arrow_status arrow_decompose_homes(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
+                                   int32_t band, int32_t homes, int32_t device, arrow_decomposition *out) {
+    g_err.clear();
+    if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (device != 0 && device != 1) return fail(ARROW_E_INVALID_ARG, "device must be 0 (host) or 1 (CUDA)");
+    std::unique_ptr<arrow_decomposition_s> D;
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, homes, device == 1, D);
+    if (st != ARROW_OK) return st;
+    *out = D.release();
+    return ARROW_OK;
+}
+
+arrow_status arrow_decomposition_homes(arrow_decomposition d, int32_t level, int32_t *homes, int64_t *ranges) {
+    if (!d) return fail(ARROW_E_INVALID_ARG, "decomposition is NULL");
+    if (level < -1 || level >= (int32_t)d->levels.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
+    if (homes) *homes = d->homes;
+    if (ranges && d->homes > 1) {
+        const std::vector<int64_t> *r = nullptr;
+        if (level == -1) r = &d->home_los;
+        else if (level >= 1) r = &d->levels[level].home_start;
+        if (r && r->size() == (size_t)d->homes + 1) std::memcpy(ranges, r->data(), r->size() * 8);
+        else if (level == 0) return fail(ARROW_E_INVALID_ARG, "level 0 has no home starts (use level -1: pi_0 ranges)");
+    }
     return ARROW_OK;
 }
 
@@ -671,7 +725,8 @@ struct Fnv {
         for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ULL; }
     }
 };
-const char kMagic[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '2'};   // 02: header + band
+const char kMagic[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '3'};   // 03: header + band + homes
+const char kMagic2[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '2'};  // 02: header + band
 const char kMagic1[8] = {'A', 'R', 'W', 'D', 'E', 'C', '0', '1'};  // 01: block band only
 }  // namespace
 
@@ -687,16 +742,20 @@ arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path) {
         ok = ok && std::fwrite(p, 1, n, f) == n;
     };
     w(kMagic, 8);
-    const int64_t hdr[7] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated,
-                            (int64_t)d->band};
+    const int64_t hdr[8] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated,
+                            (int64_t)d->band, (int64_t)d->homes};
     w(hdr, sizeof(hdr));
-    for (const HostLevel &L : d->levels) {
+    const bool homes = d->homes > 1 && !d->levels.empty();
+    if (homes) w(d->home_los.data(), d->home_los.size() * 8);
+    for (size_t i = 0; i < d->levels.size(); ++i) {
+        const HostLevel &L = d->levels[i];
         const int64_t lh[4] = {L.rows, L.n_i, L.head, L.row_ptr[L.rows]};
         w(lh, sizeof(lh));
         w(L.perm.data(), L.perm.size() * 4);
         w(L.row_ptr.data(), L.row_ptr.size() * 8);
         w(L.col.data(), L.col.size() * 4);
         w(L.val.data(), L.val.size() * 8);
+        if (homes && i > 0) w(L.home_start.data(), L.home_start.size() * 8);
     }
     w(d->res_u.data(), d->res_u.size() * 4);
     w(d->res_v.data(), d->res_v.size() * 4);
@@ -724,13 +783,21 @@ arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out
         D.reset(new arrow_decomposition_s());
         char magic[8];
         r(magic, 8);
-        const bool v1 = ok && std::memcmp(magic, kMagic1, 8) == 0;
-        if (!ok || (!v1 && std::memcmp(magic, kMagic, 8) != 0)) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "not an arrow decomposition file"); }
-        int64_t hdr[7] = {0, 0, 0, 0, 0, 0, 0};
-        r(hdr, (v1 ? 6 : 7) * sizeof(int64_t));
-        if (!ok || hdr[0] < 0 || hdr[1] < 2 || hdr[3] < 0 || hdr[4] < 0 || hdr[6] < 0 || hdr[6] > 1) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
+        const int ver = !ok ? 0 : std::memcmp(magic, kMagic1, 8) == 0 ? 1 : std::memcmp(magic, kMagic2, 8) == 0 ? 2
+                                      : std::memcmp(magic, kMagic, 8) == 0 ? 3 : 0;
+        if (!ver) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "not an arrow decomposition file"); }
+        int64_t hdr[8] = {0, 0, 0, 0, 0, 0, 0, 1};
+        r(hdr, (ver == 1 ? 6 : ver == 2 ? 7 : 8) * sizeof(int64_t));
+        if (!ok || hdr[0] < 0 || hdr[1] < 2 || hdr[3] < 0 || hdr[4] < 0 || hdr[6] < 0 || hdr[6] > 1 || hdr[7] < 1 ||
+            hdr[7] > 8) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
         D->n = hdr[0]; D->b = hdr[1]; D->seed = (uint64_t)hdr[2]; D->isolated = hdr[5]; D->band = (int32_t)hdr[6];
+        D->homes = (int32_t)hdr[7];
         D->levels.resize(hdr[3]);
+        const bool homes = D->homes > 1 && !D->levels.empty();
+        if (homes) {
+            D->home_los.resize(D->homes + 1);
+            r(D->home_los.data(), D->home_los.size() * 8);
+        }
         for (HostLevel &L : D->levels) {
             int64_t lh[4];
             r(lh, sizeof(lh));
@@ -741,6 +808,10 @@ arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out
             r(L.row_ptr.data(), L.row_ptr.size() * 8);
             r(L.col.data(), L.col.size() * 4);
             r(L.val.data(), L.val.size() * 8);
+            if (homes && &L != &D->levels[0]) {
+                L.home_start.resize(D->homes + 1);
+                r(L.home_start.data(), L.home_start.size() * 8);
+            }
         }
         D->res_u.resize(hdr[4]); D->res_v.resize(hdr[4]); D->res_a.resize(hdr[4]);
         r(D->res_u.data(), D->res_u.size() * 4);

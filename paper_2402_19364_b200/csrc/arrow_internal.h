@@ -20,6 +20,7 @@ struct HostLevel {
     std::vector<int32_t> col;       // [nnz] positions, strictly increasing per row
     std::vector<uint32_t> src;      // [nnz] entry index into A's CSR arrays (decomposer output)
     std::vector<double> val;        // [nnz] values (exact copy of A's fp32/fp64 values)
+    std::vector<int64_t> home_start;  // [homes + 1] (home-aware, levels >= 1): trees of home g at [hs[g], hs[g+1])
 };
 
 struct HostDecomposition {
@@ -27,17 +28,27 @@ struct HostDecomposition {
     int band = 0;                    // step 3's band: 0 block-diagonal tiles (R3), 1 strict |p-q| <= b
     std::vector<HostLevel> levels;
     std::vector<uint32_t> residual;  // entry indices of A left when the level cap is reached
+    int homes = 1;                   // G of the home-set-aware arrangement (R25); 1 = R11
+    std::vector<int64_t> home_los;   // [homes + 1] pi_0 home ranges (homes > 1)
 };
 
-// LA-Decompose (decompose.cpp).  Returns 0 on success, else sets `err`.
+// LA-Decompose (decompose.cpp).  homes > 1: home-set-aware levels >= 1 (R25).  Returns 0 on
+// success, else sets `err`.
 int la_decompose(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
-                 uint64_t seed, int band, HostDecomposition &out, std::string &err);
+                 uint64_t seed, int band, int homes, HostDecomposition &out, std::string &err);
+
+// R25: tile boundaries of a G-way split of prefix costs pre[0..T] (each boundary the
+// prefix nearest g/G of the total, ties to the upper one, never before the previous) -> tb[0..G]
+std::vector<int64_t> split_prefix(const std::vector<int64_t> &pre, int G);
+// R25: pi_0 home ranges los[0..G] from level 0's tile work plus the remainder degree of every vertex
+// (rem_deg[v] = entries of row v left for levels >= 1); A-isolated positions are a last pseudo-tile
+std::vector<int64_t> home_ranges(const HostLevel &L0, int64_t n, int64_t b, int G, const int32_t *rem_deg);
 
 // LA-Decompose on the current CUDA device (gdecompose.cu): the same output as
 // la_decompose, bit for bit (same rules and keys; Boruvka + Euler-tour list ranking in place of the
 // sequential Kruskal / BFS / DFS).  n < 2^31 - 1, nnz < 2^32 - 1.  0 on success, else sets `err`.
 int la_decompose_gpu(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
-                     uint64_t seed, int band, HostDecomposition &out, std::string &err);
+                     uint64_t seed, int band, int homes, HostDecomposition &out, std::string &err);
 
 // Validation helpers (decompose.cpp): 0 ok, 1 bad CSR, 2 not symmetric.
 int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, std::string &err);

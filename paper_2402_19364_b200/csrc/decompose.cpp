@@ -14,6 +14,12 @@
 //   band = 1 (strict, NEXT-2): p<b or q<b or |p-q| <= b -- the arrow-width definition of
 //   and Fig. 3.
 //
+// homes = G > 1 (R25): after level 0 every vertex gets the home range of its
+// pi_0 position (home_ranges: level-0 tile work plus remainder degrees, split G ways); the forest
+// of every level >= 1 takes only edges inside one home and its trees are laid out by (home of the
+// root, size desc, min id asc), so that rank g's level-i tiles hold rows whose X and Y live on
+// rank g (edges between homes wait for a later level or a head).
+//
 // Parallel where the work is bulk (degree histograms, edge keys, the edge sort, extraction,
 // CSR assembly); union-find and the tree layouts are sequential.
 #include <algorithm>
@@ -123,12 +129,49 @@ void stable_partition_par(const std::vector<uint32_t> &in, Pred pred, std::vecto
 
 }  // namespace
 
+std::vector<int64_t> split_prefix(const std::vector<int64_t> &pre, int G) {
+    const int64_t T = (int64_t)pre.size() - 1, tot = pre[T];
+    std::vector<int64_t> tb(G + 1, T);
+    tb[0] = 0;
+    for (int g = 1; g < G; ++g) {
+        // first t with pre[t] * G >= tot * g (exact), one back if pre[t-1] is strictly nearer
+        int64_t lo = 0, hi = T;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (pre[mid] * G >= tot * g) hi = mid;
+            else lo = mid + 1;
+        }
+        int64_t t = lo;
+        if (t > 0 && tot * g - pre[t - 1] * G < pre[t] * G - tot * g) t -= 1;
+        tb[g] = std::min(std::max(t, tb[g - 1]), T);
+    }
+    return tb;
+}
+
+std::vector<int64_t> home_ranges(const HostLevel &L0, int64_t n, int64_t b, int G, const int32_t *rem_deg) {
+    const int64_t T = (L0.n_i + b - 1) / b, h = L0.head;
+    std::vector<int64_t> pre(T + 2, 0);  // T level-0 tiles + the A-isolated pseudo-tile
+    for (int64_t p = h; p < L0.n_i; ++p) pre[p / b + 1] += (L0.row_ptr[p + 1] - L0.row_ptr[p]) + 4;
+    for (int64_t e = 0; e < L0.row_ptr[h]; ++e) pre[L0.col[e] / b + 1] += 1;
+    for (int64_t p = 0; p < L0.n_i; ++p) pre[p / b + 1] += rem_deg[L0.perm[p]];
+    pre[T + 1] = n - L0.n_i;
+    for (int64_t t = 0; t <= T; ++t) pre[t + 1] += pre[t];
+    const std::vector<int64_t> tb = split_prefix(pre, G);
+    std::vector<int64_t> los(G + 1);
+    for (int g = 0; g <= G; ++g) los[g] = std::min<int64_t>(L0.n_i, tb[g] * b);
+    los[0] = 0;
+    los[G] = n;
+    return los;
+}
+
 int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, int32_t max_levels,
-                 uint64_t seed, int band, HostDecomposition &out, std::string &err) {
+                 uint64_t seed, int band, int homes, HostDecomposition &out, std::string &err) {
     out = HostDecomposition{};
     out.n = n;
     out.b = b;
     out.band = band;
+    out.homes = homes;
+    std::vector<uint8_t> home;  // homes > 1: home of every vertex (after level 0)
     const int64_t nnz = rp[n];
     if (nnz == 0) return 0;
 
@@ -181,7 +224,7 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
             ent,
             [&](uint32_t e) {
                 const int32_t u = erow[e], v = col[e];
-                return u < v && !in_head[u] && !in_head[v];
+                return u < v && !in_head[u] && !in_head[v] && (home.empty() || home[u] == home[v]);
             },
             gent, dummy);
         dummy.clear();
@@ -273,10 +316,21 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
             trees.push_back(Tree{tsize, r, off});
         }
         if (fpos + h != n_i) { err = "internal: forest layout does not cover V_i"; return 1; }
-        std::stable_sort(trees.begin(), trees.end(), [](const Tree &a, const Tree &c) {
-            return a.size != c.size ? a.size > c.size : a.root < c.root;
-        });
         HostLevel L;
+        if (home.empty()) {
+            std::stable_sort(trees.begin(), trees.end(), [](const Tree &a, const Tree &c) {
+                return a.size != c.size ? a.size > c.size : a.root < c.root;
+            });
+        } else {  // R25: by home of the root first
+            std::stable_sort(trees.begin(), trees.end(), [&](const Tree &a, const Tree &c) {
+                if (home[a.root] != home[c.root]) return home[a.root] < home[c.root];
+                return a.size != c.size ? a.size > c.size : a.root < c.root;
+            });
+            L.home_start.assign(homes + 1, 0);
+            for (const Tree &t : trees) L.home_start[home[t.root] + 1] += t.size;
+            L.home_start[0] = h;
+            for (int g = 0; g < homes; ++g) L.home_start[g + 1] += L.home_start[g];
+        }
         L.n_i = n_i;
         L.head = h;
         L.rows = (i == 0) ? n : n_i;
@@ -335,6 +389,17 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
             L.src[t] = (uint32_t)(packed[t] & 0xFFFFFFFFu);
         }
         out.levels.push_back(std::move(L));
+        if (i == 0 && homes > 1) {  // R25: homes from level 0's tile work and the remainder degrees
+            std::vector<int32_t> rem(n, 0);
+            for (uint32_t e : rest_ent) rem[erow[e]]++;
+            out.home_los = home_ranges(out.levels[0], n, b, homes, rem.data());
+            home.assign(n, 0);
+            for (int64_t p = 0; p < n; ++p) {
+                const int64_t g = std::upper_bound(out.home_los.begin() + 1, out.home_los.end() - 1, p) -
+                                  (out.home_los.begin() + 1);
+                home[out.levels[0].perm[p]] = (uint8_t)g;
+            }
+        }
         // ---- step 4: remainder A_{i+1}, kept as original entries
         ent.swap(rest_ent);
         rest_ent.clear();

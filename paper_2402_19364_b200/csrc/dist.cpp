@@ -164,19 +164,9 @@ int32_t *upload(DistState *S, const std::vector<V> &v, bool &ok) { return upload
 
 // contiguous split of tiles [0, T) into G ranges of ~equal cost; returns G+1 tile boundaries
 std::vector<int64_t> split_tiles(const std::vector<int64_t> &cost, int G) {
-    const int64_t T = (int64_t)cost.size();
-    std::vector<int64_t> pre(T + 1, 0);
-    for (int64_t t = 0; t < T; ++t) pre[t + 1] = pre[t] + cost[t];
-    std::vector<int64_t> tb(G + 1, T);
-    tb[0] = 0;
-    for (int g = 1; g < G; ++g) {
-        const double target = (double)pre[T] * g / G;
-        tb[g] = std::lower_bound(pre.begin(), pre.end(), (int64_t)target) - pre.begin();
-        // the boundary whose prefix cost is nearest the target (lower_bound alone favours the left)
-        if (tb[g] > 0 && tb[g] <= T && target - (double)pre[tb[g] - 1] < (double)pre[tb[g]] - target) tb[g] -= 1;
-        tb[g] = std::min(std::max(tb[g], tb[g - 1]), T);
-    }
-    return tb;
+    std::vector<int64_t> pre(cost.size() + 1, 0);
+    for (size_t t = 0; t < cost.size(); ++t) pre[t + 1] = pre[t] + cost[t];
+    return split_prefix(pre, G);
 }
 
 std::vector<int64_t> tile_costs(const HostLevel &L, int64_t b) {
@@ -220,10 +210,16 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     const int64_t n = D.n, b = D.b;
     const int nl = (int)D.levels.size();
 
-    // ---- home ranges from the level-0 tile split
+    // ---- home ranges from the level-0 tile split (home-aware decompositions for G ranks: the ranges
+    // the arrangement was made for, R25)
     std::vector<int64_t> los(G + 1, 0);
     std::vector<int32_t> pos0(n, 0);
-    if (nl > 0) {
+    const bool aware = G > 1 && D.homes == G && nl > 0;
+    if (aware) {
+        const HostLevel &L0 = D.levels[0];
+        for (int64_t p = 0; p < n; ++p) pos0[L0.perm[p]] = (int32_t)p;
+        los = D.home_los;
+    } else if (nl > 0) {
         const HostLevel &L0 = D.levels[0];
         for (int64_t p = 0; p < n; ++p) pos0[L0.perm[p]] = (int32_t)p;
         // A-isolated rows (positions >= n_0, R8) go to the last rank: one pseudo tile costing a
@@ -258,10 +254,6 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             qa = std::min<int64_t>(n_i, tbs[i][c] * b);
             qb = std::min<int64_t>(n_i, tbs[i][c + 1] * b);
         }
-    };
-    auto tile_owner = [&](int i, int64_t q) -> int {
-        if (i == 0) return owner(q);
-        return rk[i][std::upper_bound(tbs[i].begin() + 1, tbs[i].end() - 1, q / b) - (tbs[i].begin() + 1)];
     };
     H.L.resize(nl);
     // strict band: a body row p also reads the columns q with |p - q| <= b that lie outside its
@@ -300,7 +292,17 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         DistHostLevel &DL = H.L[i];
         DL.h = L.head;
         if (i == 0) continue;
-        {
+        if (aware) {
+            // R25: rank g takes the tiles of home g's trees (boundaries at the nearest tile edge)
+            const int64_t T = (L.n_i + b - 1) / b;
+            tbs[i].assign(G + 1, T);
+            tbs[i][0] = 0;
+            for (int g = 1; g < G; ++g)
+                tbs[i][g] = std::min(std::max((L.home_start[g] + b / 2) / b, tbs[i][g - 1]), T);
+            rk[i].resize(G);
+            cr[i].resize(G);
+            for (int g = 0; g < G; ++g) rk[i][g] = cr[i][g] = g;
+        } else {
             const std::vector<int64_t> cost = tile_costs(L, b);
             tbs[i] = split_tiles(cost, G);
             std::vector<int64_t> cc(G, 0);

@@ -97,12 +97,13 @@ __global__ void k_mark_head(const uint64_t *sorted, int64_t h, uint8_t *in_head,
         head[j] = (int32_t)v;
     }
 }
+// home != nullptr (R25, levels >= 1): only edges inside one home
 __global__ void k_gprime_flags(const uint32_t *ent, int64_t m, const int32_t *erow, const int32_t *col,
-                               const uint8_t *in_head, uint8_t *flag) {
+                               const uint8_t *in_head, const uint8_t *home, uint8_t *flag) {
     GRID_LOOP(t, m) {
         const uint32_t e = ent[t];
         const int32_t u = erow[e], v = col[e];
-        flag[t] = (u < v && !in_head[u] && !in_head[v]) ? 1 : 0;
+        flag[t] = (u < v && !in_head[u] && !in_head[v] && (!home || home[u] == home[v])) ? 1 : 0;
     }
 }
 __global__ void k_edge_keys(const uint32_t *gent, int64_t me, const int32_t *erow, const int32_t *col, uint64_t s_i,
@@ -353,6 +354,14 @@ __global__ void k_count_src64(const int32_t *asrc, int64_t na, unsigned long lon
     GRID_LOOP(a, na) atomicAdd(&cnt[asrc[a]], 1ull);
 }
 __global__ void k_u8_to_i64(const uint8_t *x, int64_t n, int64_t *y) { GRID_LOOP(i, n) y[i] = x[i]; }
+// R25: home of each tree's root (its min id; troot holds component labels) and the vertices per home
+__global__ void k_root_homes(const int32_t *troot, int64_t nt, const int32_t *tmin, const uint8_t *home, uint8_t *key) {
+    GRID_LOOP(t, nt) key[t] = home[tmin[troot[t]]];
+}
+__global__ void k_home_sizes(const int32_t *troot, int64_t nt, const int32_t *tmin, const uint8_t *home,
+                             const int32_t *tsize, unsigned long long *cnt) {
+    GRID_LOOP(t, nt) atomicAdd(&cnt[home[tmin[troot[t]]]], (unsigned long long)tsize[troot[t]]);
+}
 
 // ARROW_DECOMPOSE_TRACE=1: per-phase wall times (device synchronised at each mark) on stderr
 struct Trace {
@@ -390,11 +399,12 @@ struct Cub {
 }  // namespace
 
 int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t b, int32_t max_levels, uint64_t seed,
-                     int band, HostDecomposition &out, std::string &err) {
+                     int band, int homes, HostDecomposition &out, std::string &err) {
     out = HostDecomposition{};
     out.n = n;
     out.b = b;
     out.band = band;
+    out.homes = homes;
     const int64_t nnz = rp[n];
     if (nnz == 0) return 0;
     if (n >= ((int64_t)1 << 31) - 1 || nnz >= ((int64_t)1 << 32) - 1) {
@@ -419,6 +429,9 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
     Buf<int64_t> cnt, dist1, dist2, f64;
     Buf<uint64_t> k1, k1s;
     Buf<uint32_t> srcs;
+    Buf<uint8_t> d_home, hk, hk2;  // R25: vertex homes (after level 0), root-home sort keys
+    Buf<int32_t> troot2;
+    Buf<unsigned long long> hcnt;
     GD_TRY(d_rp.need(n + 1));
     GD_TRY(d_col.need(nnz));
     GD_TRY(d_erow.need(nnz));
@@ -492,7 +505,8 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
         // ---- step 2: G'_i edges with their keys
         GD_TRY(d_flag.need(m));
         GD_TRY(d_gent.need(m));
-        k_gprime_flags<<<blocks_for(m), 256>>>(d_ent.p, m, d_erow.p, d_col.p, d_inhead.p, d_flag.p);
+        k_gprime_flags<<<blocks_for(m), 256>>>(d_ent.p, m, d_erow.p, d_col.p, d_inhead.p,
+                                               (i > 0 && homes > 1) ? d_home.p : nullptr, d_flag.p);
         GD_TRY(cub.run([&](void *t, size_t &s) {
             return cub::DeviceSelect::Flagged(t, s, d_ent.p, d_flag.p, d_gent.p, d_cnt.p, (int)m);
         }));
@@ -593,6 +607,24 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
             GD_TRY(cub.run([&](void *t, size_t &s) {
                 return cub::DeviceRadixSort::SortPairs(t, s, d_k2.p, d_k2b.p, vals.p, d_troot.p, (int)nt);
             }));
+        }
+        std::vector<int64_t> home_start;
+        if (i > 0 && homes > 1) {  // R25: stable re-sort by the home of the root, home starts
+            GD_TRY(hk.need(std::max<int64_t>(nt, 1)));
+            GD_TRY(hk2.need(std::max<int64_t>(nt, 1)));
+            GD_TRY(troot2.need(std::max<int64_t>(nt, 1)));
+            GD_TRY(hcnt.need(homes));
+            k_root_homes<<<blocks_for(nt), 256>>>(d_troot.p, nt, d_tmin.p, d_home.p, hk.p);
+            GD_TRY(cub.run([&](void *t, size_t &s) {
+                return cub::DeviceRadixSort::SortPairs(t, s, hk.p, hk2.p, d_troot.p, troot2.p, (int)nt, 0, 8);
+            }));
+            GD_TRY(cudaMemcpy(d_troot.p, troot2.p, nt * 4, cudaMemcpyDeviceToDevice));
+            GD_TRY(cudaMemset(hcnt.p, 0, homes * 8));
+            k_home_sizes<<<blocks_for(nt), 256>>>(d_troot.p, nt, d_tmin.p, d_home.p, d_tsize.p, hcnt.p);
+            std::vector<unsigned long long> hc(homes);
+            GD_TRY(cudaMemcpy(hc.data(), hcnt.p, homes * 8, cudaMemcpyDeviceToHost));
+            home_start.assign(homes + 1, h);
+            for (int g = 0; g < homes; ++g) home_start[g + 1] = home_start[g] + (int64_t)hc[g];
         }
         GD_TRY(d_tsz.need(std::max<int64_t>(nt, 1)));
         GD_TRY(d_toff_scan.need(std::max<int64_t>(nt, 1)));
@@ -700,6 +732,7 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
         L.n_i = n_i;
         L.head = h;
         L.rows = rows;
+        L.home_start = std::move(home_start);
         L.perm.resize(rows);
         GD_TRY(cudaMemcpy(L.perm.data(), d_perm.p, n_i * 4, cudaMemcpyDeviceToHost));
         if (i == 0) std::copy(isolated.begin(), isolated.end(), L.perm.begin() + n_i);
@@ -750,6 +783,21 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
             tr.mark(7);
         }
         out.levels.push_back(std::move(L));
+        if (i == 0 && homes > 1) {  // R25: homes from level 0's tile work and the remainder degrees
+            GD_TRY(cudaMemset(d_deg.p, 0, n * 4));
+            k_degree<<<blocks_for(mr), 256>>>(d_rest.p, mr, d_erow.p, d_deg.p);
+            std::vector<int32_t> rem(n);
+            GD_TRY(cudaMemcpy(rem.data(), d_deg.p, n * 4, cudaMemcpyDeviceToHost));
+            out.home_los = home_ranges(out.levels[0], n, b, homes, rem.data());
+            std::vector<uint8_t> hv(n, 0);
+            for (int64_t p = 0; p < n; ++p) {
+                const int64_t g = std::upper_bound(out.home_los.begin() + 1, out.home_los.end() - 1, p) -
+                                  (out.home_los.begin() + 1);
+                hv[out.levels[0].perm[p]] = (uint8_t)g;
+            }
+            GD_TRY(d_home.need(n));
+            GD_TRY(cudaMemcpy(d_home.p, hv.data(), n, cudaMemcpyHostToDevice));
+        }
         swap_buf(d_ent, d_rest);
         m = mr;
     }

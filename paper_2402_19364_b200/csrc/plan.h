@@ -123,6 +123,8 @@ struct arrow_decomposition_s {
     int64_t n = 0, b = 0;
     uint64_t seed = 4;
     int32_t band = 0;                    // ARROW_BAND_* of step 3
+    int32_t homes = 1;                   // home-set-aware arrangement for this many ranks (R25); 1 = off
+    std::vector<int64_t> home_los;       // [homes + 1] pi_0 home ranges (homes > 1)
     int64_t isolated = 0;
     std::vector<HostLevel> levels;
     std::vector<int32_t> res_u, res_v;  // residual entries, original ids, CSR order

@@ -19,7 +19,10 @@ CASES = [("RMAT(12,8,1)", 64, (16, 16, 16), "f64"), ("RMAT(14,8,2)", 256, (128, 
          ("RMAT(10,4,3)", 1024, (4, 4), "f64"), ("PATH(3000,1)", 8, (3, 5), "f64"),
          # strict band (|p - q| <= b): level-0 and level->=1 rows read X rows of the neighbouring ranks
          ("RMAT(13,8,4)", 128, (64, 16), "f64", "strict"), ("GRID(128,1)", 256, (32,), "f32", "strict"),
-         ("PATH(3000,1)", 8, (3,), "f64", "strict"), ("RMAT(12,8,1)", 32, (8,), "f64", "strict")]
+         ("PATH(3000,1)", 8, (3,), "f64", "strict"), ("RMAT(12,8,1)", 32, (8,), "f64", "strict"),
+         # home-set-aware levels >= 1 for this world size (R25, ARROW_FLAG_HOME_AWARE)
+         ("RMAT(13,8,4)", 128, (64, 16), "f64", "block", "homes"), ("RMAT(14,8,2)", 256, (128,), "f32", "block", "homes"),
+         ("GRID(128,1)", 256, (32,), "f64", "strict", "homes")]
 
 
 def run(rank, world, port):
@@ -37,10 +40,12 @@ def run(rank, world, port):
     comm = ab.Comm(world, rank, uid[0])
     fails = []
     transport = os.environ.get("ARROW_TEST_TRANSPORT", "auto")
-    for spec, b, ks, dtype, *band in CASES:
+    for spec, b, ks, dtype, *extra in CASES:
         g = datagen.make_graph(spec)
+        band = extra[0] if extra else "block"
+        flags = ab.arrow.FLAG_HOME_AWARE if "homes" in extra else 0
         plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, b, dtype=dtype, comm=comm, transport=transport,
-                       band=band[0] if band else "block")
+                       band=band, flags=flags)
         lo, hi = plan.local_begin, plan.local_end
         perm0 = plan.export_level(0)[0]
         rows = perm0[lo:hi]
@@ -59,7 +64,7 @@ def run(rank, world, port):
                 ok = ((np.linalg.norm(Y - ref) / den if den > 0 else np.linalg.norm(Y)) <= 1e-4 and
                       bool(np.all(np.abs(Y - ref) <= 1e-5 * scale + 1e-30)))
             if not ok:
-                fails.append(f"{spec} b={b} {band} k={k} call {rep} {dtype} rank {rank}: max err {np.abs(Y - ref).max()}")
+                fails.append(f"{spec} b={b} {extra} k={k} call {rep} {dtype} rank {rank}: max err {np.abs(Y - ref).max()}")
         plan.close()
     comm.close()
     dist.destroy_process_group()

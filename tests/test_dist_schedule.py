@@ -17,9 +17,9 @@ import datagen
 import paper_2402_19364_b200 as ab
 
 
-def _dec(spec="RMAT(12,8,1)", b=64, band="block"):
+def _dec(spec="RMAT(12,8,1)", b=64, band="block", homes=1):
     g = datagen.make_graph(spec)
-    return g, ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band)
+    return g, ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band, homes=homes)
 
 
 def check_schedules(g, D, scheds, strict=False):
@@ -81,6 +81,20 @@ def test_schedule_consistency_single_process(G):
 def test_schedule_strict_band(G, spec, b):
     g, D = _dec(spec, b, band="strict")
     check_schedules(g, D, [D.dist_schedule(G, r) for r in range(G)], strict=True)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+@pytest.mark.parametrize("band", ["block", "strict"])
+def test_schedule_home_aware(G, band):
+    """R25: a decomposition made for G homes uses its home ranges as the pi_0 split and gives rank g
+    the tiles of home g's trees; schedules for another rank count fall back to the cost split."""
+    g, D = _dec("RMAT(13,8,2)", 128, band=band, homes=G)
+    sc = [D.dist_schedule(G, r) for r in range(G)]
+    check_schedules(g, D, sc, strict=band == "strict")
+    los = D.homes(-1)[1]
+    assert [s["lo"] for s in sc] == list(los[:-1]) and sc[-1]["hi"] == los[-1]
+    other = 2 if G != 2 else 3
+    check_schedules(g, D, [D.dist_schedule(other, r) for r in range(other)], strict=band == "strict")
 
 
 def test_schedule_more_ranks_than_tiles():
