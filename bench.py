@@ -326,6 +326,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0, help="arrow_options.flags (ARROW_FLAG_*)")
     ap.add_argument("--home-aware", action="store_true",
                     help="N > 1: decompose with home-set-aware levels >= 1 for the N ranks (R25)")
+    ap.add_argument("--home-levels", type=int, default=1, help="--home-aware: levels 1..L use same-home forests")
     ap.add_argument("--gpu-decompose", action="store_true", help="N > 1: rank 0 decomposes on its GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -366,7 +367,7 @@ def main():
         if rank == 0:
             t0 = time.perf_counter()
             dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, cfg["b"], band=args.band,
-                                   homes=world if args.home_aware else 1,
+                                   homes=world if args.home_aware else 1, home_levels=args.home_levels,
                                    device="cuda" if args.gpu_decompose else "cpu")
             decompose_s[0] = time.perf_counter() - t0
             dec.save(path[0])
@@ -551,7 +552,8 @@ def main():
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
                        "band": args.band,
-                       "arrangement": ("home-aware (R25) for %d ranks" % world) if (args.home_aware and world > 1)
+                       "arrangement": ("home-aware (R25) for %d ranks, levels 1..%d" % (world, args.home_levels))
+                                      if (args.home_aware and world > 1)
                                       else "random spanning forest, smallest-first (R6-R12)",
                        "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",
                        "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},

@@ -103,7 +103,7 @@ enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each
        ARROW_FLAG_GPU_DECOMPOSE = 4,   /* arrow_plan_create_ex: run LA-Decompose on the current CUDA device
                                           (arrow_decompose_gpu) instead of the host; same decomposition */
        ARROW_FLAG_HOME_AWARE = 8,      /* arrow_plan_create_ex with a comm: home-set-aware arrangement for the
-                                          comm's ranks (arrow_decompose_homes, homes = nranks) */
+                                          comm's ranks (arrow_decompose_homes, homes = nranks, home_levels = 1) */
        ARROW_FLAGS_ALL = 15 };
 /* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
  * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
@@ -270,18 +270,22 @@ arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, 
  * R25 of DESIGN.md §3; an extension, not in the paper): after level 0 every vertex gets the home range
  * of its pi_0 position -- G contiguous ranges of whole level-0 tiles balanced by level-0 work plus
  * every vertex's entries left for levels >= 1 -- and the trees of every level >= 1 are laid out by
- * (home of the root, size desc, min id asc) instead of (size desc, min id asc), so a distributed
- * plan for G ranks computes each level's home-g trees on rank g and moves few rows over NVLink.
- * homes = 1 is arrow_decompose_ex.  device: 0 = host, 1 = the current CUDA device (as
+ * (home of the root, size desc, min id asc) instead of (size desc, min id asc) for the levels
+ * 1..home_levels (>= 1; their forests use only the edges inside one home), so a distributed plan for G
+ * ranks computes those levels' home-g trees on rank g and moves few of their rows over NVLink; edges
+ * between homes wait for a later level, so more home-aware levels mean more levels and rows
+ * (DESIGN.md §8.2 measures the trade).  homes = 1 is arrow_decompose_ex (home_levels ignored).  device: 0 = host, 1 = the current CUDA device (as
  * arrow_decompose_gpu; the same decomposition).  Errors as arrow_decompose_ex / _gpu; homes outside
  * [1, 8] or device not 0/1 -> ARROW_E_INVALID_ARG.  Saved files (format 3) record the homes. */
 arrow_status arrow_decompose_homes(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
-                                   int32_t band, int32_t homes, int32_t device, arrow_decomposition *out);
-/* homes of a decomposition (*homes, may be NULL) and, when homes > 1 and ranges != NULL, level = -1:
- * the pi_0 home ranges ranges[0..homes]; level >= 1: the first position of each home's trees
- * (ranges[g] .. ranges[g+1] hold home g's trees, ranges[0] = head, ranges[homes] = n_i); level 0 ->
- * ARROW_E_INVALID_ARG. */
-arrow_status arrow_decomposition_homes(arrow_decomposition d, int32_t level, int32_t *homes, int64_t *ranges);
+                                   int32_t band, int32_t homes, int32_t home_levels, int32_t device,
+                                   arrow_decomposition *out);
+/* homes and home_levels of a decomposition (either pointer may be NULL) and, when homes > 1 and
+ * ranges != NULL, level = -1: the pi_0 home ranges ranges[0..homes]; level in 1..home_levels: the
+ * first position of each home's trees (ranges[g] .. ranges[g+1] hold home g's trees, ranges[0] = head,
+ * ranges[homes] = n_i); any other level -> ARROW_E_INVALID_ARG. */
+arrow_status arrow_decomposition_homes(arrow_decomposition d, int32_t level, int32_t *homes, int32_t *home_levels,
+                                       int64_t *ranges);
 /* n, b, order (number of arrow matrices), residual entries; any pointer may be NULL. */
 arrow_status arrow_decomposition_info(arrow_decomposition d, int64_t *n, int64_t *b, int32_t *levels,
                                       int64_t *residual_nnz);

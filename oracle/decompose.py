@@ -30,11 +30,12 @@ listed in DESIGN.md §3:
 Home-set-aware arrangement (homes = G > 1, reading R25 in DESIGN.md §3 --
 an extension for G GPUs, not in the paper): after level 0, every vertex gets a home
 g = home_of(pi_0 position) from the G contiguous pi_0 ranges of home_ranges() (level-0 tiles
-split by level-0 work plus the remainder degrees); for levels i >= 1 the spanning forest is
-taken over the edges of G'_i whose endpoints share a home (so every tree lies in one home) and
-the trees are sorted by (home of the root, size desc, min id asc) instead of R11's (size desc,
-min id asc); home_start[g] records where home g's trees begin.  Edges between homes wait for a
-later level (or a head).  homes = 1 is the decomposition above.
+split by level-0 work plus the remainder degrees); for the levels 1 <= i <= home_levels the
+spanning forest is taken over the edges of G'_i whose endpoints share a home (so every tree lies
+in one home) and the trees are sorted by (home of the root, size desc, min id asc) instead of
+R11's (size desc, min id asc); home_start[g] records where home g's trees begin.  Edges between
+homes wait for a later level (or a head); levels after home_levels are laid out as above.
+homes = 1 is the decomposition above.
 """
 from __future__ import annotations
 
@@ -72,7 +73,7 @@ class Level:
     col: np.ndarray          # int64[nnz_i] positions, sorted within each row
     val: np.ndarray          # float64[nnz_i]
     head: int                # h_i = min(b, n_i)
-    home_start: np.ndarray | None = None   # int64[G+1] (homes > 1, levels >= 1): trees of home g at [hs[g], hs[g+1])
+    home_start: np.ndarray | None = None   # int64[G+1] (home-aware levels): trees of home g at [hs[g], hs[g+1])
 
     @property
     def rows(self) -> int:
@@ -92,6 +93,7 @@ class Decomposition:
     band: str = "block"              # step 3's band (captured())
     homes: int = 1                   # G of the home-set-aware arrangement (R25); 1 = R11
     home_los: np.ndarray | None = None   # int64[G+1] pi_0 home ranges (homes > 1)
+    home_levels: int = 0             # levels 1..home_levels are home-aware (homes > 1)
 
     @property
     def order(self) -> int:
@@ -272,11 +274,13 @@ def extract(eu, ev, ea, order, b: int, band: str = "block"):
 
 # ---------------------------------------------------------------------------- LA-Decompose
 def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4,
-                 band: str = "block", homes: int = 1) -> Decomposition:
+                 band: str = "block", homes: int = 1, home_levels: int = 1) -> Decomposition:
     if band not in BANDS:
         raise ValueError(f"unknown band {band!r}")
     if not 1 <= homes <= 8:
         raise ValueError("homes must be in [1, 8]")
+    if home_levels < 1:
+        raise ValueError("home_levels must be >= 1")
     if b < 2:
         raise ValueError("arrow width b must be >= 2 (P:807)")
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
@@ -285,7 +289,7 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
     ea = np.asarray(val, dtype=np.float64)
     deg_a = np.diff(row_ptr)
     isolated_a = np.flatnonzero(deg_a == 0)
-    dec = Decomposition(n=n, b=b, band=band, homes=homes)
+    dec = Decomposition(n=n, b=b, band=band, homes=homes, home_levels=home_levels if homes > 1 else 0)
     home = None                        # R25: vertex homes, set after level 0 when homes > 1
     i = 0
     while True:
@@ -302,8 +306,9 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
         in_h = np.zeros(n, dtype=bool)
         in_h[H] = True
         # step 2: arrangement of G'_i = G_i[V_i \ H_i] by a random spanning forest
+        aware = home is not None and i <= home_levels
         m = (eu < ev) & ~in_h[eu] & ~in_h[ev]
-        if home is not None:           # R25: the forest of each home set
+        if aware:                      # R25: the forest of each home set
             m &= home[eu] == home[ev]
         gu, gv = eu[m], ev[m]
         s_i = splitmix64_int((seed + i) & _M64)
@@ -311,7 +316,7 @@ def la_decompose(n: int, row_ptr, col, val, b: int, levels: int = 0, seed: int =
         fu, fv = minimum_spanning_forest(n, gu, gv, key)
         rest = V[~in_h[V]]
         hs = None
-        if home is None:
+        if not aware:
             order_i = np.concatenate([H, forest_layout(rest, fu, fv, n)])
         else:
             lay, hs = forest_layout(rest, fu, fv, n, home, homes)

@@ -115,8 +115,8 @@ def lib() -> ctypes.CDLL:
             "arrow_decompose": [p, i64, i32, u64, i32, p],
             "arrow_decompose_ex": [p, i64, i32, u64, i32, i32, p],
             "arrow_decompose_gpu": [p, i64, i32, u64, i32, i32, p],
-            "arrow_decompose_homes": [p, i64, i32, u64, i32, i32, i32, i32, p],
-            "arrow_decomposition_homes": [p, i32, p, p],
+            "arrow_decompose_homes": [p, i64, i32, u64, i32, i32, i32, i32, i32, p],
+            "arrow_decomposition_homes": [p, i32, p, p, p],
             "arrow_decomposition_info": [p, p, p, p, p],
             "arrow_decomposition_level_info": [p, i32, p],
             "arrow_decomposition_export_level": [p, i32, p, p, p, p],
@@ -206,7 +206,7 @@ class Decomposition:
     a G-rank plan (arrow_decompose_homes, reading R25)."""
 
     def __init__(self, n, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4, keep_residual: bool = False,
-                 band: str = "block", device: str = "cpu", homes: int = 1, _handle=None):
+                 band: str = "block", device: str = "cpu", homes: int = 1, home_levels: int = 1, _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
@@ -217,7 +217,7 @@ class Decomposition:
             raise ValueError(f"device must be 'cpu' or 'cuda', not {device!r}")
         if homes != 1:
             _check(lib().arrow_decompose_homes(ctypes.byref(A), b, levels, seed, int(keep_residual), BAND[band], homes,
-                                               1 if device == "cuda" else 0, ctypes.byref(self._h)),
+                                               home_levels, 1 if device == "cuda" else 0, ctypes.byref(self._h)),
                    "arrow_decompose_homes")
             return
         fn = "arrow_decompose_gpu" if device == "cuda" else "arrow_decompose_ex"
@@ -241,16 +241,21 @@ class Decomposition:
         return {"n": n.value, "b": b.value, "levels": L.value, "residual_nnz": r.value}
 
     def homes(self, level: int = -1):
-        """(G, ranges): level -1 -> the pi_0 home ranges; level >= 1 -> first position of each home's
-        trees (G + 1 values); ranges is None when G == 1."""
-        G = ctypes.c_int32()
-        _check(lib().arrow_decomposition_homes(self._h, level, ctypes.byref(G), None), "arrow_decomposition_homes")
+        """(G, ranges): level -1 -> the pi_0 home ranges; level in 1..home_levels -> first position of
+        each home's trees (G + 1 values); ranges is None when G == 1."""
+        G, HL = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().arrow_decomposition_homes(self._h, level, ctypes.byref(G), ctypes.byref(HL), None),
+               "arrow_decomposition_homes")
         if G.value == 1:
             return 1, None
         r = np.zeros(G.value + 1, np.int64)
-        _check(lib().arrow_decomposition_homes(self._h, level, ctypes.byref(G), r.ctypes.data),
-               "arrow_decomposition_homes")
+        _check(lib().arrow_decomposition_homes(self._h, level, None, None, r.ctypes.data), "arrow_decomposition_homes")
         return G.value, r
+
+    def home_levels(self) -> int:
+        HL = ctypes.c_int32()
+        _check(lib().arrow_decomposition_homes(self._h, -1, None, ctypes.byref(HL), None), "arrow_decomposition_homes")
+        return HL.value
 
     def level_info(self, i: int) -> dict:
         li = LevelInfo()

@@ -222,12 +222,14 @@ arrow_status arrow_plan_create(const arrow_csr *A, int64_t b, int32_t levels, ar
 }
 
 static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, bool keep_residual,
-                                   int32_t band, int32_t homes, bool on_gpu, std::unique_ptr<arrow_decomposition_s> &D) {
+                                   int32_t band, int32_t homes, int32_t home_levels, bool on_gpu,
+                                   std::unique_ptr<arrow_decomposition_s> &D) {
     const auto t0 = std::chrono::steady_clock::now();
     arrow_status st = validate_args(A, b, levels);
     if (st != ARROW_OK) return st;
     if (band != ARROW_BAND_BLOCK && band != ARROW_BAND_STRICT) return fail(ARROW_E_INVALID_ARG, "bad band");
     if (homes < 1 || homes > 8) return fail(ARROW_E_INVALID_ARG, "homes must be in [1, 8]");
+    if (homes > 1 && home_levels < 1) return fail(ARROW_E_INVALID_ARG, "home_levels must be >= 1");
     std::string err;
     const int64_t n = A->n;
     if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
@@ -243,9 +245,9 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         if (on_gpu) {
             if (n >= ((int64_t)1 << 31) - 1 || A->nnz >= ((int64_t)1 << 32) - 1)
                 return fail(ARROW_E_INVALID_ARG, "GPU decomposer: n or nnz beyond 32-bit indices");
-            if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, H, err))
+            if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, home_levels, H, err))
                 return fail(ARROW_E_CUDA, err);
-        } else if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, H, err)) {
+        } else if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, home_levels, H, err)) {
             return fail(ARROW_E_INVALID_ARG, err);
         }
         const auto t2 = std::chrono::steady_clock::now();
@@ -278,6 +280,7 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         for (int64_t v = 0; v < n; ++v) D->isolated += (A->row_ptr[v + 1] == A->row_ptr[v]) ? 1 : 0;
         D->levels = std::move(H.levels);
         D->homes = H.homes;
+        D->home_levels = H.home_levels;
         D->home_los = std::move(H.home_los);
     } catch (const std::bad_alloc &) {
         D.reset();
@@ -346,8 +349,13 @@ static int validate_decomposition(const arrow_decomposition_s &D, std::string &e
             err = "home ranges";
             return 1;
         }
+        if (D.home_levels < 1) {
+            err = "home_levels";
+            return 1;
+        }
         for (size_t i = 1; i < D.levels.size(); ++i)
-            if (!ranges_ok(D.levels[i].home_start, D.levels[i].head, D.levels[i].n_i)) {
+            if ((int64_t)i <= D.home_levels ? !ranges_ok(D.levels[i].home_start, D.levels[i].head, D.levels[i].n_i)
+                                            : !D.levels[i].home_start.empty()) {
                 err = "level " + std::to_string(i) + ": home starts";
                 return 1;
             }
@@ -596,7 +604,7 @@ arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels,
     if (opt.flags & ~ARROW_FLAGS_ALL) return fail(ARROW_E_INVALID_ARG, "bad options.flags");
     int32_t homes = 1;
     if ((opt.flags & ARROW_FLAG_HOME_AWARE) && comm) homes = comm->nranks;
-    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, homes,
+    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, homes, 1,
                                      (opt.flags & ARROW_FLAG_GPU_DECOMPOSE) != 0, D);
     if (st != ARROW_OK) return st;
     st = plan_from(*D, &opt, A->dtype, comm, out);
@@ -623,7 +631,7 @@ arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, u
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, 1, false, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, 1, 0, false, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
     return ARROW_OK;
@@ -635,35 +643,38 @@ arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, 
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, 1, true, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, 1, 0, true, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
     return ARROW_OK;
 }
 
 arrow_status arrow_decompose_homes(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
-                                   int32_t band, int32_t homes, int32_t device, arrow_decomposition *out) {
+                                   int32_t band, int32_t homes, int32_t home_levels, int32_t device,
+                                   arrow_decomposition *out) {
     g_err.clear();
     if (!out) return fail(ARROW_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (device != 0 && device != 1) return fail(ARROW_E_INVALID_ARG, "device must be 0 (host) or 1 (CUDA)");
     std::unique_ptr<arrow_decomposition_s> D;
-    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, homes, device == 1, D);
+    arrow_status st = decompose_impl(A, b, levels, seed, keep_residual != 0, band, homes, home_levels, device == 1, D);
     if (st != ARROW_OK) return st;
     *out = D.release();
     return ARROW_OK;
 }
 
-arrow_status arrow_decomposition_homes(arrow_decomposition d, int32_t level, int32_t *homes, int64_t *ranges) {
+arrow_status arrow_decomposition_homes(arrow_decomposition d, int32_t level, int32_t *homes, int32_t *home_levels,
+                                       int64_t *ranges) {
     if (!d) return fail(ARROW_E_INVALID_ARG, "decomposition is NULL");
     if (level < -1 || level >= (int32_t)d->levels.size()) return fail(ARROW_E_INVALID_ARG, "level out of range");
     if (homes) *homes = d->homes;
+    if (home_levels) *home_levels = d->home_levels;
     if (ranges && d->homes > 1) {
-        const std::vector<int64_t> *r = nullptr;
-        if (level == -1) r = &d->home_los;
-        else if (level >= 1) r = &d->levels[level].home_start;
-        if (r && r->size() == (size_t)d->homes + 1) std::memcpy(ranges, r->data(), r->size() * 8);
-        else if (level == 0) return fail(ARROW_E_INVALID_ARG, "level 0 has no home starts (use level -1: pi_0 ranges)");
+        const std::vector<int64_t> &r = level == -1 ? d->home_los : d->levels[level].home_start;
+        if (r.size() != (size_t)d->homes + 1)
+            return fail(ARROW_E_INVALID_ARG, "level " + std::to_string(level) + " is not home-aware (levels 1.." +
+                                                 std::to_string(d->home_levels) + " are; -1: pi_0 ranges)");
+        std::memcpy(ranges, r.data(), r.size() * 8);
     }
     return ARROW_OK;
 }
@@ -742,8 +753,8 @@ arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path) {
         ok = ok && std::fwrite(p, 1, n, f) == n;
     };
     w(kMagic, 8);
-    const int64_t hdr[8] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated,
-                            (int64_t)d->band, (int64_t)d->homes};
+    const int64_t hdr[9] = {d->n, d->b, (int64_t)d->seed, (int64_t)d->levels.size(), (int64_t)d->res_u.size(), d->isolated,
+                            (int64_t)d->band, (int64_t)d->homes, (int64_t)d->home_levels};
     w(hdr, sizeof(hdr));
     const bool homes = d->homes > 1 && !d->levels.empty();
     if (homes) w(d->home_los.data(), d->home_los.size() * 8);
@@ -755,7 +766,7 @@ arrow_status arrow_decomposition_save(arrow_decomposition d, const char *path) {
         w(L.row_ptr.data(), L.row_ptr.size() * 8);
         w(L.col.data(), L.col.size() * 4);
         w(L.val.data(), L.val.size() * 8);
-        if (homes && i > 0) w(L.home_start.data(), L.home_start.size() * 8);
+        if (homes && i > 0 && (int64_t)i <= d->home_levels) w(L.home_start.data(), L.home_start.size() * 8);
     }
     w(d->res_u.data(), d->res_u.size() * 4);
     w(d->res_v.data(), d->res_v.size() * 4);
@@ -786,12 +797,13 @@ arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out
         const int ver = !ok ? 0 : std::memcmp(magic, kMagic1, 8) == 0 ? 1 : std::memcmp(magic, kMagic2, 8) == 0 ? 2
                                       : std::memcmp(magic, kMagic, 8) == 0 ? 3 : 0;
         if (!ver) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "not an arrow decomposition file"); }
-        int64_t hdr[8] = {0, 0, 0, 0, 0, 0, 0, 1};
-        r(hdr, (ver == 1 ? 6 : ver == 2 ? 7 : 8) * sizeof(int64_t));
+        int64_t hdr[9] = {0, 0, 0, 0, 0, 0, 0, 1, 0};
+        r(hdr, (ver == 1 ? 6 : ver == 2 ? 7 : 9) * sizeof(int64_t));
         if (!ok || hdr[0] < 0 || hdr[1] < 2 || hdr[3] < 0 || hdr[4] < 0 || hdr[6] < 0 || hdr[6] > 1 || hdr[7] < 1 ||
-            hdr[7] > 8) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
+            hdr[7] > 8 || hdr[8] < 0 || (hdr[7] > 1) != (hdr[8] > 0)) { std::fclose(f); return fail(ARROW_E_INVALID_ARG, "corrupt header"); }
         D->n = hdr[0]; D->b = hdr[1]; D->seed = (uint64_t)hdr[2]; D->isolated = hdr[5]; D->band = (int32_t)hdr[6];
         D->homes = (int32_t)hdr[7];
+        D->home_levels = (int32_t)std::min<int64_t>(hdr[8], 1 << 30);
         D->levels.resize(hdr[3]);
         const bool homes = D->homes > 1 && !D->levels.empty();
         if (homes) {
@@ -808,7 +820,8 @@ arrow_status arrow_decomposition_load(const char *path, arrow_decomposition *out
             r(L.row_ptr.data(), L.row_ptr.size() * 8);
             r(L.col.data(), L.col.size() * 4);
             r(L.val.data(), L.val.size() * 8);
-            if (homes && &L != &D->levels[0]) {
+            const int64_t li = &L - &D->levels[0];
+            if (homes && li > 0 && li <= D->home_levels) {
                 L.home_start.resize(D->homes + 1);
                 r(L.home_start.data(), L.home_start.size() * 8);
             }

@@ -29,13 +29,14 @@ struct HostDecomposition {
     std::vector<HostLevel> levels;
     std::vector<uint32_t> residual;  // entry indices of A left when the level cap is reached
     int homes = 1;                   // G of the home-set-aware arrangement (R25); 1 = R11
+    int home_levels = 0;             // levels 1..home_levels are home-aware (homes > 1)
     std::vector<int64_t> home_los;   // [homes + 1] pi_0 home ranges (homes > 1)
 };
 
-// LA-Decompose (decompose.cpp).  homes > 1: home-set-aware levels >= 1 (R25).  Returns 0 on
-// success, else sets `err`.
+// LA-Decompose (decompose.cpp).  homes > 1: levels 1..home_levels home-set-aware (R25).  Returns 0
+// on success, else sets `err`.
 int la_decompose(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
-                 uint64_t seed, int band, int homes, HostDecomposition &out, std::string &err);
+                 uint64_t seed, int band, int homes, int home_levels, HostDecomposition &out, std::string &err);
 
 // R25: tile boundaries of a G-way split of prefix costs pre[0..T] (each boundary the
 // prefix nearest g/G of the total, ties to the upper one, never before the previous) -> tb[0..G]
@@ -48,7 +49,8 @@ std::vector<int64_t> home_ranges(const HostLevel &L0, int64_t n, int64_t b, int 
 // la_decompose, bit for bit (same rules and keys; Boruvka + Euler-tour list ranking in place of the
 // sequential Kruskal / BFS / DFS).  n < 2^31 - 1, nnz < 2^32 - 1.  0 on success, else sets `err`.
 int la_decompose_gpu(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
-                     uint64_t seed, int band, int homes, HostDecomposition &out, std::string &err);
+                     uint64_t seed, int band, int homes, int home_levels, HostDecomposition &out,
+                     std::string &err);
 
 // Validation helpers (decompose.cpp): 0 ok, 1 bad CSR, 2 not symmetric.
 int validate_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, std::string &err);

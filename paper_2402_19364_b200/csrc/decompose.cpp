@@ -17,8 +17,8 @@
 // homes = G > 1 (R25): after level 0 every vertex gets the home range of its
 // pi_0 position (home_ranges: level-0 tile work plus remainder degrees, split G ways); the forest
 // of every level >= 1 takes only edges inside one home and its trees are laid out by (home of the
-// root, size desc, min id asc), so that rank g's level-i tiles hold rows whose X and Y live on
-// rank g (edges between homes wait for a later level or a head).
+// root, size desc, min id asc) for the levels 1..home_levels, so that rank g's level-i tiles hold
+// rows whose X and Y live on rank g (edges between homes wait for a later level or a head).
 //
 // Parallel where the work is bulk (degree histograms, edge keys, the edge sort, extraction,
 // CSR assembly); union-find and the tree layouts are sequential.
@@ -165,12 +165,13 @@ std::vector<int64_t> home_ranges(const HostLevel &L0, int64_t n, int64_t b, int 
 }
 
 int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, int32_t max_levels,
-                 uint64_t seed, int band, int homes, HostDecomposition &out, std::string &err) {
+                 uint64_t seed, int band, int homes, int home_levels, HostDecomposition &out, std::string &err) {
     out = HostDecomposition{};
     out.n = n;
     out.b = b;
     out.band = band;
     out.homes = homes;
+    out.home_levels = homes > 1 ? home_levels : 0;
     std::vector<uint8_t> home;  // homes > 1: home of every vertex (after level 0)
     const int64_t nnz = rp[n];
     if (nnz == 0) return 0;
@@ -217,6 +218,7 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
         std::fill(in_head.begin(), in_head.end(), 0);
         for (int32_t v : H) in_head[v] = 1;
 
+        const bool aware = !home.empty() && i <= home_levels;  // R25 at this level
         // ---- step 2a: G'_i edges with their random keys (R9)
         const uint64_t s_i = mix64(seed + (uint64_t)i);
         std::vector<uint32_t> gent, dummy;
@@ -224,7 +226,7 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
             ent,
             [&](uint32_t e) {
                 const int32_t u = erow[e], v = col[e];
-                return u < v && !in_head[u] && !in_head[v] && (home.empty() || home[u] == home[v]);
+                return u < v && !in_head[u] && !in_head[v] && (!aware || home[u] == home[v]);
             },
             gent, dummy);
         dummy.clear();
@@ -317,7 +319,7 @@ int la_decompose(int64_t n, const int64_t *rp, const int32_t *col, int64_t b, in
         }
         if (fpos + h != n_i) { err = "internal: forest layout does not cover V_i"; return 1; }
         HostLevel L;
-        if (home.empty()) {
+        if (!aware) {
             std::stable_sort(trees.begin(), trees.end(), [](const Tree &a, const Tree &c) {
                 return a.size != c.size ? a.size > c.size : a.root < c.root;
             });

@@ -292,16 +292,20 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
         DistHostLevel &DL = H.L[i];
         DL.h = L.head;
         if (i == 0) continue;
-        if (aware) {
+        if (aware && (int)L.home_start.size() == G + 1) {
             // R25: rank g takes the tiles of home g's trees (boundaries at the nearest tile edge)
-            const int64_t T = (L.n_i + b - 1) / b;
+            const std::vector<int64_t> cost = tile_costs(L, b);
+            const int64_t T = (int64_t)cost.size();
             tbs[i].assign(G + 1, T);
             tbs[i][0] = 0;
             for (int g = 1; g < G; ++g)
                 tbs[i][g] = std::min(std::max((L.home_start[g] + b / 2) / b, tbs[i][g - 1]), T);
             rk[i].resize(G);
             cr[i].resize(G);
-            for (int g = 0; g < G; ++g) rk[i][g] = cr[i][g] = g;
+            for (int g = 0; g < G; ++g) {
+                rk[i][g] = cr[i][g] = g;
+                for (int64_t t = tbs[i][g]; t < tbs[i][g + 1]; ++t) load[g] += cost[t];
+            }
         } else {
             const std::vector<int64_t> cost = tile_costs(L, b);
             tbs[i] = split_tiles(cost, G);

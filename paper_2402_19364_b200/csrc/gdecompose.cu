@@ -399,12 +399,13 @@ struct Cub {
 }  // namespace
 
 int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t b, int32_t max_levels, uint64_t seed,
-                     int band, int homes, HostDecomposition &out, std::string &err) {
+                     int band, int homes, int home_levels, HostDecomposition &out, std::string &err) {
     out = HostDecomposition{};
     out.n = n;
     out.b = b;
     out.band = band;
     out.homes = homes;
+    out.home_levels = homes > 1 ? home_levels : 0;
     const int64_t nnz = rp[n];
     if (nnz == 0) return 0;
     if (n >= ((int64_t)1 << 31) - 1 || nnz >= ((int64_t)1 << 32) - 1) {
@@ -502,11 +503,12 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
         GD_TRY(d_head.need(std::max<int64_t>(h, 1)));
         k_mark_head<<<blocks_for(h), 256>>>(d_key.p, h, d_inhead.p, d_head.p);
         tr.mark(1);
+        const bool aware = i > 0 && homes > 1 && i <= home_levels;  // R25 at this level
         // ---- step 2: G'_i edges with their keys
         GD_TRY(d_flag.need(m));
         GD_TRY(d_gent.need(m));
         k_gprime_flags<<<blocks_for(m), 256>>>(d_ent.p, m, d_erow.p, d_col.p, d_inhead.p,
-                                               (i > 0 && homes > 1) ? d_home.p : nullptr, d_flag.p);
+                                               aware ? d_home.p : nullptr, d_flag.p);
         GD_TRY(cub.run([&](void *t, size_t &s) {
             return cub::DeviceSelect::Flagged(t, s, d_ent.p, d_flag.p, d_gent.p, d_cnt.p, (int)m);
         }));
@@ -609,7 +611,7 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
             }));
         }
         std::vector<int64_t> home_start;
-        if (i > 0 && homes > 1) {  // R25: stable re-sort by the home of the root, home starts
+        if (aware) {  // R25: stable re-sort by the home of the root, home starts
             GD_TRY(hk.need(std::max<int64_t>(nt, 1)));
             GD_TRY(hk2.need(std::max<int64_t>(nt, 1)));
             GD_TRY(troot2.need(std::max<int64_t>(nt, 1)));

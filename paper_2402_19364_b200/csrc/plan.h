@@ -124,6 +124,7 @@ struct arrow_decomposition_s {
     uint64_t seed = 4;
     int32_t band = 0;                    // ARROW_BAND_* of step 3
     int32_t homes = 1;                   // home-set-aware arrangement for this many ranks (R25); 1 = off
+    int32_t home_levels = 0;             // levels 1..home_levels home-aware (homes > 1)
     std::vector<int64_t> home_los;       // [homes + 1] pi_0 home ranges (homes > 1)
     int64_t isolated = 0;
     std::vector<HostLevel> levels;

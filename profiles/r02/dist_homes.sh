@@ -7,7 +7,7 @@ N=$(nvidia-smi -L | wc -l)
 python -c "import paper_2402_19364_b200 as ab; ab.lib()" > $OUT/build.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_decompose.py -q -x -p no:cacheprovider > $OUT/pytest_gd.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gd.log
 timeout 1500 python -m pytest tests/test_gpu_dist.py -q -p no:cacheprovider > $OUT/pytest_dist.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_dist.log
-tail -2 $OUT/pytest_gd.log $OUT/pytest_dist.log
+tail -n 2 $OUT/pytest_gd.log $OUT/pytest_dist.log
 run() {  # name, bench args
   local name=$1; shift
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29555 \
@@ -26,9 +26,9 @@ trace() {  # name, bench args: a short run with the per-phase trace (host-synchr
   grep "arrow dist rank" $OUT/trace_n${N}_$name.err | tail -$N
 }
 run k128 --k 128
-run k128_homes --k 128 --home-aware --gpu-decompose
+run k128_hl1 --k 128 --home-aware --home-levels 1 --gpu-decompose
+run k128_hl2 --k 128 --home-aware --home-levels 2 --gpu-decompose
 run k32 --k 32
-run k32_homes --k 32 --home-aware --gpu-decompose
-run k128_homes_strict --k 128 --home-aware --band strict --gpu-decompose
+run k32_hl1 --k 32 --home-aware --home-levels 1 --gpu-decompose
 trace k128 --k 128
-trace k128_homes --k 128 --home-aware --gpu-decompose
+trace k128_hl1 --k 128 --home-aware --home-levels 1 --gpu-decompose

@@ -65,15 +65,15 @@ def test_gpu_decomposer_seeds(seed):
 
 @pytest.mark.parametrize("spec,b", [("RMAT(12,8,1)", 64), ("GRID(100,1)", 32), ("RMAT(14,8,2)", 256), ("PATH(500,1)", 8)])
 @pytest.mark.parametrize("homes", [2, 3, 4, 8])
-@pytest.mark.parametrize("band", ["block", "strict"])
-def test_gpu_decomposer_homes(spec, b, homes, band):
+@pytest.mark.parametrize("band,hl", [("block", 1), ("strict", 1), ("block", 3)])
+def test_gpu_decomposer_homes(spec, b, homes, band, hl):
     """R25 (home-set-aware levels >= 1) on the GPU: the same decomposition, home ranges and starts."""
     g = datagen.make_graph(spec)
-    Dh = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band, homes=homes)
-    Dg = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band, homes=homes, device="cuda")
+    Dh = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band, homes=homes, home_levels=hl)
+    Dg = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b, band=band, homes=homes, home_levels=hl, device="cuda")
     _same(Dg, Dh)
-    assert np.array_equal(Dg.homes(-1)[1], Dh.homes(-1)[1])
-    for i in range(1, Dh.info()["levels"]):
+    assert np.array_equal(Dg.homes(-1)[1], Dh.homes(-1)[1]) and Dg.home_levels() == hl
+    for i in range(1, min(hl, Dh.info()["levels"] - 1) + 1):
         assert np.array_equal(Dg.homes(i)[1], Dh.homes(i)[1])
 
 
