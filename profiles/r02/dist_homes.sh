@@ -28,6 +28,8 @@ trace() {  # name, bench args: a short run with the per-phase trace (host-synchr
 run k128 --k 128
 run k128_hl1 --k 128 --home-aware --home-levels 1 --gpu-decompose
 run k128_hl2 --k 128 --home-aware --home-levels 2 --gpu-decompose
+run k128_nccl --k 128 --transport nccl
+run k128_strict --k 128 --band strict
 run k32 --k 32
 run k32_hl1 --k 32 --home-aware --home-levels 1 --gpu-decompose
 trace k128 --k 128
