@@ -324,10 +324,12 @@ def main():
     ap.add_argument("--head-chunk", type=int, default=0)
     ap.add_argument("--batch-segments", type=int, default=0)
     ap.add_argument("--flags", type=int, default=0, help="arrow_options.flags (ARROW_FLAG_*)")
-    ap.add_argument("--home-aware", action="store_true",
-                    help="N > 1: decompose with home-set-aware levels >= 1 for the N ranks (R25)")
-    ap.add_argument("--home-levels", type=int, default=1, help="--home-aware: levels 1..L use same-home forests")
-    ap.add_argument("--gpu-decompose", action="store_true", help="N > 1: rank 0 decomposes on its GPU")
+    ap.add_argument("--home-aware", action=argparse.BooleanOptionalAction, default=True,
+                    help="N > 1: decompose with home-set-aware levels >= 1 for the N ranks (R25; default on)")
+    ap.add_argument("--home-levels", type=int, default=0,
+                    help="--home-aware: levels 1..L use same-home forests (0 = the library default for N ranks)")
+    ap.add_argument("--gpu-decompose", action=argparse.BooleanOptionalAction, default=True,
+                    help="N > 1: rank 0 decomposes on its GPU (default on)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -359,8 +361,8 @@ def main():
     dec = None
     decompose_s = [None]
     if world > 1:
-        # one host decomposition for the node: rank 0 computes and checkpoints it, the others load it
-        # (arrow_decomposition_save/load), instead of G processes decomposing the same A at once
+        # one decomposition for the node (on rank 0's GPU by default, home-aware for the N ranks): rank 0
+        # computes and checkpoints it, the others load it (arrow_decomposition_save/load)
         import tempfile
         path = [os.path.join(tempfile.mkdtemp(prefix="arrow_bench_"), "A.dec") if rank == 0 else None]
         dist.broadcast_object_list(path, src=0)
@@ -378,6 +380,7 @@ def main():
         if rank == 0:
             os.remove(path[0])
             os.rmdir(os.path.dirname(path[0]))
+    home_levels_used = dec.home_levels() if dec is not None else 0
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
                    window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
@@ -552,7 +555,7 @@ def main():
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
                        "band": args.band,
-                       "arrangement": ("home-aware (R25) for %d ranks, levels 1..%d" % (world, args.home_levels))
+                       "arrangement": ("home-aware (R25) for %d ranks, levels 1..%d" % (world, home_levels_used))
                                       if (args.home_aware and world > 1)
                                       else "random spanning forest, smallest-first (R6-R12)",
                        "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",

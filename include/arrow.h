@@ -90,7 +90,9 @@ typedef struct {
     int32_t band;               /* ARROW_BAND_*: step 3's band; default BLOCK */
     int32_t flags;              /* ARROW_FLAG_* bits; default 0 */
     int32_t transport;          /* ARROW_TRANSPORT_* (distributed plans); default AUTO */
-    int32_t reserved[3];
+    int32_t home_levels;        /* ARROW_FLAG_HOME_AWARE: levels 1..home_levels home-set-aware; 0 = default
+                                   (1 for 2 ranks, 3 for more; measured) */
+    int32_t reserved[2];
 } arrow_options;
 
 /* options.flags */
@@ -103,7 +105,8 @@ enum { ARROW_FLAG_NO_GRAPHS = 1,       /* single GPU: launch the kernels of each
        ARROW_FLAG_GPU_DECOMPOSE = 4,   /* arrow_plan_create_ex: run LA-Decompose on the current CUDA device
                                           (arrow_decompose_gpu) instead of the host; same decomposition */
        ARROW_FLAG_HOME_AWARE = 8,      /* arrow_plan_create_ex with a comm: home-set-aware arrangement for the
-                                          comm's ranks (arrow_decompose_homes, homes = nranks, home_levels = 1) */
+                                          comm's ranks (arrow_decompose_homes, homes = nranks, home_levels =
+                                          options.home_levels) */
        ARROW_FLAGS_ALL = 15 };
 /* options.transport (distributed plans): AUTO = P2P when every peer's memory can be mapped (CUDA IPC
  * over NVLink), else NCCL; P2P fails with ARROW_E_UNSUPPORTED if a peer cannot be mapped. */
@@ -274,7 +277,8 @@ arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, 
  * 1..home_levels (>= 1; their forests use only the edges inside one home), so a distributed plan for G
  * ranks computes those levels' home-g trees on rank g and moves few of their rows over NVLink; edges
  * between homes wait for a later level, so more home-aware levels mean more levels and rows
- * (DESIGN.md §8.2 measures the trade).  homes = 1 is arrow_decompose_ex (home_levels ignored).  device: 0 = host, 1 = the current CUDA device (as
+ * (DESIGN.md §8 measures the trade); home_levels = 0 picks the default (1 for homes = 2, else 3).
+ * homes = 1 is arrow_decompose_ex (home_levels ignored).  device: 0 = host, 1 = the current CUDA device (as
  * arrow_decompose_gpu; the same decomposition).  Errors as arrow_decompose_ex / _gpu; homes outside
  * [1, 8] or device not 0/1 -> ARROW_E_INVALID_ARG.  Saved files (format 3) record the homes. */
 arrow_status arrow_decompose_homes(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,

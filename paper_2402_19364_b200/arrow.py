@@ -58,7 +58,7 @@ class Options(ctypes.Structure):
     _fields_ = [("compute", ctypes.c_int), ("seed", ctypes.c_uint64), ("order", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("window_rows", ctypes.c_int64), ("head_chunk", ctypes.c_int32),
                 ("batch_segments", ctypes.c_int32), ("band", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("transport", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("transport", ctypes.c_int32), ("home_levels", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -171,7 +171,7 @@ def _dtype_code(dtype) -> int:
 
 def options(dtype=None, seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
             head_chunk: int = 0, batch_segments: int = 0, band: str = "block", flags: int = 0,
-            transport: str = "auto") -> Options:
+            transport: str = "auto", home_levels: int = 0) -> Options:
     o = Options()
     _check(lib().arrow_options_default(ctypes.byref(o)), "arrow_options_default")
     o.compute = _dtype_code(dtype)
@@ -184,6 +184,7 @@ def options(dtype=None, seed: int = 4, order: str = "original", residual: str = 
     o.band = BAND[band]
     o.flags = flags
     o.transport = TRANSPORT[transport]
+    o.home_levels = home_levels
     return o
 
 
@@ -206,7 +207,7 @@ class Decomposition:
     a G-rank plan (arrow_decompose_homes, reading R25)."""
 
     def __init__(self, n, row_ptr, col, val, b: int, levels: int = 0, seed: int = 4, keep_residual: bool = False,
-                 band: str = "block", device: str = "cpu", homes: int = 1, home_levels: int = 1, _handle=None):
+                 band: str = "block", device: str = "cpu", homes: int = 1, home_levels: int = 0, _handle=None):
         self._h = ctypes.c_void_p()
         if _handle is not None:
             self._h = _handle
@@ -329,9 +330,10 @@ class Plan:
                  seed: int = 4, order: str = "original", residual: str = "error", window_rows: int = 0,
                  head_chunk: int = 0, batch_segments: int = 0, comm=None,
                  decomposition: Optional[Decomposition] = None, band: str = "block", flags: int = 0,
-                 transport: str = "auto"):
+                 transport: str = "auto", home_levels: int = 0):
         self._h = ctypes.c_void_p()
-        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments, band, flags, transport)
+        opt = options(dtype, seed, order, residual, window_rows, head_chunk, batch_segments, band, flags, transport,
+                      home_levels)
         comm_h = comm.handle if comm is not None else None
         if decomposition is not None:
             _check(lib().arrow_plan_create_from(decomposition._h, ctypes.byref(opt), comm_h, ctypes.byref(self._h)),

@@ -229,7 +229,8 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
     if (st != ARROW_OK) return st;
     if (band != ARROW_BAND_BLOCK && band != ARROW_BAND_STRICT) return fail(ARROW_E_INVALID_ARG, "bad band");
     if (homes < 1 || homes > 8) return fail(ARROW_E_INVALID_ARG, "homes must be in [1, 8]");
-    if (homes > 1 && home_levels < 1) return fail(ARROW_E_INVALID_ARG, "home_levels must be >= 1");
+    if (home_levels < 0) return fail(ARROW_E_INVALID_ARG, "home_levels must be >= 0 (0 = default)");
+    if (homes > 1 && home_levels == 0) home_levels = default_home_levels(homes);
     std::string err;
     const int64_t n = A->n;
     if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
@@ -604,8 +605,8 @@ arrow_status arrow_plan_create_ex(const arrow_csr *A, int64_t b, int32_t levels,
     if (opt.flags & ~ARROW_FLAGS_ALL) return fail(ARROW_E_INVALID_ARG, "bad options.flags");
     int32_t homes = 1;
     if ((opt.flags & ARROW_FLAG_HOME_AWARE) && comm) homes = comm->nranks;
-    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, homes, 1,
-                                     (opt.flags & ARROW_FLAG_GPU_DECOMPOSE) != 0, D);
+    arrow_status st = decompose_impl(A, b, levels, opt.seed, opt.residual == ARROW_RESIDUAL_CSR, opt.band, homes,
+                                     opt.home_levels, (opt.flags & ARROW_FLAG_GPU_DECOMPOSE) != 0, D);
     if (st != ARROW_OK) return st;
     st = plan_from(*D, &opt, A->dtype, comm, out);
     if (st == ARROW_OK) (*out)->create_seconds += D->seconds;

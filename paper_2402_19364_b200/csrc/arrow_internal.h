@@ -69,6 +69,9 @@ constexpr uint32_t kPseudoRec = 0x80000000u;
 constexpr uint32_t kFlag = 0x80000000u;
 constexpr uint32_t kAuxRec = 0x40000000u;
 constexpr int64_t kMaxRows = (int64_t)1 << 30;
+// default home-aware levels (R25) for G homes, measured at config R: at G = 2 the
+// halo already hides under level 0, so one level; from G = 4 on three levels
+inline int default_home_levels(int homes) { return homes <= 2 ? 1 : 3; }
 constexpr int kDefaultBatchSegs = 16;  // segments per K-A work batch of full-warp rows (measured: 16 > 32)
 
 // metadata of one level (introspection) and its level-0 zero-row list

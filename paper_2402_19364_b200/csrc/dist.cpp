@@ -935,20 +935,21 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     Marks M;
     M.on = P->profiling || trace;
 
-    // S: the previous call (and the caller's writes of X) precede everything.  My head rows go into
-    // every rank's D0 first (level 0 needs only them), then C0 = 0 and the zero rows; the rows for
-    // the peers are packed, and C moves one chunk per peer with the copy engines while the SMs run
-    // level 0.
+    // S: the previous call (and the caller's writes of X) precede everything (C waits for S's start).
     const int m0 = M(st);
+    DCUDA(cudaEventRecord(S->ev[2], st));  // call start: the previous call and the caller's writes of X
+    DCUDA(cudaStreamWaitEvent(S->cs, S->ev[2], 0));
+    // S: only what level 0 needs from the peers goes first -- my head rows (and strict-band H0 rows)
+    // into every rank's D0; the counters and this call's C0
     DK(launch_push_rows(dt, X, S->d0push_src, S->d0push_dst, S->n_d0push, k, S->ws_peer, 0, st));
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(c0), 0, (size_t)S->d0_rows * k * es, st));
-    DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, st));
-    DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, st));
     const int m0p = M(st);
-    DCUDA(cudaEventRecord(S->ev[0], st));
-    DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
+    // C: the zero rows (read-modify-written by levels >= 1 at the earliest) and the packing of the rows
+    // for my peers run next to level 0; then the copy engines move one chunk per peer
     const int m0c = M(S->cs);
+    DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, S->cs));
+    DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, S->cs));
     {
         DCUDA(cudaEventRecord(S->ev[5], S->cs));
         for (int g = 0, q = 0; g < G; ++g) {
@@ -991,8 +992,8 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     const int m6 = M(st);
     if (trace) {
         cudaEventSynchronize(M.ev[m6]);
-        std::string line = "[arrow dist rank " + std::to_string(me) + " p2p] ms: halo " +
-                           std::string("D0+zero+pack " + M.el(m0, m0p) + " dma ") + M.el(m0c, m1c) +
+        std::string line = "[arrow dist rank " + std::to_string(me) + " p2p] ms: D0 " + M.el(m0, m0p) +
+                           " | halo zero+pack+dma " + M.el(m0c, m1c) +
                            " + barrier " + M.el(m1c, m2c) + " (done at " + M.el(m0, m2c) + ") | barrier0 " +
                            M.el(m0p, m1) + " | K-A L0 " + M.el(m1, m2) + " | wait " + M.el(m2, m3) + " | K-A L>=1 " +
                            M.el(m3, m4) + " | barrier " + M.el(m4, m5) + " | gather-add " + M.el(m5, m6) +

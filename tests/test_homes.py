@@ -176,10 +176,13 @@ def test_homes_save_load_and_errors(tmp_path):
     with pytest.raises(ArrowError):
         E.homes(3)
     with pytest.raises(ArrowError):
-        ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 16, homes=4, home_levels=0)
+        ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 16, homes=4, home_levels=-1)
     with pytest.raises(ArrowError):
         ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 16, homes=9)
     assert ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 16).homes() == (1, None)
+    # home_levels = 0: the library default (1 level for 2 homes, 3 for more)
+    assert ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 16, homes=2).home_levels() == 1
+    assert ab.Decomposition(g.n, g.row_ptr, g.col, g.val, 16, homes=4).home_levels() == 3
 
 
 def test_home_aware_moves_fewer_rows():
