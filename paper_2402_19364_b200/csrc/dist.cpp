@@ -75,6 +75,7 @@ struct DistHost {
     int64_t zero_tail_lo = 0, zero_tail_n = 0;  // local Y rows of the A-isolated tail (written as 0)
     std::vector<int64_t> halo_all, stage_all;           // per rank
     std::vector<int32_t> d0push_src, d0push_dst;        // my heads -> every rank's D0
+    int64_t n_d0push_l0 = 0;                            // the first n_d0push_l0 pushes: what level 0 reads
     std::vector<int32_t> pack_src, pack_dst;            // my X rows -> my send chunks / my own halo (DMA)
     std::vector<int64_t> send_row, halo_dst_row;        // per peer: my send chunk, its place in the peer's halo
     int64_t send_rows = 0;
@@ -109,7 +110,7 @@ struct DistState {
     int64_t n_pre = 0;
     // P2P: pushes of my head rows into every D0 and of my X rows into every halo (encoded rows)
     int32_t *d0push_src = nullptr, *d0push_dst = nullptr;
-    int64_t n_d0push = 0;
+    int64_t n_d0push = 0, n_d0push_l0 = 0;
     // P2P halo: X rows packed per peer, then one copy-engine transfer per peer into its halo
     int32_t *pack_src = nullptr, *pack_dst = nullptr;
     int64_t n_pack = 0;
@@ -557,6 +558,7 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
                                                                        (uint32_t)(H.d0_rows + H.d0_index[i][j])));
                 }
         }
+        if (i == 0) H.n_d0push_l0 = (int64_t)H.d0push_src.size();  // strict-band H0 rows + level 0's heads
         if (i == 0) {  // level 0: entry-less body rows of my home range; the A-isolated tail is a range
             for (int64_t p = std::max(lo, h); p < std::min(hi, L.n_i); ++p)
                 if (L.row_ptr[p + 1] == L.row_ptr[p]) DL.zero_rows.push_back((int32_t)(p - lo));
@@ -833,6 +835,7 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     S->pre_src = upload(S, pre_src, ok);
     S->pre_dst = upload(S, pre_dst, ok);
     S->n_d0push = (int64_t)H.d0push_src.size();
+    S->n_d0push_l0 = H.n_d0push_l0;
     S->d0push_src = upload(S, H.d0push_src, ok);
     S->d0push_dst = upload(S, H.d0push_dst, ok);
     S->n_pack = (int64_t)H.pack_src.size();
@@ -939,15 +942,18 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     const int m0 = M(st);
     DCUDA(cudaEventRecord(S->ev[2], st));  // call start: the previous call and the caller's writes of X
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[2], 0));
-    // S: only what level 0 needs from the peers goes first -- my head rows (and strict-band H0 rows)
-    // into every rank's D0; the counters and this call's C0
-    DK(launch_push_rows(dt, X, S->d0push_src, S->d0push_dst, S->n_d0push, k, S->ws_peer, 0, st));
+    // S: only what level 0 needs from the peers goes first -- my level-0 head rows (and strict-band H0
+    // rows) into every rank's D0; the counters and this call's C0
+    DK(launch_push_rows(dt, X, S->d0push_src, S->d0push_dst, S->n_d0push_l0, k, S->ws_peer, 0, st));
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(c0), 0, (size_t)S->d0_rows * k * es, st));
     const int m0p = M(st);
     // C: the zero rows (read-modify-written by levels >= 1 at the earliest) and the packing of the rows
     // for my peers run next to level 0; then the copy engines move one chunk per peer
     const int m0c = M(S->cs);
+    // the head rows of levels >= 1 (read after barrier slot 1, like the halos)
+    DK(launch_push_rows(dt, X, S->d0push_src + S->n_d0push_l0, S->d0push_dst + S->n_d0push_l0,
+                        S->n_d0push - S->n_d0push_l0, k, S->ws_peer, 0, S->cs));
     DK(launch_zero_rows(dt, S->zero_rows, S->n_zero, k, Y, S->cs));
     DK(launch_rows(dt, X, S->pack_src, S->pack_dst, S->n_pack, k, 0, ws, S->cs));
     {
