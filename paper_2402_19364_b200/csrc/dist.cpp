@@ -52,10 +52,10 @@ struct DistHostLevel {
 
 struct DistHost {
     int G = 1, me = 0;
-    // D0 / C0 row of head j of level i: owner-major (level 0's heads first, then the heads of levels
-    // >= 1, each block ordered by owning rank), so Alg. 1's broadcast of D^(0) and reduction of C^(0)
-    // are one ncclBroadcast / ncclReduce per owner (rows [blk[r], blk[r+1]) of a block), and with the
-    // P2P transport my heads of levels >= 1 are one contiguous block that the copy engines send
+    // D0 / C0 row of head j of level i: NCCL transport = owner-major (level 0's heads first, then the
+    // heads of levels >= 1, each block ordered by owning rank), so Alg. 1's broadcast of D^(0) and
+    // reduction of C^(0) are one ncclBroadcast / ncclReduce per owner (rows [blk[r], blk[r+1]) of a
+    // block); P2P transport = level-major (d0_off[i] + j)
     std::vector<std::vector<int32_t>> d0_index;
     std::vector<int64_t> blk0, blk1;  // [G + 1] owner ranges of the level-0 block / levels >= 1 block
     int64_t lo = 0, hi = 0;
@@ -74,7 +74,7 @@ struct DistHost {
     int64_t d0_rows = 0;
     int64_t zero_tail_lo = 0, zero_tail_n = 0;  // local Y rows of the A-isolated tail (written as 0)
     std::vector<int64_t> halo_all, stage_all;           // per rank
-    std::vector<int32_t> d0push_src, d0push_dst;        // my level-0 heads (+ strict-band H0 rows) -> every rank
+    std::vector<int32_t> d0push_src, d0push_dst;        // my heads -> every rank's D0
     std::vector<int32_t> pack_src, pack_dst;            // my X rows -> my send chunks / my own halo (DMA)
     std::vector<int64_t> send_row, halo_dst_row;        // per peer: my send chunk, its place in the peer's halo
     int64_t send_rows = 0;
@@ -110,7 +110,6 @@ struct DistState {
     // P2P: pushes of my head rows into every D0 and of my X rows into every halo (encoded rows)
     int32_t *d0push_src = nullptr, *d0push_dst = nullptr;
     int64_t n_d0push = 0;
-    int64_t d0blk_row = 0, d0blk_rows = 0;  // P2P: my heads of levels >= 1 (sent to every peer's D0)
     // P2P halo: X rows packed per peer, then one copy-engine transfer per peer into its halo
     int32_t *pack_src = nullptr, *pack_dst = nullptr;
     int64_t n_pack = 0;
@@ -417,7 +416,13 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
     H.blk1.assign(G + 1, 0);
     {
         int64_t off = 0;
-        {
+        if (p2p) {
+            for (int i = 0; i < nl; ++i) {
+                H.d0_index[i].resize(D.levels[i].head);
+                for (int64_t j = 0; j < D.levels[i].head; ++j) H.d0_index[i][j] = (int32_t)(off + j);
+                off += D.levels[i].head;
+            }
+        } else {
             // two blocks (level 0 | levels >= 1), each owner-major; heads keep level, then j order
             for (int blk = 0; blk < 2; ++blk) {
                 std::vector<int64_t> &bnd = blk == 0 ? H.blk0 : H.blk1;
@@ -544,20 +549,13 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             if (owner(P0) != me) continue;
             DL.head_j.push_back((int32_t)j);
             DL.head_row.push_back((int32_t)(P0 - lo));
-            if (p2p) {
-                if (i > 0) {  // levels >= 1: into my own D0 block, which the copy engines send to every peer
-                    H.pack_src.push_back((int32_t)(P0 - lo));
-                    H.pack_dst.push_back(H.d0_index[i][j]);
-                }
+            if (p2p)
                 for (int t = 0; t < G; ++t) {
-                    if (i == 0) {  // level 0: pushed into every rank's D0 before level 0 runs
-                        H.d0push_src.push_back((int32_t)(P0 - lo));
-                        H.d0push_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)H.d0_index[i][j]));
-                    }
+                    H.d0push_src.push_back((int32_t)(P0 - lo));
+                    H.d0push_dst.push_back((int32_t)(((uint32_t)t << kPeerShift) | (uint32_t)H.d0_index[i][j]));
                     H.post.emplace_back((int32_t)(P0 - lo), (int32_t)(((uint32_t)t << kPeerShift) | kParityBit |
                                                                        (uint32_t)(H.d0_rows + H.d0_index[i][j])));
                 }
-            }
         }
         if (i == 0) {  // level 0: entry-less body rows of my home range; the A-isolated tail is a range
             for (int64_t p = std::max(lo, h); p < std::min(hi, L.n_i); ++p)
@@ -835,8 +833,6 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     S->pre_src = upload(S, pre_src, ok);
     S->pre_dst = upload(S, pre_dst, ok);
     S->n_d0push = (int64_t)H.d0push_src.size();
-    S->d0blk_row = H.blk0[G] + H.blk1[me];
-    S->d0blk_rows = H.blk1[me + 1] - H.blk1[me];
     S->d0push_src = upload(S, H.d0push_src, ok);
     S->d0push_dst = upload(S, H.d0push_dst, ok);
     S->n_pack = (int64_t)H.pack_src.size();
@@ -939,11 +935,11 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     Marks M;
     M.on = P->profiling || trace;
 
-    // S: the previous call (and the caller's writes of X) precede everything.
+    // S: the previous call (and the caller's writes of X) precede everything.  My head rows go into
+    // every rank's D0 first (level 0 needs only them), then C0 = 0 and the zero rows; the rows for
+    // the peers are packed, and C moves one chunk per peer with the copy engines while the SMs run
+    // level 0.
     const int m0 = M(st);
-    // S: what level 0 needs from the peers first -- my level-0 head rows (and strict-band H0 rows) into
-    // every rank's D0; the counters, this call's C0, the zero rows; then the packing of the X rows my
-    // peers need and of my heads of levels >= 1 (into my own D0 block)
     DK(launch_push_rows(dt, X, S->d0push_src, S->d0push_dst, S->n_d0push, k, S->ws_peer, 0, st));
     DCUDA(cudaMemsetAsync(S->counters, 0, (nl + 1) * sizeof(unsigned), st));
     DCUDA(cudaMemsetAsync(row(c0), 0, (size_t)S->d0_rows * k * es, st));
@@ -952,7 +948,6 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     const int m0p = M(st);
     DCUDA(cudaEventRecord(S->ev[0], st));
     DCUDA(cudaStreamWaitEvent(S->cs, S->ev[0], 0));
-    // C: the copy engines move, per peer, its halo chunk and my D0 block while the SMs run level 0
     const int m0c = M(S->cs);
     {
         DCUDA(cudaEventRecord(S->ev[5], S->cs));
@@ -960,9 +955,6 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
             if (g == me) continue;
             cudaStream_t d = S->ds[q];
             DCUDA(cudaStreamWaitEvent(d, S->ev[5], 0));
-            if (S->d0blk_rows)
-                DCUDA(cudaMemcpyAsync(reinterpret_cast<char *>(S->ws_peer.p[g]) + (size_t)S->d0blk_row * k * es,
-                                      row(S->d0blk_row), (size_t)S->d0blk_rows * k * es, cudaMemcpyDeviceToDevice, d));
             if (S->send_peer[g])
                 DCUDA(cudaMemcpyAsync(reinterpret_cast<char *>(S->ws_peer.p[g]) + (size_t)S->halo_dst_row[g] * k * es,
                                       row(S->send_row[g]), (size_t)S->send_peer[g] * k * es, cudaMemcpyDeviceToDevice,
@@ -999,8 +991,8 @@ arrow_status dist_spmm_p2p(arrow_plan P, DistState *S, const void *X, void *Y, i
     const int m6 = M(st);
     if (trace) {
         cudaEventSynchronize(M.ev[m6]);
-        std::string line = "[arrow dist rank " + std::to_string(me) + " p2p] ms: D0+zero+pack " + M.el(m0, m0p) +
-                           " | dma " + M.el(m0c, m1c) +
+        std::string line = "[arrow dist rank " + std::to_string(me) + " p2p] ms: halo " +
+                           std::string("D0+zero+pack " + M.el(m0, m0p) + " dma ") + M.el(m0c, m1c) +
                            " + barrier " + M.el(m1c, m2c) + " (done at " + M.el(m0, m2c) + ") | barrier0 " +
                            M.el(m0p, m1) + " | K-A L0 " + M.el(m1, m2) + " | wait " + M.el(m2, m3) + " | K-A L>=1 " +
                            M.el(m3, m4) + " | barrier " + M.el(m4, m5) + " | gather-add " + M.el(m5, m6) +
