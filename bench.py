@@ -329,7 +329,7 @@ def main():
     ap.add_argument("--home-levels", type=int, default=0,
                     help="--home-aware: levels 1..L use same-home forests (0 = the library default for N ranks)")
     ap.add_argument("--gpu-decompose", action=argparse.BooleanOptionalAction, default=True,
-                    help="N > 1: rank 0 decomposes on its GPU (default on)")
+                    help="decompose on the GPU (N = 1: the plan's own decomposition; N > 1: rank 0's; default on)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -384,7 +384,8 @@ def main():
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
                    window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
-                   band=args.band, flags=args.flags, transport=args.transport)
+                   band=args.band, transport=args.transport,
+                   flags=args.flags | (ab.arrow.FLAG_GPU_DECOMPOSE if (args.gpu_decompose and dec is None) else 0))
     info = plan.info()
     lo, hi = plan.local_begin, plan.local_end
     if comm is not None or args.order == "permuted":

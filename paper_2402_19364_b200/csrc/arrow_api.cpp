@@ -452,12 +452,22 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
         const int e = upload_seg_level(hs, (int)es, bs, li == 0 ? 0 : 1, P->n, P->seg_allocs, S, err);
         if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
         P->seg.push_back(S);
-        if (P->det && !hrows.empty()) {  // K-C of this level: CSR (head row -> its slots, in order)
-            std::vector<int32_t> ptr(hstart.begin(), hstart.end()), src((size_t)hstart.back());
-            for (size_t t = 0; t < src.size(); ++t) src[t] = (int32_t)t;
+        if (P->det && !hrows.empty()) {  // K-C of this level: slots -> groups -> head rows, in order
             if (hstart.back() >= ((int64_t)1 << 31)) return fail(ARROW_E_UNSUPPORTED, "too many head-row chunks");
+            std::vector<int32_t> gptr(1, 0), gsrc((size_t)hstart.back()), gdst, ptr(1, 0), src;
+            for (size_t t = 0; t < gsrc.size(); ++t) gsrc[t] = (int32_t)t;
+            for (size_t j = 0; j < hrows.size(); ++j) {
+                for (int64_t a = hstart[j]; a < hstart[j + 1]; a += kDetGroup) {
+                    src.push_back((int32_t)gdst.size());
+                    gdst.push_back((int32_t)gdst.size());
+                    gptr.push_back((int32_t)std::min<int64_t>(a + kDetGroup, hstart[j + 1]));
+                }
+                ptr.push_back((int32_t)src.size());
+            }
             DetLevel &DLv = P->det_levels[li];
             DLv.nh = (int64_t)hrows.size();
+            DLv.ng = (int64_t)gdst.size();
+            P->det_groups = std::max(P->det_groups, DLv.ng);
             auto up = [&](const std::vector<int32_t> &v) -> int32_t * {
                 void *d = nullptr;
                 if (cudaMalloc(&d, std::max<size_t>(v.size() * 4, 16)) != cudaSuccess) return nullptr;
@@ -468,7 +478,11 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
             DLv.ptr = up(ptr);
             DLv.src = up(src);
             DLv.rows = up(hrows);
-            if (!DLv.ptr || !DLv.src || !DLv.rows) return fail(ARROW_E_CUDA, "upload of the head-combine lists failed");
+            DLv.gptr = up(gptr);
+            DLv.gsrc = up(gsrc);
+            DLv.gdst = up(gdst);
+            if (!DLv.ptr || !DLv.src || !DLv.rows || !DLv.gptr || !DLv.gsrc || !DLv.gdst)
+                return fail(ARROW_E_CUDA, "upload of the head-combine lists failed");
         }
     }
     P->n_post = (int64_t)post_rows.size();
@@ -873,7 +887,7 @@ static arrow_status ensure_ws(arrow_plan P, int64_t k) {
         P->ws = nullptr;
         P->ws_k = 0;
     }
-    cudaError_t e = cudaMalloc(&P->ws, (size_t)(P->det_slots * k * (int64_t)P->esize()));
+    cudaError_t e = cudaMalloc(&P->ws, (size_t)((P->det_slots + P->det_groups) * k * (int64_t)P->esize()));
     if (e != cudaSuccess) return fail(ARROW_E_CUDA, std::string("cudaMalloc(head-partial slots): ") + cudaGetErrorString(e));
     P->ws_k = k;
     return ARROW_OK;
@@ -927,7 +941,10 @@ static arrow_status enqueue_rmw(arrow_plan P, const void *X, void *Y, int64_t k,
         if (P->det && P->det_levels[i].nh > 0) {  // S3, K-C: Y[head] += its chunk partials, in chunk order
             const DetLevel &DLv = P->det_levels[i];
             prof_begin(P, st, a);
-            e = launch_gather_add(dt, P->ws, DLv.ptr, DLv.src, DLv.rows, DLv.nh, k, Y, st);
+            char *groups = reinterpret_cast<char *>(P->ws) + (size_t)(P->det_slots * k * (int64_t)P->esize());
+            e = (int)cudaMemsetAsync(groups, 0, (size_t)(DLv.ng * k * (int64_t)P->esize()), st);
+            if (!e) e = launch_gather_add(dt, P->ws, DLv.gptr, DLv.gsrc, DLv.gdst, DLv.ng, k, groups, st);
+            if (!e) e = launch_gather_add(dt, groups, DLv.ptr, DLv.src, DLv.rows, DLv.nh, k, Y, st);
             prof_end(P, st, ARROW_K_HEAD_EPI, a);
             if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-C: ") + cudaGetErrorString((cudaError_t)e)); }
         }

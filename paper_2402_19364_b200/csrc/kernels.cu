@@ -140,7 +140,19 @@ __global__ void __launch_bounds__(256) k_gather_add(const T *__restrict__ src, c
         T *p = dst + (int64_t)__ldg(drow + r) * k + c;
         Frag<T, VEC> a = ld_plain<T, VEC>(p);
         const int e1 = __ldg(ptr + r + 1);
-        for (int e = __ldg(ptr + r); e < e1; ++e) {
+        int e = __ldg(ptr + r);
+        // 8 source rows in flight, added in list order (the order fixes the fp result: deterministic
+        // head combine, fixed-order distributed adds); long lists (hub head rows) are latency-bound
+        for (; e + 8 <= e1; e += 8) {
+            Frag<T, VEC> s[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[u] = ld_plain<T, VEC>(src + (int64_t)__ldg(sidx + e + u) * k + c);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) a.v[q] += s[u].v[q];
+        }
+        for (; e < e1; ++e) {
             const Frag<T, VEC> s = ld_plain<T, VEC>(src + (int64_t)__ldg(sidx + e) * k + c);
 #pragma unroll
             for (int q = 0; q < VEC; ++q) a.v[q] += s.v[q];

@@ -25,10 +25,14 @@ struct ProfRec {
 };
 
 // deterministic mode: K-C of one level (head row r: Y[rows[r]] += slots ptr[r] .. ptr[r+1], in order)
+// deterministic K-C of one level in two fixed-order passes: (1) group g = the sum of up to
+// kDetGroup consecutive slots of one head row, in slot order; (2) Y[head] += its groups, in order
 struct DetLevel {
-    int64_t nh = 0;
-    int32_t *ptr = nullptr, *src = nullptr, *rows = nullptr;
+    int64_t nh = 0, ng = 0;
+    int32_t *gptr = nullptr, *gsrc = nullptr, *gdst = nullptr;  // pass 1: group -> its slots
+    int32_t *ptr = nullptr, *src = nullptr, *rows = nullptr;     // pass 2: head row -> its groups
 };
+constexpr int kDetGroup = 32;
 
 struct DistState;  // dist.cpp
 void dist_free(DistState *d);
@@ -70,7 +74,7 @@ struct arrow_plan_s {
     void *ws = nullptr;            // single GPU, deterministic mode: head-partial slots (det_slots x ws_k)
     int64_t ws_k = 0;
     bool det = false;              // options.flags & ARROW_FLAG_DETERMINISTIC
-    int64_t det_slots = 0;
+    int64_t det_slots = 0, det_groups = 0;  // rows of the slot and group regions of ws
     std::vector<arrow::DetLevel> det_levels;
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
