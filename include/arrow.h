@@ -84,7 +84,8 @@ typedef struct {
     int32_t order;              /* ARROW_ORDER_*; default ORIGINAL.  Distributed mode forces PERMUTED. */
     int32_t residual;           /* ARROW_RESIDUAL_*; default ERROR */
     int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (16384) */
-    int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32) */
+    int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32; 128 with
+                                   ARROW_FLAG_DETERMINISTIC, one slot per segment) */
     int32_t batch_segments;     /* segments per K-A work batch of full-warp rows: 0 = default = 16 (the only
                                    value accepted; short rows are taken 32 at a time) */
     int32_t band;               /* ARROW_BAND_*: step 3's band; default BLOCK */

@@ -512,9 +512,11 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     if (opt.transport < ARROW_TRANSPORT_AUTO || opt.transport > ARROW_TRANSPORT_NCCL)
         return fail(ARROW_E_INVALID_ARG, "bad options.transport");
     const int64_t window_rows = opt.window_rows > 0 ? opt.window_rows : kDefaultWindowRows;
-    // deterministic head partials use the same chunks (one slot each): one chunk per (head row, window)
-    // made a hub's whole window one warp's serial work (config R level 0: 10.7 vs 1.6 ms)
-    const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : kDefaultHeadChunk;
+    // deterministic head partials: one slot per chunk; longer chunks (fewer slots for K-C to add) but
+    // not one chunk per (head row, window), which made a hub's whole window one warp's serial work
+    // (config R level 0: 10.7 vs 1.6 ms)
+    const bool det = (opt.flags & ARROW_FLAG_DETERMINISTIC) && !comm;
+    const int32_t head_chunk = opt.head_chunk > 0 ? opt.head_chunk : det ? kDetHeadChunk : kDefaultHeadChunk;
     const int bs = opt.batch_segments > 0 ? opt.batch_segments : kDefaultBatchSegs;
     const int order = comm ? ARROW_ORDER_PERMUTED : opt.order;
     const int64_t n = D.n, b = D.b;

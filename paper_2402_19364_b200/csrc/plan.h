@@ -33,6 +33,7 @@ struct DetLevel {
     int32_t *ptr = nullptr, *src = nullptr, *rows = nullptr;     // pass 2: head row -> its groups
 };
 constexpr int kDetGroup = 32;
+constexpr int kDetHeadChunk = 128;  // deterministic mode's default head chunk (entries per slot)
 
 struct DistState;  // dist.cpp
 void dist_free(DistState *d);
