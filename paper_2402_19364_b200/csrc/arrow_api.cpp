@@ -394,20 +394,29 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
     // the last launch writing each Y row: 2 * level + (1 if as a head-row partial); a body segment in
     // its row's last launch is final (kFinalBit: arrow_spmm_iterate applies the activation when it is
     // flushed); rows last written by head partials get a post pass
+    // (deterministic mode: every head partial is added by the one K-C pass after the last level)
     std::vector<int32_t> last((size_t)P->n, -1);
     for (size_t li = 0; li < nlv; ++li)
         for (const uint32_t key : built[li].keys)
-            if (key & kPseudoRec) last[key & (kAuxRec - 1)] = (int32_t)(2 * li + ((key & kAuxRec) ? 1 : 0));
+            if (key & kPseudoRec) {
+                const int32_t w = (key & kAuxRec) ? (int32_t)(P->det ? 2 * nlv + 1 : 2 * li + 1) : (int32_t)(2 * li);
+                int32_t &l = last[key & (kAuxRec - 1)];
+                l = std::max(l, w);
+            }
     std::vector<int32_t> post_rows;
     for (int64_t r = 0; r < P->n; ++r)
         if (last[r] >= 0 && (last[r] & 1)) post_rows.push_back((int32_t)r);
-    P->det_levels.resize(nlv);
+    // deterministic head partials (ARROW_FLAG_DETERMINISTIC): chunk c of head row j of level i is
+    // stored into its own slot (level i's slots follow level i-1's); after the last level one K-C pass
+    // adds every row's slots into Y in a fixed order (by level, then chunk) -- addition order is all
+    // determinism needs, so the partials of all levels are combined once instead of per level
+    int64_t slot_base = 0;
+    struct HeadSlots { int32_t row; int64_t a, b; };
+    std::vector<HeadSlots> hslots;
     for (size_t li = 0; li < nlv; ++li) {
         BuiltLevel &B = built[li];
         HostSegs hs;
         hs.ent_val.reserve(B.vals.size());
-        // deterministic head partials (ARROW_FLAG_DETERMINISTIC): chunk c of head row j is stored into
-        // slot hstart[j] + (its ordinal among j's chunks); K-C adds the slots of j in order into Y
         std::vector<int64_t> nchunk, hstart;
         std::vector<int32_t> hrows;
         std::vector<int32_t> hidx;  // row -> head index of this level
@@ -423,10 +432,12 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
                     }
                     ++nchunk[hidx[row]];
                 }
-            hstart.assign(hrows.size() + 1, 0);
+            hstart.assign(hrows.size() + 1, slot_base);
             for (size_t j = 0; j < hrows.size(); ++j) hstart[j + 1] = hstart[j] + nchunk[j];
             std::fill(nchunk.begin(), nchunk.end(), 0);
-            P->det_slots = std::max(P->det_slots, hstart.back());
+            for (size_t j = 0; j < hrows.size(); ++j) hslots.push_back(HeadSlots{hrows[j], hstart[j], hstart[j + 1]});
+            slot_base = hstart.back();
+            if (slot_base >= ((int64_t)1 << 31)) return fail(ARROW_E_UNSUPPORTED, "too many head-row chunks");
         }
         for (size_t r = 0; r < B.keys.size(); ++r) {
             const uint32_t key = B.keys[r];
@@ -452,38 +463,48 @@ static arrow_status build_single_gpu(arrow_plan P, std::vector<BuiltLevel> &buil
         const int e = upload_seg_level(hs, (int)es, bs, li == 0 ? 0 : 1, P->n, P->seg_allocs, S, err);
         if (e) return fail(e == -1 ? ARROW_E_UNSUPPORTED : ARROW_E_CUDA, err);
         P->seg.push_back(S);
-        if (P->det && !hrows.empty()) {  // K-C of this level: slots -> groups -> head rows, in order
-            if (hstart.back() >= ((int64_t)1 << 31)) return fail(ARROW_E_UNSUPPORTED, "too many head-row chunks");
-            std::vector<int32_t> gptr(1, 0), gsrc((size_t)hstart.back()), gdst, ptr(1, 0), src;
-            for (size_t t = 0; t < gsrc.size(); ++t) gsrc[t] = (int32_t)t;
-            for (size_t j = 0; j < hrows.size(); ++j) {
-                for (int64_t a = hstart[j]; a < hstart[j + 1]; a += kDetGroup) {
-                    src.push_back((int32_t)gdst.size());
-                    gdst.push_back((int32_t)gdst.size());
-                    gptr.push_back((int32_t)std::min<int64_t>(a + kDetGroup, hstart[j + 1]));
+    }
+    if (P->det && !hslots.empty()) {  // K-C: slots -> groups of kDetGroup -> head rows, in a fixed order
+        std::stable_sort(hslots.begin(), hslots.end(), [](const HeadSlots &x, const HeadSlots &y) { return x.row < y.row; });
+        std::vector<int32_t> gptr(1, 0), gsrc, gdst, ptr(1, 0), src, rows;
+        gsrc.reserve((size_t)slot_base);
+        for (size_t t = 0; t < hslots.size();) {
+            const int32_t row = hslots[t].row;
+            int32_t in_group = 0;
+            for (; t < hslots.size() && hslots[t].row == row; ++t)
+                for (int64_t sl = hslots[t].a; sl < hslots[t].b; ++sl) {
+                    if (in_group == 0) {
+                        src.push_back((int32_t)gdst.size());
+                        gdst.push_back((int32_t)gdst.size());
+                        gptr.push_back(gptr.back());
+                    }
+                    gsrc.push_back((int32_t)sl);
+                    ++gptr.back();
+                    in_group = (in_group + 1) % kDetGroup;
                 }
-                ptr.push_back((int32_t)src.size());
-            }
-            DetLevel &DLv = P->det_levels[li];
-            DLv.nh = (int64_t)hrows.size();
-            DLv.ng = (int64_t)gdst.size();
-            P->det_groups = std::max(P->det_groups, DLv.ng);
-            auto up = [&](const std::vector<int32_t> &v) -> int32_t * {
-                void *d = nullptr;
-                if (cudaMalloc(&d, std::max<size_t>(v.size() * 4, 16)) != cudaSuccess) return nullptr;
-                P->seg_allocs.push_back(d);
-                if (!v.empty() && cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-                return (int32_t *)d;
-            };
-            DLv.ptr = up(ptr);
-            DLv.src = up(src);
-            DLv.rows = up(hrows);
-            DLv.gptr = up(gptr);
-            DLv.gsrc = up(gsrc);
-            DLv.gdst = up(gdst);
-            if (!DLv.ptr || !DLv.src || !DLv.rows || !DLv.gptr || !DLv.gsrc || !DLv.gdst)
-                return fail(ARROW_E_CUDA, "upload of the head-combine lists failed");
+            rows.push_back(row);
+            ptr.push_back((int32_t)src.size());
         }
+        DetLevel &K = P->det_kc;
+        K.nh = (int64_t)rows.size();
+        K.ng = (int64_t)gdst.size();
+        P->det_slots = slot_base;
+        P->det_groups = K.ng;
+        auto up = [&](const std::vector<int32_t> &v) -> int32_t * {
+            void *d = nullptr;
+            if (cudaMalloc(&d, std::max<size_t>(v.size() * 4, 16)) != cudaSuccess) return nullptr;
+            P->seg_allocs.push_back(d);
+            if (!v.empty() && cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+            return (int32_t *)d;
+        };
+        K.ptr = up(ptr);
+        K.src = up(src);
+        K.rows = up(rows);
+        K.gptr = up(gptr);
+        K.gsrc = up(gsrc);
+        K.gdst = up(gdst);
+        if (!K.ptr || !K.src || !K.rows || !K.gptr || !K.gsrc || !K.gdst)
+            return fail(ARROW_E_CUDA, "upload of the head-combine lists failed");
     }
     P->n_post = (int64_t)post_rows.size();
     if (P->n_post) {
@@ -940,16 +961,17 @@ static arrow_status enqueue_rmw(arrow_plan P, const void *X, void *Y, int64_t k,
                        P->launch, nullptr, act, i == 0 ? L.zero_rows + nh : nullptr, i == 0 ? L.nzero - nh : 0);
         prof_end(P, st, ARROW_K_SEGMENTS, a);
         if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-A: ") + cudaGetErrorString((cudaError_t)e)); }
-        if (P->det && P->det_levels[i].nh > 0) {  // S3, K-C: Y[head] += its chunk partials, in chunk order
-            const DetLevel &DLv = P->det_levels[i];
-            prof_begin(P, st, a);
-            char *groups = reinterpret_cast<char *>(P->ws) + (size_t)(P->det_slots * k * (int64_t)P->esize());
-            e = (int)cudaMemsetAsync(groups, 0, (size_t)(DLv.ng * k * (int64_t)P->esize()), st);
-            if (!e) e = launch_gather_add(dt, P->ws, DLv.gptr, DLv.gsrc, DLv.gdst, DLv.ng, k, groups, st);
-            if (!e) e = launch_gather_add(dt, groups, DLv.ptr, DLv.src, DLv.rows, DLv.nh, k, Y, st);
-            prof_end(P, st, ARROW_K_HEAD_EPI, a);
-            if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-C: ") + cudaGetErrorString((cudaError_t)e)); }
-        }
+    }
+    if (P->det && P->det_kc.nh > 0) {  // S3, K-C: Y[head] += its chunk partials of every level, in order
+        const DetLevel &K = P->det_kc;
+        cudaEvent_t a = nullptr;
+        prof_begin(P, st, a);
+        char *groups = reinterpret_cast<char *>(P->ws) + (size_t)(P->det_slots * k * (int64_t)P->esize());
+        int e = (int)cudaMemsetAsync(groups, 0, (size_t)(K.ng * k * (int64_t)P->esize()), st);
+        if (!e) e = launch_gather_add(dt, P->ws, K.gptr, K.gsrc, K.gdst, K.ng, k, groups, st);
+        if (!e) e = launch_gather_add(dt, groups, K.ptr, K.src, K.rows, K.nh, k, Y, st);
+        prof_end(P, st, ARROW_K_HEAD_EPI, a);
+        if (e) { P->poisoned = true; return fail(ARROW_E_CUDA, std::string("K-C: ") + cudaGetErrorString((cudaError_t)e)); }
     }
     if (act && P->n_post) {  // iterate mode: rows last written by head-row partials
         const int e = launch_act_rows(dt, P->post_rows, P->n_post, k, act, Y, st);

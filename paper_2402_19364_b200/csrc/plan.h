@@ -25,7 +25,7 @@ struct ProfRec {
 };
 
 // deterministic mode: K-C of one level (head row r: Y[rows[r]] += slots ptr[r] .. ptr[r+1], in order)
-// deterministic K-C of one level in two fixed-order passes: (1) group g = the sum of up to
+// deterministic K-C in two fixed-order passes over the head partials of every level: (1) group g = the sum of up to
 // kDetGroup consecutive slots of one head row, in slot order; (2) Y[head] += its groups, in order
 struct DetLevel {
     int64_t nh = 0, ng = 0;
@@ -76,7 +76,7 @@ struct arrow_plan_s {
     int64_t ws_k = 0;
     bool det = false;              // options.flags & ARROW_FLAG_DETERMINISTIC
     int64_t det_slots = 0, det_groups = 0;  // rows of the slot and group regions of ws
-    std::vector<arrow::DetLevel> det_levels;
+    arrow::DetLevel det_kc;  // deterministic mode: the one K-C pass over every level's head partials
     void *host_x = nullptr, *host_y = nullptr;  // device staging for arrow_spmm_host
     int64_t host_k = 0;
     // arrow_spmm_host_batch: two device slots, two copy streams, per-slot events
