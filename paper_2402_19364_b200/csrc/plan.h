@@ -24,9 +24,9 @@ struct ProfRec {
     cudaEvent_t a, b;
 };
 
-// deterministic mode: K-C of one level (head row r: Y[rows[r]] += slots ptr[r] .. ptr[r+1], in order)
-// deterministic K-C in two fixed-order passes over the head partials of every level: (1) group g = the sum of up to
-// kDetGroup consecutive slots of one head row, in slot order; (2) Y[head] += its groups, in order
+// deterministic mode's K-C, two fixed-order passes over the head partials of every level: (1) group g
+// = the sum of up to kDetGroup consecutive slots of one head row (slots by level, then chunk);
+// (2) Y[rows[r]] += the groups of head row r, in order
 struct DetLevel {
     int64_t nh = 0, ng = 0;
     int32_t *gptr = nullptr, *gsrc = nullptr, *gdst = nullptr;  // pass 1: group -> its slots
