@@ -266,10 +266,11 @@ def test_graph_replay_on_a_stream():
             assert np.array_equal(Y.cpu().numpy(), oracle.spmm(g.n, g.row_ptr, g.col, g.val, X)), (k, r)
 
 
-@pytest.mark.parametrize("order", ["original", "permuted"])
-def test_iterate_relu(order):
+@pytest.mark.parametrize("order,flags", [("original", 0), ("permuted", 0), ("original", 2)])
+def test_iterate_relu(order, flags):
     """NEXT-1: X_{t+1} = relu(A X_t) with the activation fused into K-A, against the oracle applied
-    step by step (fp64; one iteration is exact on dyadic data, more within 1e-12)."""
+    step by step (fp64; one iteration is exact on dyadic data, more within 1e-12); flags = 2: the
+    deterministic mode, whose head partials land after the last level (activation after K-C)."""
     g = datagen.rmat(13, 8, 7)
     rng = np.random.default_rng(5)
     # signed values so that ReLU is not the identity: a(u,v) -> +-a(u,v), symmetric
@@ -278,7 +279,7 @@ def test_iterate_relu(order):
     S.data = S.data * sign
     S = S.tocsr()
     S.sort_indices()
-    plan = ab.Plan(g.n, S.indptr, S.indices, S.data, 128, dtype="f64", order=order)
+    plan = ab.Plan(g.n, S.indptr, S.indices, S.data, 128, dtype="f64", order=order, flags=flags)
     perm0 = plan.export_level(0)[0] if order == "permuted" else np.arange(g.n)
     k = 16
     X0 = datagen.make_x(g.n, k) - 0.5
