@@ -15,19 +15,21 @@
 // one contiguous send and one contiguous receive per peer; a rank's own rows never leave the GPU
 // (packed straight into its halo, added straight from its staging buffer).
 //
-// Per arrow_spmm call (compute stream S = the caller's, communication stream C):
-//   S: one row-mover launch: D0 rows (owners copy X, others zero), C0 = 0, X rows packed for the
-//      peers and for this rank's own halo; zero Y rows no K-A launch writes                 -> e0
-//   C: all-reduce D0 of level 0 -> e1; grouped send/recv of the forward rows + all-reduce of the
-//      other levels' D0 -> e2                            (Alg. 1 line 1, Alg. 2 forward propagation)
+// Per arrow_spmm call, NCCL transport (compute stream S = the caller's, communication stream C):
+//   S: one row-mover launch: my owned head rows into D0, C0 = 0, X rows packed for the peers and
+//      for this rank's own halo (and the strict-band H0 rows); zero Y rows no K-A launch writes -> e0
+//   C: Alg. 1 line 1, Broadcast(D^(0)): one ncclBroadcast per owner of level 0's head block (+ the
+//      strict-band H0 send/recv) -> e1; grouped send/recv of the forward rows + the broadcasts of
+//      the other levels' head blocks -> e2                 (Alg. 2 forward propagation)
 //   S: wait e1; K-A level 0 (overlaps the forward exchange); wait e2; K-A levels >= 1 into the
 //      peer-major staging buffer -> e3
-//   C: wait e3; grouped send/recv of the staging rows to their homes + all-reduce of every C0
-//      -> e4                                             (Alg. 1 line 3, Alg. 2 reverse aggregation)
+//   C: wait e3; grouped send/recv of the staging rows to their homes + Alg. 1 line 3, Reduce(C^(0)):
+//      one ncclReduce per owner of each head block -> e4    (Alg. 2 reverse aggregation)
 //   S: add this rank's own staging rows (overlaps the reverse exchange); wait e4; add received
 //      rows and owned head partials -- both as CSR gather-adds, contributions in level order.
-// K-A leaves ARROW_DIST_RESERVE_SMS (default 16) SMs' worth of blocks out so that the NCCL kernels
-// can run next to it.
+// K-A leaves a few SMs' worth of blocks out (DistState::reserve_sms) so that the NCCL kernels can
+// run next to it.  The P2P transport (dist_spmm_p2p) replaces the collectives by stores into the
+// peers' memory and flag barriers.
 #include <nccl.h>
 
 #include <algorithm>
