@@ -266,7 +266,7 @@ arrow_status arrow_decompose_ex(const arrow_csr *A, int64_t b, int32_t levels, u
  * order finds the forest Kruskal finds), the same smallest-first tree layout (Euler-tour list ranking
  * in place of the host's DFS).  A is read from HOST memory and the result lives on the host like
  * arrow_decompose's; device scratch is allocated and freed inside the call (the default stream,
- * synchronous).  Errors as arrow_decompose_ex, plus: n >= 2^31 - 1 or nnz >= 2^31 - 1 ->
+ * synchronous).  Errors as arrow_decompose_ex, plus: n >= 2^30 or nnz >= 2^31 - 1 ->
  * ARROW_E_INVALID_ARG; no device, allocation or launch failure -> ARROW_E_CUDA. */
 arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, uint64_t seed, int32_t keep_residual,
                                  int32_t band, arrow_decomposition *out);

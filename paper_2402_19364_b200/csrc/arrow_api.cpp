@@ -244,7 +244,7 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         D->band = band;
         HostDecomposition H;
         if (on_gpu) {
-            if (n >= ((int64_t)1 << 31) - 1 || A->nnz >= ((int64_t)1 << 31) - 1)  // CUB item counts are int
+            if (n >= ((int64_t)1 << 30) || A->nnz >= ((int64_t)1 << 31) - 1)  // CUB item counts (2 n arcs) are int
                 return fail(ARROW_E_INVALID_ARG, "GPU decomposer: n or nnz beyond 32-bit indices");
             if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, home_levels, H, err))
                 return fail(ARROW_E_CUDA, err);

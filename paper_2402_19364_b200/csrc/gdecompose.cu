@@ -408,7 +408,7 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
     out.home_levels = homes > 1 ? home_levels : 0;
     const int64_t nnz = rp[n];
     if (nnz == 0) return 0;
-    if (n >= ((int64_t)1 << 31) - 1 || nnz >= ((int64_t)1 << 31) - 1) {  // CUB item counts are int
+    if (n >= ((int64_t)1 << 30) || nnz >= ((int64_t)1 << 31) - 1) {  // CUB item counts (2 n arcs) are int
         err = "GPU decomposer: n or nnz beyond 32-bit indices";
         return 1;
     }
