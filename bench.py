@@ -484,20 +484,24 @@ def main():
                "h2d_bytes_per_step": int(Xl.nbytes) * world, "d2h_bytes_per_step": int(Xl.nbytes) * world,
                "ms_per_step": round(float(te.item()) * 1e3, 3),
                "mode": "arrow_spmm_host per step (H2D, kernels, D2H, sync)"}
-        if world == 1:
-            # the batched host entry: H2D of step c+1 and D2H of step c-1 overlap the kernels of c
-            # (arrow_spmm_host_batch); every step still copies its X in and its Y out
-            Yh2 = torch.empty_like(Xh).pin_memory().numpy()
-            nb = max(args.e2e_steps, 4)
-            Xs, Ys = [Xh_np] * nb, [Yh_np if c % 2 == 0 else Yh2 for c in range(nb)]
-            plan.spmm_host_batch(Xs[:2], Ys[:2], stream.cuda_stream)  # warm (allocates the slots)
-            t0 = time.perf_counter()
-            plan.spmm_host_batch(Xs, Ys, stream.cuda_stream)
-            tb = (time.perf_counter() - t0) / nb
-            e2e.update({"value": round(flop / tb / 1e9, 3), "ms_per_step": round(tb * 1e3, 3),
-                        "mode": f"arrow_spmm_host_batch of {nb} steps (copies pipelined with the kernels)",
-                        "sequential": {"value": e2e["value"], "ms_per_step": e2e["ms_per_step"],
-                                       "mode": e2e["mode"]}})
+        # the batched host entry: H2D of step c+1 and D2H of step c-1 overlap the kernels of c
+        # (arrow_spmm_host_batch; collective for N > 1); every step still copies its X in and its Y out
+        Yh2 = torch.empty_like(Xh).pin_memory().numpy()
+        nb = max(args.e2e_steps, 4)
+        Xs, Ys = [Xh_np] * nb, [Yh_np if c % 2 == 0 else Yh2 for c in range(nb)]
+        plan.spmm_host_batch(Xs[:2], Ys[:2], stream.cuda_stream)  # warm (allocates the slots)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        plan.spmm_host_batch(Xs, Ys, stream.cuda_stream)
+        tbt = torch.tensor([(time.perf_counter() - t0) / nb], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tbt, op=dist.ReduceOp.MAX)
+        tb = float(tbt.item())
+        e2e.update({"value": round(flop / tb / 1e9, 3), "ms_per_step": round(tb * 1e3, 3),
+                    "mode": f"arrow_spmm_host_batch of {nb} steps (copies pipelined with the kernels)",
+                    "sequential": {"value": e2e["value"], "ms_per_step": e2e["ms_per_step"],
+                                   "mode": e2e["mode"]}})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

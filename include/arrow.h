@@ -162,11 +162,12 @@ arrow_status arrow_spmm_host(arrow_plan plan, const void *X_host, void *Y_host, 
 
 /* Batched end-to-end call: Y_host[c] = A X_host[c] for c = 0..count-1, each an n x k HOST buffer
  * of the plan's dtype (pinned memory needed for the overlap), e.g. several feature matrices
- * multiplied by the same A (preprocessing amortised over many products).  Single-GPU plans
- * pipeline the copies with the kernels through two device slots owned by the plan: the H2D copy
- * of X[c+1] and the D2H copy of Y[c-1] run on two copy streams while the kernels of c run on
- * `stream` (PCIe is full duplex).  Distributed plans run the items one by one (arrow_spmm_host).
- * Synchronises `stream` before returning.  count < 0 or a NULL pointer: ARROW_E_INVALID_ARG. */
+ * multiplied by the same A (preprocessing amortised over many products).  The copies are
+ * pipelined with the kernels through two device slots owned by the plan: the H2D copy of X[c+1]
+ * and the D2H copy of Y[c-1] run on two copy streams while the kernels of c run on `stream` (PCIe
+ * is full duplex).  Distributed plans: every rank passes its local rows (n_local x k) and the same
+ * count (collective, like arrow_spmm).  Synchronises `stream` before returning.  count < 0 or a
+ * NULL pointer: ARROW_E_INVALID_ARG. */
 arrow_status arrow_spmm_host_batch(arrow_plan plan, const void *const *X_host, void *const *Y_host,
                                    int64_t count, int64_t k, void *stream);
 

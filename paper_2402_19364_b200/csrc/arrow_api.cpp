@@ -1129,7 +1129,7 @@ arrow_status arrow_spmm_host_batch(arrow_plan P, const void *const *Xh, void *co
     for (int64_t c = 0; c < count; ++c)
         if (!Xh[c] || !Yh[c]) return fail(ARROW_E_INVALID_ARG, "X or Y is NULL");
     if (P->poisoned) return fail(ARROW_E_STATE, "plan poisoned by an earlier CUDA error");
-    if (P->dist || count == 1) {
+    if (count == 1) {
         for (int64_t c = 0; c < count; ++c) {
             const arrow_status s = arrow_spmm_host(P, Xh[c], Yh[c], k, stream);
             if (s != ARROW_OK) return s;
