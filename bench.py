@@ -351,6 +351,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     k, dtype = args.k or cfg["k"], args.dtype or cfg["dtype"]
     es = 8 if dtype == "f64" else 4
+    # tile window of the layout: ~8 MB of X rows (16,384 rows at 512-byte rows, up to 65,536 rows for
+    # rows of 128 bytes or less; swept in profiles/r02/win/: k=32 -4.7 %, k=8 -8.3 % vs 16,384)
+    window_rows = args.window_rows or 16384 * max(1, min(4, 512 // (k * es)))
     g, X = make_inputs(cfg, k, dtype)
 
     comm = None
@@ -383,7 +386,7 @@ def main():
     home_levels_used = dec.home_levels() if dec is not None else 0
     plan = ab.Plan(g.n, g.row_ptr, g.col, g.val, cfg["b"], dtype=dtype, comm=comm, decomposition=dec,
                    order=("permuted" if comm is not None else args.order),
-                   window_rows=args.window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
+                   window_rows=window_rows, head_chunk=args.head_chunk, batch_segments=args.batch_segments,
                    band=args.band, transport=args.transport,
                    flags=args.flags | (ab.arrow.FLAG_GPU_DECOMPOSE if (args.gpu_decompose and dec is None) else 0))
     info = plan.info()
@@ -559,7 +562,7 @@ def main():
             "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}",
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
-                       "band": args.band,
+                       "band": args.band, "window_rows": window_rows,
                        "arrangement": ("home-aware (R25) for %d ranks, levels 1..%d" % (world, home_levels_used))
                                       if (args.home_aware and world > 1)
                                       else "random spanning forest, smallest-first (R6-R12)",
