@@ -351,9 +351,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     k, dtype = args.k or cfg["k"], args.dtype or cfg["dtype"]
     es = 8 if dtype == "f64" else 4
-    # tile window of the layout: ~8 MB of X rows (16,384 rows at 512-byte rows, up to 65,536 rows for
-    # rows of 128 bytes or less; swept in profiles/r02/win/: k=32 -4.7 %, k=8 -8.3 % vs 16,384)
-    window_rows = args.window_rows or 16384 * max(1, min(4, 512 // (k * es)))
+    # tile window of the layout (profiles/r02/win/): the library default for 512-byte rows (level 0
+    # 65,536 rows, levels >= 1 16,384); ~8 MB of X rows for shorter rows (k=32: 65,536 rows, -4.7 %)
+    window_rows = args.window_rows or (0 if k * es >= 512 else 16384 * min(4, 512 // (k * es)))
     g, X = make_inputs(cfg, k, dtype)
 
     comm = None
@@ -562,7 +562,8 @@ def main():
             "config": {"workload": f"config {args.config}: {cfg['graph']} b={cfg['b']} k={k}",
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
-                       "band": args.band, "window_rows": window_rows,
+                       "band": args.band,
+                       "window_rows": window_rows or ("default: level 0 65536, levels >= 1 16384" if world == 1 else 16384),
                        "arrangement": ("home-aware (R25) for %d ranks, levels 1..%d" % (world, home_levels_used))
                                       if (args.home_aware and world > 1)
                                       else "random spanning forest, smallest-first (R6-R12)",

@@ -570,8 +570,12 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
             pos0p = &pos0;
         }
         built.resize(D.levels.size() + (D.res_u.empty() ? 0 : 1));
+        // default window: level 0 (store-only, gather-bound) runs faster with a larger window, the
+        // read-modify-write levels with 16,384 rows (profiles/r02/win/)
         for (size_t i = 0; i < D.levels.size(); ++i)
-            build_level(D.levels[i], (int)i, b, window_rows, head_chunk, pos0p, pdt, comm ? 1 : 0, built[i]);
+            build_level(D.levels[i], (int)i, b,
+                        (i == 0 && opt.window_rows == 0) ? std::max(window_rows, kDefaultLevel0WindowRows) : window_rows,
+                        head_chunk, pos0p, pdt, comm ? 1 : 0, built[i]);
         if (!D.res_u.empty()) build_residual(D, pos0p, pdt, built.back());
         P->residual_nnz = (int64_t)D.res_u.size();
         P->arrow_levels = (int32_t)D.levels.size();
