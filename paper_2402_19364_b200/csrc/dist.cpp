@@ -202,8 +202,8 @@ void build_csr(const std::vector<std::pair<int32_t, int32_t>> &c, std::vector<in
 
 }  // namespace
 
-arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_t window_rows, int32_t head_chunk,
-                           size_t es, int p2p, DistHost &H) {
+arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_t window_rows, int64_t window_rows0,
+                           int32_t head_chunk, size_t es, int p2p, DistHost &H) {
     if (!D.res_u.empty()) return set_error(ARROW_E_UNSUPPORTED, "distributed mode does not support a residual level");
     if (G < 1 || me < 0 || me >= G) return set_error(ARROW_E_INVALID_ARG, "bad nranks/rank");
     if (p2p && G > kMaxPeers) return set_error(ARROW_E_UNSUPPORTED, "P2P transport supports at most 8 ranks");
@@ -576,7 +576,7 @@ arrow_status dist_schedule(const arrow_decomposition_s &D, int G, int me, int64_
             if (es == 8) std::memcpy(DL.segs.ent_val.data() + at, &v, 8);
             else { const float f = (float)v; std::memcpy(DL.segs.ent_val.data() + at, &f, 4); }
         };
-        const int64_t W = std::max<int64_t>(1, window_rows / b) * b;
+        const int64_t W = std::max<int64_t>(1, (i == 0 ? window_rows0 : window_rows) / b) * b;
         for (int64_t lo_w = qa; lo_w < qb; lo_w += W) {
             const int64_t hi_w = std::min(qb, lo_w + W);
             for (int64_t p = std::max(h, lo_w); p < hi_w; ++p) {
@@ -695,7 +695,7 @@ void dist_free(DistState *d) {
 
 
 arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm comm, int64_t window_rows,
-                        int32_t head_chunk, int bs) {
+                        int64_t window_rows0, int32_t head_chunk, int bs) {
     auto *S = new DistState();
     P->dist = S;
     S->comm = (ncclComm_t)comm->comm;
@@ -731,7 +731,7 @@ arrow_status dist_build(arrow_plan P, const arrow_decomposition_s &D, arrow_comm
     if (S->flags) S->allocs.push_back(S->flags);
 
     DistHost H;
-    arrow_status st = dist_schedule(D, S->G, S->me, window_rows, head_chunk, P->esize(), S->p2p, H);
+    arrow_status st = dist_schedule(D, S->G, S->me, window_rows, window_rows0, head_chunk, P->esize(), S->p2p, H);
     if (st != ARROW_OK) return st;
     S->lo = H.lo;
     S->hi = H.hi;
@@ -1163,8 +1163,10 @@ extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nrank
     if (nranks < 1 || nranks > arrow::kMaxPeers || rank < 0 || rank >= nranks)
         return arrow::set_error(ARROW_E_INVALID_ARG, "nranks must be in [1, 8] and rank in [0, nranks)");
     arrow::DistHost H;
-    arrow_status st = arrow::dist_schedule(*d, nranks, rank, window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
-                                           head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, 0, H);
+    arrow_status st = arrow::dist_schedule(
+        *d, nranks, rank, window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
+        window_rows > 0 ? window_rows : arrow::kDefaultLevel0WindowRows,
+        head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, 0, H);
     if (st != ARROW_OK) return st;
     lohi[0] = H.lo;
     lohi[1] = H.hi;

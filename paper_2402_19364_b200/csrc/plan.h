@@ -15,7 +15,7 @@ namespace arrow {
 arrow_status set_error(arrow_status s, const std::string &msg);  // thread-local detail (arrow_last_error)
 
 constexpr int64_t kDefaultWindowRows = 16384;
-constexpr int64_t kDefaultLevel0WindowRows = 65536;  // single GPU, default window: level 0 (profiles/r02/win)
+constexpr int64_t kDefaultLevel0WindowRows = 65536;  // default window of level 0 (profiles/r02/win)
 constexpr int32_t kDefaultHeadChunk = 32;  // measured best at config R (k = 8, 32, 128): sweep in DESIGN.md §7
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
