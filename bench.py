@@ -563,7 +563,7 @@ def main():
                        "n": g.n, "nnz": g.nnz, "k": k, "b": cfg["b"], "levels": info["levels"],
                        "sum_n_i": info["sum_rows"], "parallelism": f"arrow tiles over {world} GPU(s)",
                        "band": args.band,
-                       "window_rows": window_rows or "default: level 0 65536, levels >= 1 16384",
+                       "window_rows": window_rows or ("default: level 0 65536, levels >= 1 16384" if world == 1 else 16384),
                        "arrangement": ("home-aware (R25) for %d ranks, levels 1..%d" % (world, home_levels_used))
                                       if (args.home_aware and world > 1)
                                       else "random spanning forest, smallest-first (R6-R12)",

@@ -83,9 +83,9 @@ typedef struct {
     uint64_t seed;              /* s_decomp of the random spanning forests (R9); default 4 */
     int32_t order;              /* ARROW_ORDER_*; default ORIGINAL.  Distributed mode forces PERMUTED. */
     int32_t residual;           /* ARROW_RESIDUAL_*; default ERROR */
-    int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (65536 for
-                                   level 0, 16384 for levels >= 1); rows of <= 128 bytes run faster with
-                                   65536 everywhere */
+    int64_t window_rows;        /* tile-window (rows) ordering the work for L2 reuse; 0 = default (single GPU:
+                                   65536 for level 0, 16384 for levels >= 1; distributed: 16384); rows of
+                                   <= 128 bytes run faster with 65536 everywhere */
     int32_t head_chunk;         /* max entries per head-row work segment; 0 = default (32; 128 with
                                    ARROW_FLAG_DETERMINISTIC, one slot per segment) */
     int32_t batch_segments;     /* segments per K-A work batch of full-warp rows: 0 = default = 16 (the only

@@ -624,9 +624,9 @@ static arrow_status plan_from(const arrow_decomposition_s &D, const arrow_option
     P->local_end = n;
     if (comm) {
         P->comm = comm;
-        arrow_status cs = dist_build(P.get(), D, comm, window_rows,
-                                     opt.window_rows == 0 ? std::max(window_rows, kDefaultLevel0WindowRows) : window_rows,
-                                     head_chunk, bs);
+        // level 0 keeps 16,384-row windows here: a rank's level-0 range is 1/G of the rows, and 65,536
+        // measured +1 % at G = 4 (profiles/r02/win_dist/)
+        arrow_status cs = dist_build(P.get(), D, comm, window_rows, window_rows, head_chunk, bs);
         if (cs != ARROW_OK) return cs;
     }
     P->create_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

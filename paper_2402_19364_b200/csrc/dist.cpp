@@ -1165,7 +1165,7 @@ extern "C" arrow_status arrow_dist_schedule(arrow_decomposition d, int32_t nrank
     arrow::DistHost H;
     arrow_status st = arrow::dist_schedule(
         *d, nranks, rank, window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
-        window_rows > 0 ? window_rows : arrow::kDefaultLevel0WindowRows,
+        window_rows > 0 ? window_rows : arrow::kDefaultWindowRows,
         head_chunk > 0 ? head_chunk : arrow::kDefaultHeadChunk, 8, 0, H);
     if (st != ARROW_OK) return st;
     lohi[0] = H.lo;
