@@ -234,7 +234,8 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
     std::string err;
     const int64_t n = A->n;
     if (validate_csr(n, A->nnz, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_BAD_CSR, err);
-    if (check_symmetric(n, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_NOT_SYMMETRIC, err);
+    // the GPU decomposer checks the symmetry itself (on the device)
+    if (!on_gpu && check_symmetric(n, A->row_ptr, A->col_idx, err)) return fail(ARROW_E_NOT_SYMMETRIC, err);
     const auto t1 = std::chrono::steady_clock::now();
     try {
         D.reset(new arrow_decomposition_s());
@@ -246,8 +247,8 @@ static arrow_status decompose_impl(const arrow_csr *A, int64_t b, int32_t levels
         if (on_gpu) {
             if (n >= ((int64_t)1 << 30) || A->nnz >= ((int64_t)1 << 31) - 1)  // CUB item counts (2 n arcs) are int
                 return fail(ARROW_E_INVALID_ARG, "GPU decomposer: n or nnz beyond 32-bit indices");
-            if (la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, home_levels, H, err))
-                return fail(ARROW_E_CUDA, err);
+            const int ge = la_decompose_gpu(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, home_levels, H, err);
+            if (ge) return fail(ge == 2 ? ARROW_E_NOT_SYMMETRIC : ARROW_E_CUDA, err);
         } else if (la_decompose(n, A->row_ptr, A->col_idx, b, levels, seed, band, homes, home_levels, H, err)) {
             return fail(ARROW_E_INVALID_ARG, err);
         }

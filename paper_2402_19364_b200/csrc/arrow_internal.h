@@ -47,7 +47,8 @@ std::vector<int64_t> home_ranges(const HostLevel &L0, int64_t n, int64_t b, int 
 
 // LA-Decompose on the current CUDA device (gdecompose.cu): the same output as
 // la_decompose, bit for bit (same rules and keys; Boruvka + Euler-tour list ranking in place of the
-// sequential Kruskal / BFS / DFS).  n < 2^30, nnz < 2^31 - 1.  0 on success, else sets `err`.
+// sequential Kruskal / BFS / DFS).  n < 2^30, nnz < 2^31 - 1.  Checks the pattern's symmetry on the
+// device (2 if it is not).  0 on success, else sets `err` (1: CUDA failure).
 int la_decompose_gpu(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t b, int32_t max_levels,
                      uint64_t seed, int band, int homes, int home_levels, HostDecomposition &out,
                      std::string &err);

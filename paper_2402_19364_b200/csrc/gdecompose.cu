@@ -81,6 +81,21 @@ __global__ void k_rows_of_entries(const int64_t *rp, int64_t n, int32_t *erow) {
     GRID_LOOP(r, n) for (int64_t e = rp[r]; e < rp[r + 1]; ++e) erow[e] = (int32_t)r;
 }
 __global__ void k_iota(uint32_t *a, int64_t m) { GRID_LOOP(t, m) a[t] = (uint32_t)t; }
+// symmetric pattern: entry (r, c) needs (c, r) -- a binary search in row c (rows sorted, validated);
+// the smallest offending row lands in *bad
+__global__ void k_check_symmetric(const int64_t *rp, const int32_t *col, const int32_t *erow, int64_t nnz,
+                                  unsigned long long *bad) {
+    GRID_LOOP(e, nnz) {
+        const int32_t r = erow[e], c = col[e];
+        int64_t lo = rp[c], hi = rp[c + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col[mid] < r) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo == rp[c + 1] || col[lo] != r) atomicMin(bad, (unsigned long long)r);
+    }
+}
 __global__ void k_degree(const uint32_t *ent, int64_t m, const int32_t *erow, int32_t *deg) {
     GRID_LOOP(t, m) atomicAdd(&deg[erow[ent[t]]], 1);
 }
@@ -439,6 +454,18 @@ int la_decompose_gpu(int64_t n, const int64_t *rp, const int32_t *col_h, int64_t
     GD_TRY(cudaMemcpy(d_rp.p, rp, (n + 1) * 8, cudaMemcpyHostToDevice));
     GD_TRY(cudaMemcpy(d_col.p, col_h, nnz * 4, cudaMemcpyHostToDevice));
     k_rows_of_entries<<<blocks_for(n), 256>>>(d_rp.p, n, d_erow.p);
+    {  // the pattern must be symmetric (what the host path's check_symmetric tests, here on the device)
+        Buf<unsigned long long> bad;
+        GD_TRY(bad.need(1));
+        GD_TRY(cudaMemset(bad.p, 0xff, 8));
+        k_check_symmetric<<<blocks_for(nnz), 256>>>(d_rp.p, d_col.p, d_erow.p, nnz, bad.p);
+        unsigned long long hb = 0;
+        GD_TRY(cudaMemcpy(&hb, bad.p, 8, cudaMemcpyDeviceToHost));
+        if (hb != ~0ull) {
+            err = "pattern not symmetric at row " + std::to_string(hb);
+            return 2;
+        }
+    }
     GD_TRY(d_ent.need(nnz));
     k_iota<<<blocks_for(nnz), 256>>>(d_ent.p, nnz);
     GD_TRY(d_flags.need(4));

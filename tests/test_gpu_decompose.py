@@ -100,6 +100,11 @@ def test_gpu_decomposer_degenerate():
     _same(Dg, Dh)
     with pytest.raises(ArrowError):
         ab.Decomposition(4, rp, col, np.ones(2), 1, device="cuda")
+    # the symmetry check runs on the device: (0, 2) without (2, 0)
+    with pytest.raises(ArrowError) as e:
+        ab.Decomposition(3, np.array([0, 2, 3, 3], np.int64), np.array([1, 2, 0], np.int32), np.ones(3), 2,
+                         device="cuda")
+    assert e.value.code == "ARROW_E_NOT_SYMMETRIC"
 
 
 @pytest.mark.parametrize("inst", GOLD["instances"], ids=lambda g: g["graph"])
