@@ -253,7 +253,8 @@ arrow_status arrow_plan_kernel_times(arrow_plan plan, arrow_kernel_times_t *out)
 /* ---------------------------------------------------------------- host decomposition object
  * The preprocessing half of arrow_plan_create, exposed so that a decomposition can be computed
  * once, checked, saved and shared (every rank of a distributed run can load the same file).
- * Host only: no CUDA device is needed for these calls. */
+ * Host only -- no CUDA device is needed -- except arrow_decompose_gpu and arrow_decompose_homes with
+ * device = 1, which compute on the current device (the result still lives on the host). */
 
 /* LA-Decompose of A (same algorithm and readings as arrow_plan_create).  keep_residual != 0
  * keeps entries left at the `levels` cap instead of failing with ARROW_E_LEVELS. */
@@ -276,9 +277,9 @@ arrow_status arrow_decompose_gpu(const arrow_csr *A, int64_t b, int32_t levels, 
 /* The general form: homes = G in [1, 8] lays levels >= 1 out for G ranks (reading
  * R25 of DESIGN.md §3; an extension, not in the paper): after level 0 every vertex gets the home range
  * of its pi_0 position -- G contiguous ranges of whole level-0 tiles balanced by level-0 work plus
- * every vertex's entries left for levels >= 1 -- and the trees of every level >= 1 are laid out by
- * (home of the root, size desc, min id asc) instead of (size desc, min id asc) for the levels
- * 1..home_levels (>= 1; their forests use only the edges inside one home), so a distributed plan for G
+ * every vertex's entries left for levels >= 1 -- and in the levels 1..home_levels the forest uses only
+ * the edges inside one home and its trees are laid out by (home of the root, size desc, min id asc)
+ * instead of (size desc, min id asc), so a distributed plan for G
  * ranks computes those levels' home-g trees on rank g and moves few of their rows over NVLink; edges
  * between homes wait for a later level, so more home-aware levels mean more levels and rows
  * (DESIGN.md §8 measures the trade); home_levels = 0 picks the default (1 for homes = 2, else 3).
