@@ -569,9 +569,11 @@ def main():
                                       else "random spanning forest, smallest-first (R6-R12)",
                        "order": "permuted (pi_0)" if (comm is not None or args.order == "permuted") else "original",
                        "l2": "inputs larger than L2 (X, Y %.2f GiB each), no flush" % (Xl.nbytes / 2**30)},
+            # whole-job algorithmic bytes over the step against the N GPUs' aggregate HBM bandwidth
             "hbm_roofline": {"bytes_alg_per_step": b_alg, "achieved_GBs": round(b_alg / (ms_per_step * 1e-3) / 1e9, 1),
-                             "frac_of_measured": round(b_alg / (ms_per_step * 1e-3) / 1e9 / peak, 4),
-                             "frac_of_8TBs": round(b_alg / (ms_per_step * 1e-3) / 8e12, 4)},
+                             "frac_of_measured": round(b_alg / (ms_per_step * 1e-3) / 1e9 / (peak * world), 4),
+                             "frac_of_8TBs": round(b_alg / (ms_per_step * 1e-3) / (8e12 * world), 4),
+                             "gpus": world},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "K-A (k_ka for full-warp rows, k_segsmall for short rows, else k_segments)",
