@@ -554,7 +554,8 @@ def main():
         lib = cusparse_baseline(g, Xd, k, flop, stream)
 
     if rank == 0:
-        traffic = load_traffic(args.config, k, dtype) if args.band == "block" else None
+        # ncu DRAM bytes of the single-GPU K-A launches (profiles/traffic.json); none measured for N > 1
+        traffic = load_traffic(args.config, k, dtype) if (args.band == "block" and world == 1) else None
         line = {
             "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
