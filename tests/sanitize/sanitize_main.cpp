@@ -85,6 +85,30 @@ int main(int argc, char **argv) {
         CHECK(ps == ARROW_E_CUDA && p == nullptr, "plan without a device");
         arrow_decomposition_destroy(d);
     }
+    // home-set-aware levels (R25): decomposition, its homes, schedules for the homes' rank count (the
+    // aligned path) and another one, save/load of format 3
+    for (int homes : {2, 4}) {
+        arrow_decomposition h = nullptr;
+        CHECK(arrow_decompose_homes(&A, b, 0, 4, 0, 0, homes, 2, 0, &h) == ARROW_OK, "decompose_homes");
+        int32_t hg = 0, hl = 0, lv = 0;
+        std::vector<int64_t> ranges((size_t)homes + 1);
+        CHECK(arrow_decomposition_homes(h, -1, &hg, &hl, ranges.data()) == ARROW_OK && hg == homes && hl == 2, "homes");
+        CHECK(arrow_decomposition_info(h, nullptr, nullptr, &lv, nullptr) == ARROW_OK, "info");
+        if (lv > 1) CHECK(arrow_decomposition_homes(h, 1, nullptr, nullptr, ranges.data()) == ARROW_OK, "home starts");
+        for (int G : {homes, 3}) {
+            std::vector<int64_t> counts((size_t)std::max(lv, 1) * (4 * G + 4) + 8);
+            for (int r = 0; r < G; ++r) {
+                int64_t lohi[2] = {0, 0};
+                CHECK(arrow_dist_schedule(h, G, r, 0, 0, lohi, counts.data()) == ARROW_OK, "dist_schedule homes");
+            }
+        }
+        const std::string path = tmp + "/h" + std::to_string(homes) + ".dec";
+        CHECK(arrow_decomposition_save(h, path.c_str()) == ARROW_OK, "save homes");
+        arrow_decomposition h2 = nullptr;
+        CHECK(arrow_decomposition_load(path.c_str(), &h2) == ARROW_OK, "load homes");
+        arrow_decomposition_destroy(h2);
+        arrow_decomposition_destroy(h);
+    }
     // level cap with residual, and the error paths of the argument validation
     arrow_decomposition d = nullptr;
     CHECK(arrow_decompose(&A, b, 1, 4, 1, &d) == ARROW_OK, "capped decomposition");
