@@ -40,7 +40,9 @@ def main():
         dec = ab.Decomposition(g.n, g.row_ptr, g.col, g.val, b)
         t_dec = time.time() - t0
         for k in [int(x) for x in args.ks.split(",")]:
-            plan = ab.Plan(decomposition=dec, dtype="f32")
+            # the bench's window choice: library default at 512-byte rows, ~8 MB of rows below
+            win = 0 if k * 4 >= 512 else 16384 * min(4, 512 // (k * 4))
+            plan = ab.Plan(decomposition=dec, dtype="f32", window_rows=win)
             X = datagen.make_x(g.n, k, dtype=np.float32)
             Xd = torch.from_numpy(X).to(dev)
             Yd = torch.empty_like(Xd)
