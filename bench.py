@@ -351,10 +351,13 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     k, dtype = args.k or cfg["k"], args.dtype or cfg["dtype"]
     es = 8 if dtype == "f64" else 4
-    # tile window of the layout (profiles/r02/win/): the library default for 512-byte rows (level 0
-    # 65,536 rows, levels >= 1 16,384); ~8 MB of X rows for shorter rows (k=32: 65,536 rows, -4.7 %)
-    window_rows = args.window_rows or (0 if k * es >= 512 else 16384 * min(4, 512 // (k * es)))
     g, X = make_inputs(cfg, k, dtype)
+    # tile window of the layout (profiles/r02/win/, S2/): the library default for 512-byte rows (level 0
+    # 65,536 rows, levels >= 1 16,384); for shorter rows up to ~8 MB of X rows but at most n/64 rows
+    # (config R k=32: 65,536 rows, -4.7 %; RMAT scale 20 was 14-19 % slower with 65,536)
+    n_cfg = g.n
+    window_rows = args.window_rows or (0 if k * es >= 512 else
+                                       min(16384 * min(4, 512 // (k * es)), max(16384, n_cfg // 64)))
 
     comm = None
     if world > 1:

@@ -41,7 +41,7 @@ def main():
         t_dec = time.time() - t0
         for k in [int(x) for x in args.ks.split(",")]:
             # the bench's window choice: library default at 512-byte rows, ~8 MB of rows below
-            win = 0 if k * 4 >= 512 else 16384 * min(4, 512 // (k * 4))
+            win = 0 if k * 4 >= 512 else min(16384 * min(4, 512 // (k * 4)), max(16384, g.n // 64))
             plan = ab.Plan(decomposition=dec, dtype="f32", window_rows=win)
             X = datagen.make_x(g.n, k, dtype=np.float32)
             Xd = torch.from_numpy(X).to(dev)
