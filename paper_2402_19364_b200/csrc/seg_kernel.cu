@@ -213,7 +213,7 @@ __device__ __forceinline__ void ka_group(const int32_t *__restrict__ ent_col, co
 // A warp takes one work batch of (up to) 16 segments at a time (measured: 16 better than 32 at
 // k = 128); a batch starts at a multiple of 8 entries and usually ends inside a group of 8.
 template <typename T, int VEC, int MODE, int DIST>
-__global__ void __launch_bounds__(256, (sizeof(T) == 8 || DIST) ? 3 : 4) k_ka(const int32_t *__restrict__ seg_out,
+__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 3 : 4) k_ka(const int32_t *__restrict__ seg_out,
                                                const uint32_t *__restrict__ seg_end, int64_t nseg,
                                                const int32_t *__restrict__ ent_col, const T *__restrict__ ent_val,
                                                const uint8_t *__restrict__ gmask, const uint2 *__restrict__ bat,
